@@ -93,7 +93,10 @@ def jacobi_eigh(A, tol=1e-15, max_sweeps=100):
                 if abs(apq) <= 1e-300:
                     continue
                 tau = (A[q, q] - A[p, p]) / (2.0 * apq)
-                t = (1.0 if tau >= 0 else -1.0) / (abs(tau) + math.sqrt(1.0 + tau * tau))
+                if abs(tau) > 1e150:          # tau^2 would overflow: t -> 1/(2 tau)
+                    t = 1.0 / (2.0 * tau)
+                else:
+                    t = (1.0 if tau >= 0 else -1.0) / (abs(tau) + math.sqrt(1.0 + tau * tau))
                 c = 1.0 / math.sqrt(1.0 + t * t)
                 s = t * c
                 # A <- J^T A J with J = [[c, s], [-s, c]] in the (p, q) plane
