@@ -1,0 +1,210 @@
+/*
+ * gft.h — C ABI of the B200-native fast graph Fourier transform library.
+ *
+ * Method: Lu & Ortega, "Fast Graph Fourier Transforms Based on Graph Symmetry and
+ * Bipartition", arXiv 1907.07875 (cited as PAPER.md:<line>, LaTeX labels in brackets).
+ *
+ * The GFT of a graph signal x on a fixed graph G is y = U^T x, where U holds the
+ * eigenvectors of the (unnormalised) Laplacian L = D - W + S ordered by ascending
+ * eigenvalue [eq:def_laplacian, PAPER.md:113-127, 136-139].  gft_plan_create() finds
+ * graph symmetries (involutions phi, [def:graph_sym] PAPER.md:444-448), factors U into
+ * stages of Haar butterflies followed by block-diagonal dense sub-GFTs
+ * ([eq:B_phi] PAPER.md:459-469, [thm:decompose] PAPER.md:484-499, recursion PAPER.md:564),
+ * solves the small sub-Laplacians once on the host in double precision, and generates
+ * sm_100a kernels that apply every butterfly stage and every dense block in one HBM pass
+ * per signal tile.  gft_forward()/gft_inverse() run those kernels on a caller stream.
+ *
+ * Conventions (all functions):
+ *   - Node ids are 0-based.  Signals are row-major [batch, n], contiguous, one signal per
+ *     row.  Coefficient k of row b is <u_k, x_b> with u_k the k-th eigenvector in
+ *     ascending-eigenvalue order (stable by leaf emission order inside ties).
+ *   - Simple eigenvalues: u_k has the canonical sign "first entry with |u_i| > 1e-8 is
+ *     positive".  Repeated eigenvalues: the basis inside the eigenspace is the plan's own
+ *      and is exported by gft_plan_basis().
+ *   - Every function returns a gft_status; none aborts or exits.  On failure a
+ *     thread-local message is available from gft_last_error().
+ *   - Pointers passed in are only read during the call (nothing is retained) unless
+ *     stated.  Device pointers are CUDA device addresses on the current device.
+ */
+#ifndef GFT_H_
+#define GFT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GFT_ABI_VERSION 1
+#if defined(__GNUC__)
+#define GFT_API __attribute__((visibility("default")))
+#else
+#define GFT_API
+#endif
+#define GFT_MAX_LEVELS 64
+
+typedef struct gft_plan_s* gft_plan;      /* opaque, library-owned, immutable after create */
+typedef void* gft_stream;                  /* a cudaStream_t (NULL = legacy default stream) */
+
+typedef enum { GFT_F32 = 0, GFT_F64 = 1 } gft_dtype;
+
+typedef enum {
+  GFT_OK = 0,
+  GFT_ERR_INVALID_ARG = 1,     /* bad size, index out of range, self-edge, duplicate pair, NaN/Inf */
+  GFT_ERR_NOT_INVOLUTION = 2,  /* phi given but phi(phi(i)) != i or not a permutation */
+  GFT_ERR_NOT_SYMMETRIC = 3,   /* phi given but the graph is not phi-symmetric (Definition 2) */
+  GFT_ERR_EIG_NOCONVERGE = 4,  /* host Jacobi did not converge / realised basis failed self-check */
+  GFT_ERR_ALIGNMENT = 5,       /* X or Y not 16-byte aligned */
+  GFT_ERR_UNSUPPORTED = 6,     /* dtype not prepared in this plan, n too large for codegen */
+  GFT_ERR_CUDA = 7,            /* CUDA driver/runtime error (detail in gft_last_error) */
+  GFT_ERR_NOMEM = 8,
+  GFT_ERR_COMPILE = 9,         /* kernel code generation / NVRTC compilation failed */
+  GFT_ERR_NO_DEVICE = 10       /* no CUDA device available for a device call */
+} gft_status;
+
+/* Plan options.  gft_plan_opts_default() fills the defaults given in brackets. */
+typedef struct {
+  int32_t max_depth;      /* max butterfly levels; <0 = unlimited [-1] ("until a
+                             symmetry property cannot be found anymore") */
+  int32_t min_leaf;       /* sub-graphs with <= min_leaf nodes are not searched further [1] */
+  int64_t search_budget;  /* backtracking extensions per involution search [1000000] */
+  double sym_rtol;        /* relative tolerance of the Definition-2 check of a USER phi [1e-12];
+                             sub-graph searches use max(sym_rtol, 1e-10) since Theorem-4
+                             weights carry rounding */
+  uint32_t dtypes;        /* bitmask (1u<<GFT_F32)|(1u<<GFT_F64) of kernels to generate [both] */
+  uint32_t flags;         /* GFT_FLAG_* below [0] */
+} gft_plan_opts;
+
+#define GFT_FLAG_HOST_ONLY 1u      /* build the factorisation only; no kernel codegen (CPU use) */
+#define GFT_FLAG_NO_CUBIN_CACHE 2u /* always run NVRTC even if an AOT cubin for the plan exists */
+
+typedef struct {
+  int32_t n;
+  int32_t depth;                          /* number of butterfly levels D */
+  int32_t n_units;                        /* total Haar units over all levels */
+  int32_t units_per_level[GFT_MAX_LEVELS];
+  int32_t n_leaves;                       /* dense sub-GFT blocks */
+  int32_t max_leaf;                       /* largest leaf size */
+  int32_t n_scale_fix;                    /* explicit sqrt(2)^m multiplies (unequal partner scales) */
+  int32_t n_vz_total;                     /* V_Z pass-through nodes summed over all decompositions */
+  int64_t sum_k2;                         /* sum over leaves of k^2 (leaf multiplies) */
+  int64_t adds;                           /* 2*n_units + sum k(k-1) (adds incl. subtractions) */
+  int64_t mults;                          /* sum k^2 + n_scale_fix (sqrt2 folded into leaves) */
+  int64_t paper_mults;                    /* sum k^2 + n_vz_total: tab:runtime convention (A-23) */
+  int64_t dense_adds;                     /* n(n-1) */
+  int64_t dense_mults;                    /* n^2 */
+  int32_t n_clusters;                     /* eigenvalue clusters (tol 1e-9*max(1,lambda_max)) */
+  int32_t kernels_ready;                  /* bitmask of dtypes with compiled kernels */
+  double residual;                        /* max |L U_f - U_f Lambda| of the realised basis */
+  double orth_error;                      /* max |U_f^T U_f - I| */
+} gft_plan_info;
+
+/* ---- plan lifecycle -------------------------------------------------------------- */
+
+GFT_API void gft_plan_opts_default(gft_plan_opts* opts);
+
+/* Build a plan for the graph with n nodes, n_edges undirected edges (src[e], dst[e], w[e])
+ * and optional self-loops s[n] (NULL = none) [eq:def_laplacian PAPER.md:113-124].
+ * An edge may be given as (i,j) or (j,i); i == j is rejected (self-loops go in
+ * self_loops); a repeated unordered pair is rejected; w == 0 edges are dropped;
+ * non-finite values are rejected; negative weights are accepted.
+ * phi (NULL = auto-detect) is an optional top-level involution [Def. 1-2,
+ * PAPER.md:440-448]; it must be an involution (else GFT_ERR_NOT_INVOLUTION) and the
+ * graph must be phi-symmetric within opts->sym_rtol (else GFT_ERR_NOT_SYMMETRIC).
+ * opts NULL = defaults.  On success *out owns host tables, the generated kernels and
+ * device tables; release with gft_plan_destroy().  Kernel generation needs no GPU;
+ * module loading happens on first device use. */
+GFT_API gft_status gft_plan_create(gft_plan* out, int32_t n, int64_t n_edges,
+                           const int32_t* src, const int32_t* dst, const double* w,
+                           const double* self_loops, const int32_t* phi,
+                           const gft_plan_opts* opts);
+
+GFT_API gft_status gft_plan_destroy(gft_plan plan);   /* caller must have synchronised its streams */
+
+/* ---- hot path (device memory, asynchronous on `stream`) ----------------------------- */
+
+/* Y[b,:] = U^T X[b,:] for b < batch using the fused fast kernel (butterflies + dense
+ * leaves + ascending-eigenvalue output order, one pass).  X, Y: device, row-major
+ * [batch, n], 16-byte aligned; X == Y (in place) allowed, other overlap undefined.
+ * batch == 0 returns GFT_OK without a launch.  No host synchronisation, no allocation. */
+GFT_API gft_status gft_forward(gft_plan plan, const void* X, void* Y, int64_t batch,
+                       gft_dtype dtype, gft_stream stream);
+
+/* X[b,:] = U Y[b,:] (exact transpose of gft_forward; B_phi^T = B_phi). */
+GFT_API gft_status gft_inverse(gft_plan plan, const void* Y, void* X, int64_t batch,
+                       gft_dtype dtype, gft_stream stream);
+
+/* In-run comparison: the plain dense "matrix GFT" Y = X U with the
+ * plan's realised basis U_f, same I/O layout and staging as gft_forward. */
+GFT_API gft_status gft_dense_forward(gft_plan plan, const void* X, void* Y, int64_t batch,
+                             gft_dtype dtype, gft_stream stream);
+GFT_API gft_status gft_dense_inverse(gft_plan plan, const void* Y, void* X, int64_t batch,
+                             gft_dtype dtype, gft_stream stream);
+
+/* End-to-end variant with HOST buffers: copies X_host -> device, runs the fast transform,
+ * copies the result back to Y_host, chunked and double-buffered over two plan-owned
+ * streams so that H2D, compute and D2H overlap.  `workspace` is a device buffer of
+ * `workspace_bytes` >= 2 * chunk_rows * n * sizeof(dtype) (chunk_rows > 0).  Work is
+ * ordered after prior work on `stream` and `stream` is made to wait for completion;
+ * host buffers must stay valid until `stream` completes (use pinned memory for overlap).
+ * direction: 0 = forward, 1 = inverse. */
+GFT_API gft_status gft_execute_host(gft_plan plan, int32_t direction, const void* in_host,
+                            void* out_host, int64_t batch, gft_dtype dtype,
+                            void* workspace, size_t workspace_bytes, int64_t chunk_rows,
+                            gft_stream stream);
+
+/* Compile (NVRTC, or load from the AOT cubin cache built by build()) all four kernels of
+ * `dtype` now instead of at first launch.  Needs no GPU. */
+GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype);
+
+/* ---- introspection (host) ------------------------------------------------------------ */
+
+GFT_API gft_status gft_plan_info_get(gft_plan plan, gft_plan_info* info);
+/* ascending eigenvalues, lambda[n] */
+GFT_API gft_status gft_plan_eigenvalues(gft_plan plan, double* lambda);
+/* realised basis, row-major U[i*n+k] = u_k(i) (node i, coefficient k) */
+GFT_API gft_status gft_plan_basis(gft_plan plan, double* U);
+/* leaf sizes in emission order; *count = number of leaves (sizes written up to cap) */
+GFT_API gft_status gft_plan_leaf_sizes(gft_plan plan, int32_t* sizes, int32_t cap, int32_t* count);
+/* Generated CUDA source for (kind 0 fast-fwd, 1 fast-inv, 2 dense-fwd, 3 dense-inv) and
+ * dtype; writes up to cap bytes (NUL-terminated) and the full length to *len. */
+GFT_API gft_status gft_plan_kernel_source(gft_plan plan, int32_t kind, gft_dtype dtype,
+                                  char* buf, size_t cap, size_t* len);
+/* Symbol name of a generated kernel (as shown by ncu / cuobjdump). */
+GFT_API gft_status gft_plan_kernel_name(gft_plan plan, int32_t kind, gft_dtype dtype, char* buf, size_t cap);
+/* Launch geometry of a kernel kind: grid, block, dynamic smem bytes, registers/thread. */
+GFT_API gft_status gft_plan_launch_config(gft_plan plan, int32_t kind, gft_dtype dtype,
+                                  int64_t batch, int32_t* grid, int32_t* block,
+                                  int32_t* smem_bytes, int32_t* regs);
+
+/* ---- building blocks of the decomposition (host, double) ------------------------------ */
+
+/* Dense Laplacian L[n*n] (row-major) [eq:l_from_sw PAPER.md:122-123], same input rules
+ * as gft_plan_create. */
+GFT_API gft_status gft_laplacian(int32_t n, int64_t n_edges, const int32_t* src, const int32_t* dst,
+                         const double* w, const double* self_loops, double* L);
+
+/* Theorem 4 [thm:decompose PAPER.md:484-499]: given a phi-symmetric graph as a Laplacian
+ * L[n*n] and an involution phi, write the Laplacians of G+ (order: V_X ascending, then
+ * V_Z ascending; size n-p) into Lplus[(n-p)^2] and of G- (order: phi(V_X); size p) into
+ * Lminus[p^2]; *p_out = p_phi [eq:p_phi].  V_X = smaller index of each pair (A-6). */
+GFT_API gft_status gft_decompose(int32_t n, const double* L, const int32_t* phi, double sym_rtol,
+                         double* Lplus, double* Lminus, int32_t* p_out);
+
+/* Involution search: the involution phi maximising p_phi (ties: the
+ * lexicographically smallest phi) such that the graph with Laplacian L is phi-symmetric
+ * within rtol; identity if none.  *p_out = p_phi; *complete = 1 if the search finished
+ * within budget (else the best found so far is returned). */
+GFT_API gft_status gft_find_involution(int32_t n, const double* L, double rtol, int64_t budget,
+                               int32_t* phi, int32_t* p_out, int32_t* complete);
+
+/* ---- errors ------------------------------------------------------------------------- */
+GFT_API const char* gft_status_str(gft_status s);
+GFT_API const char* gft_last_error(void);              /* thread-local detail of the last failure */
+GFT_API int32_t gft_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GFT_H_ */

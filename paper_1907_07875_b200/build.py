@@ -1,0 +1,158 @@
+"""Build the C-ABI library (and the AOT cubin cache of the BASELINE configs).
+
+  python -m paper_1907_07875_b200.build            # libgft.so + AOT cubins
+  python -m paper_1907_07875_b200.build --no-aot   # library only
+
+The library (host planner + codegen + driver runtime) is compiled with g++ and has no
+link-time dependency on libcuda / libnvrtc (both are dlopen-ed), so it loads on a
+CPU-only host.  The AOT step generates the plan-specialised kernels of the BASELINE
+configurations through the library itself and compiles each with
+`nvcc -cubin -gencode arch=compute_100a,code=sm_100a -lineinfo`, storing them under
+_lib/kernels/<kernel-name>.cubin where the runtime finds them before falling back to
+NVRTC.  The kernel name embeds a hash of the full generated source, so a stale cubin
+can never be picked up for a different plan.
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import os
+import subprocess
+import sys
+import tempfile
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIBDIR = os.path.join(HERE, "_lib")
+LIB = os.path.join(LIBDIR, "libgft.so")
+KDIR = os.path.join(LIBDIR, "kernels")
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+SOURCES = ["plan.cpp", "search.cpp", "codegen.cpp", "cuda_rt.cpp", "capi.cpp"]
+ARCH = "-gencode=arch=compute_100a,code=sm_100a"
+
+
+def _write_skeleton_inc():
+    with open(os.path.join(CSRC, "kernel_skeleton.cuh")) as f:
+        text = f.read()
+    assert ")GFTSKEL\"" not in text
+    out = os.path.join(CSRC, "skeleton_inc.h")
+    new = 'R"GFTSKEL(' + text + ')GFTSKEL"\n'
+    if not os.path.exists(out) or open(out).read() != new:
+        with open(out, "w") as f:
+            f.write(new)
+
+
+def _stamp():
+    h = hashlib.sha256()
+    for s in SOURCES + ["plan.hpp", "kernels.hpp", "kernel_skeleton.cuh"]:
+        with open(os.path.join(CSRC, s), "rb") as f:
+            h.update(f.read())
+    with open(os.path.join(ROOT, "include", "gft.h"), "rb") as f:
+        h.update(f.read())
+    return h.hexdigest()
+
+
+def build_library(force=False, verbose=True):
+    os.makedirs(LIBDIR, exist_ok=True)
+    _write_skeleton_inc()
+    stamp = _stamp()
+    stamp_file = LIB + ".stamp"
+    if not force and os.path.exists(LIB) and os.path.exists(stamp_file) and open(stamp_file).read() == stamp:
+        return LIB
+    objs = []
+    with tempfile.TemporaryDirectory() as td:
+        procs = []
+        for s in SOURCES:
+            o = os.path.join(td, s + ".o")
+            cmd = ["g++", "-std=c++17", "-O2", "-g", "-fPIC", "-Wall", "-Wno-unused-function",
+                   "-fvisibility=hidden", "-I", os.path.join(CUDA_HOME, "include"),
+                   "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, s), "-o", o]
+            procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
+            objs.append(o)
+        for cmd, p in procs:
+            out = p.communicate()[0].decode()
+            if p.returncode != 0:
+                raise RuntimeError("compile failed: " + " ".join(cmd) + "\n" + out)
+            if verbose and out.strip():
+                print(out)
+        tmp = LIB + ".tmp"
+        cmd = ["g++", "-shared", "-o", tmp] + objs + ["-ldl", "-lpthread"]
+        subprocess.check_call(cmd)
+        os.replace(tmp, LIB)
+    with open(stamp_file, "w") as f:
+        f.write(stamp)
+    if verbose:
+        print("built", LIB)
+    return LIB
+
+
+def aot_kernel_specs():
+    """(config name, dtype list, plan kwargs) of the kernels shipped as AOT cubins."""
+    import workloads
+    specs = []
+    for name in ("cfg1", "cfg2", "cfg2b", "cfg3", "cfg4", "cfg5a", "cfg5b"):
+        cfg = workloads.config(name)
+        depths = [cfg.max_depth] + ([1] if name == "cfg1" else [])
+        for md in depths:
+            specs.append((cfg, list(cfg.dtypes), md))
+    return specs
+
+
+def build_aot_cubins(jobs=8, verbose=True):
+    """Generate the BASELINE configs' kernels via the library and nvcc-compile them."""
+    sys.path.insert(0, ROOT)
+    from paper_1907_07875_b200 import gft as G
+    os.makedirs(KDIR, exist_ok=True)
+    todo = {}
+    for cfg, dtypes, md in aot_kernel_specs():
+        for dt in dtypes:
+            plan = G.Plan(cfg.n, cfg.src, cfg.dst, cfg.w, cfg.self_loops, cfg.phi, max_depth=md,
+                          dtypes=(dt,))
+            for kind in range(4):
+                name = plan.kernel_name(kind, dt)
+                if name not in todo:
+                    todo[name] = plan.kernel_source(kind, dt)
+    nvcc = os.path.join(CUDA_HOME, "bin", "nvcc")
+    pending = [(n, s) for n, s in todo.items() if not os.path.exists(os.path.join(KDIR, n + ".cubin"))]
+    with tempfile.TemporaryDirectory() as td:
+        procs = []
+        for name, src in pending:
+            cu = os.path.join(td, name + ".cu")
+            with open(cu, "w") as f:
+                f.write(src)
+            out = os.path.join(KDIR, name + ".cubin")
+            cmd = [nvcc, "-cubin", ARCH, "-lineinfo", "-O3", "-std=c++17", "-o", out + ".tmp", cu]
+            procs.append((name, out, cmd))
+        running = []
+        while procs or running:
+            while procs and len(running) < jobs:
+                name, out, cmd = procs.pop()
+                running.append((name, out, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                                                 stderr=subprocess.STDOUT)))
+            name, out, cmd, p = running.pop(0)
+            o = p.communicate()[0].decode()
+            if p.returncode != 0:
+                raise RuntimeError("nvcc failed for %s:\n%s" % (name, o[-4000:]))
+            os.replace(out + ".tmp", out)
+    # prune cubins that no longer correspond to a generated kernel
+    for f in os.listdir(KDIR):
+        if f.endswith(".cubin") and f[:-6] not in todo:
+            os.remove(os.path.join(KDIR, f))
+    if verbose:
+        print("AOT cubins: %d (%d compiled now) in %s" % (len(todo), len(pending), KDIR))
+    return sorted(todo)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--no-aot", action="store_true")
+    a = ap.parse_args(argv)
+    build_library(force=a.force)
+    if not a.no_aot:
+        build_aot_cubins()
+
+
+if __name__ == "__main__":
+    main()

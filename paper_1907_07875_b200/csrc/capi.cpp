@@ -1,0 +1,318 @@
+// capi.cpp — the extern "C" boundary declared in include/gft.h.
+// Every entry point converts internal exceptions into a gft_status and a thread-local
+// message; nothing aborts.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "../../include/gft.h"
+#include "kernels.hpp"
+#include "plan.hpp"
+
+struct gft_plan_s {
+  gft::Plan P;
+  uint32_t dtypes = 0;
+  uint32_t flags = 0;
+  std::unique_ptr<gft::Kernel> k[2][gft::K_NUM];
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+gft_status guard(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return GFT_OK;
+  } catch (const gft::Error& e) {
+    g_last_error = e.msg;
+    return (gft_status)e.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return GFT_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return GFT_ERR_INVALID_ARG;
+  } catch (...) {
+    g_last_error = "unknown internal error";
+    return GFT_ERR_INVALID_ARG;
+  }
+}
+
+gft::Kernel& kernel_of(gft_plan plan, int kind, gft_dtype dtype) {
+  if (!plan) gft::fail(GFT_ERR_INVALID_ARG, "NULL plan");
+  if (dtype != GFT_F32 && dtype != GFT_F64) gft::fail(GFT_ERR_UNSUPPORTED, "unsupported dtype");
+  if (kind < 0 || kind >= gft::K_NUM) gft::fail(GFT_ERR_INVALID_ARG, "bad kernel kind");
+  auto& k = plan->k[dtype][kind];
+  if (!k) gft::fail(GFT_ERR_UNSUPPORTED, "dtype not prepared in this plan (opts.dtypes / HOST_ONLY)");
+  return *k;
+}
+
+void check_io(const void* a, const void* b) {
+  if (!a || !b) gft::fail(GFT_ERR_INVALID_ARG, "NULL signal pointer");
+  if ((reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
+    gft::fail(GFT_ERR_ALIGNMENT, "X and Y must be 16-byte aligned");
+}
+
+gft_status run(gft_plan plan, int kind, const void* in, void* out, int64_t batch, gft_dtype dtype,
+               gft_stream stream) {
+  return guard([&] {
+    gft::Kernel& k = kernel_of(plan, kind, dtype);
+    if (batch < 0) gft::fail(GFT_ERR_INVALID_ARG, "batch < 0");
+    if (batch == 0) return;
+    check_io(in, out);
+    gft::launch_kernel(k, in, out, batch, stream, !(plan->flags & GFT_FLAG_NO_CUBIN_CACHE));
+  });
+}
+}  // namespace
+
+extern "C" {
+
+void gft_plan_opts_default(gft_plan_opts* o) {
+  if (!o) return;
+  o->max_depth = -1;
+  o->min_leaf = 1;
+  o->search_budget = 1000000;
+  o->sym_rtol = 1e-12;
+  o->dtypes = (1u << GFT_F32) | (1u << GFT_F64);
+  o->flags = 0;
+}
+
+gft_status gft_plan_create(gft_plan* out, int32_t n, int64_t n_edges, const int32_t* src,
+                           const int32_t* dst, const double* w, const double* self_loops,
+                           const int32_t* phi, const gft_plan_opts* opts) {
+  return guard([&] {
+    if (!out) gft::fail(GFT_ERR_INVALID_ARG, "NULL out");
+    *out = nullptr;
+    gft_plan_opts o;
+    gft_plan_opts_default(&o);
+    if (opts) o = *opts;
+    if (!(o.sym_rtol >= 0) || !std::isfinite(o.sym_rtol)) gft::fail(GFT_ERR_INVALID_ARG, "bad sym_rtol");
+    if (o.search_budget <= 0) gft::fail(GFT_ERR_INVALID_ARG, "search_budget must be > 0");
+    if (o.dtypes & ~3u) gft::fail(GFT_ERR_UNSUPPORTED, "unknown dtype bits");
+    gft::PlanOptions po;
+    po.max_depth = o.max_depth;
+    po.min_leaf = o.min_leaf < 1 ? 1 : o.min_leaf;
+    po.search_budget = o.search_budget;
+    po.sym_rtol = o.sym_rtol;
+    gft::SubGraph g = gft::graph_from_edges(n, n_edges, src, dst, w, self_loops);
+    std::unique_ptr<gft_plan_s> p(new gft_plan_s);
+    p->P = gft::build_plan(g, phi, po);
+    p->flags = o.flags;
+    if (!(o.flags & GFT_FLAG_HOST_ONLY)) {
+      if (n > 256) gft::fail(GFT_ERR_UNSUPPORTED, "kernel generation supports n <= 256 (use HOST_ONLY)");
+      p->dtypes = o.dtypes;
+      for (int dt = 0; dt < 2; ++dt) {
+        if (!(o.dtypes & (1u << dt))) continue;
+        for (int kind = 0; kind < gft::K_NUM; ++kind) {
+          p->k[dt][kind].reset(new gft::Kernel);
+          gft::generate_kernel(p->P, kind, dt, *p->k[dt][kind]);
+        }
+      }
+    }
+    *out = p.release();
+  });
+}
+
+gft_status gft_plan_destroy(gft_plan plan) {
+  return guard([&] {
+    if (!plan) return;
+    for (auto& row : plan->k)
+      for (auto& k : row)
+        if (k) gft::unload_kernel(*k);
+    delete plan;
+  });
+}
+
+gft_status gft_forward(gft_plan plan, const void* X, void* Y, int64_t batch, gft_dtype dtype,
+                       gft_stream stream) {
+  return run(plan, gft::K_FAST_FWD, X, Y, batch, dtype, stream);
+}
+gft_status gft_inverse(gft_plan plan, const void* Y, void* X, int64_t batch, gft_dtype dtype,
+                       gft_stream stream) {
+  return run(plan, gft::K_FAST_INV, Y, X, batch, dtype, stream);
+}
+gft_status gft_dense_forward(gft_plan plan, const void* X, void* Y, int64_t batch, gft_dtype dtype,
+                             gft_stream stream) {
+  return run(plan, gft::K_DENSE_FWD, X, Y, batch, dtype, stream);
+}
+gft_status gft_dense_inverse(gft_plan plan, const void* Y, void* X, int64_t batch, gft_dtype dtype,
+                             gft_stream stream) {
+  return run(plan, gft::K_DENSE_INV, Y, X, batch, dtype, stream);
+}
+
+gft_status gft_execute_host(gft_plan plan, int32_t direction, const void* in_host, void* out_host,
+                            int64_t batch, gft_dtype dtype, void* workspace, size_t workspace_bytes,
+                            int64_t chunk_rows, gft_stream stream) {
+  return guard([&] {
+    if (direction != 0 && direction != 1) gft::fail(GFT_ERR_INVALID_ARG, "direction must be 0 or 1");
+    gft::Kernel& k = kernel_of(plan, direction == 0 ? gft::K_FAST_FWD : gft::K_FAST_INV, dtype);
+    if (batch < 0) gft::fail(GFT_ERR_INVALID_ARG, "batch < 0");
+    if (batch == 0) return;
+    if (!in_host || !out_host) gft::fail(GFT_ERR_INVALID_ARG, "NULL host pointer");
+    gft::execute_host(k, in_host, out_host, batch, workspace, workspace_bytes, chunk_rows, stream,
+                      !(plan->flags & GFT_FLAG_NO_CUBIN_CACHE));
+  });
+}
+
+gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype) {
+  return guard([&] {
+    for (int kind = 0; kind < gft::K_NUM; ++kind)
+      gft::compile_kernel(kernel_of(plan, kind, dtype), !(plan->flags & GFT_FLAG_NO_CUBIN_CACHE));
+  });
+}
+
+gft_status gft_plan_info_get(gft_plan plan, gft_plan_info* info) {
+  return guard([&] {
+    if (!plan || !info) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
+    const gft::Plan& P = plan->P;
+    std::memset(info, 0, sizeof *info);
+    info->n = P.n;
+    info->depth = P.depth;
+    info->n_units = P.n_units;
+    for (int l = 0; l < P.depth && l < GFT_MAX_LEVELS; ++l) info->units_per_level[l] = P.units_per_level[l];
+    info->n_leaves = (int32_t)P.leaves.size();
+    info->max_leaf = P.max_leaf;
+    info->n_scale_fix = P.n_fix;
+    info->n_vz_total = P.n_vz_total;
+    info->sum_k2 = P.sum_k2;
+    info->adds = 2 * (int64_t)P.n_units + P.sum_kk1;
+    info->mults = P.sum_k2 + P.n_fix;
+    info->paper_mults = P.sum_k2 + P.n_vz_total;
+    info->dense_adds = (int64_t)P.n * (P.n - 1);
+    info->dense_mults = (int64_t)P.n * P.n;
+    info->n_clusters = P.n_clusters;
+    uint32_t ready = 0;
+    for (int dt = 0; dt < 2; ++dt) {
+      bool all = true;
+      for (int kind = 0; kind < gft::K_NUM; ++kind)
+        all = all && plan->k[dt][kind] && !plan->k[dt][kind]->cubin.empty();
+      if (all) ready |= 1u << dt;
+    }
+    info->kernels_ready = (int32_t)ready;
+    info->residual = P.residual;
+    info->orth_error = P.orth_error;
+  });
+}
+
+gft_status gft_plan_eigenvalues(gft_plan plan, double* lambda) {
+  return guard([&] {
+    if (!plan || !lambda) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
+    std::memcpy(lambda, plan->P.lambda.data(), sizeof(double) * plan->P.n);
+  });
+}
+
+gft_status gft_plan_basis(gft_plan plan, double* U) {
+  return guard([&] {
+    if (!plan || !U) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
+    std::memcpy(U, plan->P.U.data(), sizeof(double) * plan->P.U.size());
+  });
+}
+
+gft_status gft_plan_leaf_sizes(gft_plan plan, int32_t* sizes, int32_t cap, int32_t* count) {
+  return guard([&] {
+    if (!plan) gft::fail(GFT_ERR_INVALID_ARG, "NULL plan");
+    const auto& L = plan->P.leaves;
+    if (count) *count = (int32_t)L.size();
+    for (int32_t i = 0; sizes && i < cap && i < (int32_t)L.size(); ++i) sizes[i] = L[i].k;
+  });
+}
+
+gft_status gft_plan_kernel_source(gft_plan plan, int32_t kind, gft_dtype dtype, char* buf, size_t cap,
+                                  size_t* len) {
+  return guard([&] {
+    gft::Kernel& k = kernel_of(plan, kind, dtype);
+    if (len) *len = k.source.size();
+    if (buf && cap) {
+      size_t m = std::min(cap - 1, k.source.size());
+      std::memcpy(buf, k.source.data(), m);
+      buf[m] = 0;
+    }
+  });
+}
+
+gft_status gft_plan_kernel_name(gft_plan plan, int32_t kind, gft_dtype dtype, char* buf, size_t cap) {
+  return guard([&] {
+    gft::Kernel& k = kernel_of(plan, kind, dtype);
+    if (!buf || cap == 0) gft::fail(GFT_ERR_INVALID_ARG, "NULL buffer");
+    size_t m = std::min(cap - 1, k.name.size());
+    std::memcpy(buf, k.name.data(), m);
+    buf[m] = 0;
+  });
+}
+
+gft_status gft_plan_launch_config(gft_plan plan, int32_t kind, gft_dtype dtype, int64_t batch,
+                                  int32_t* grid, int32_t* block, int32_t* smem_bytes, int32_t* regs) {
+  return guard([&] {
+    gft::Kernel& k = kernel_of(plan, kind, dtype);
+    gft::kernel_launch_config(k, batch, grid, block, smem_bytes, regs,
+                              !(plan->flags & GFT_FLAG_NO_CUBIN_CACHE));
+  });
+}
+
+gft_status gft_laplacian(int32_t n, int64_t n_edges, const int32_t* src, const int32_t* dst,
+                         const double* w, const double* self_loops, double* L) {
+  return guard([&] {
+    if (!L) gft::fail(GFT_ERR_INVALID_ARG, "NULL output");
+    gft::SubGraph g = gft::graph_from_edges(n, n_edges, src, dst, w, self_loops);
+    auto l = g.laplacian();
+    std::memcpy(L, l.data(), sizeof(double) * l.size());
+  });
+}
+
+gft_status gft_decompose(int32_t n, const double* L, const int32_t* phi, double sym_rtol,
+                         double* Lplus, double* Lminus, int32_t* p_out) {
+  return guard([&] {
+    if (n < 1 || !L || !phi) gft::fail(GFT_ERR_INVALID_ARG, "bad argument");
+    gft::check_involution(n, phi);
+    gft::SubGraph g = gft::subgraph_from_laplacian(n, L);
+    std::vector<int> ph(phi, phi + n);
+    if (!gft::is_phi_symmetric(g, ph, sym_rtol))
+      gft::fail(GFT_ERR_NOT_SYMMETRIC, "graph is not phi-symmetric within sym_rtol (Definition 2)");
+    gft::SubGraph plus, minus;
+    std::vector<int> pn, mn;
+    gft::theorem4(g, ph, gft::orient_pairs(g, ph, true), 0.0, plus, minus, pn, mn);
+    if (p_out) *p_out = minus.k;
+    if (Lplus) { auto a = plus.laplacian(); std::memcpy(Lplus, a.data(), sizeof(double) * a.size()); }
+    if (Lminus) { auto a = minus.laplacian(); std::memcpy(Lminus, a.data(), sizeof(double) * a.size()); }
+  });
+}
+
+gft_status gft_find_involution(int32_t n, const double* L, double rtol, int64_t budget, int32_t* phi,
+                               int32_t* p_out, int32_t* complete) {
+  return guard([&] {
+    if (n < 1 || !L || !phi) gft::fail(GFT_ERR_INVALID_ARG, "bad argument");
+    if (budget <= 0) gft::fail(GFT_ERR_INVALID_ARG, "budget must be > 0");
+    gft::SubGraph g = gft::subgraph_from_laplacian(n, L);
+    gft::SearchResult r = gft::find_involution(g, rtol, budget);
+    for (int i = 0; i < n; ++i) phi[i] = r.phi[i];
+    if (p_out) *p_out = r.p;
+    if (complete) *complete = r.complete ? 1 : 0;
+  });
+}
+
+const char* gft_status_str(gft_status s) {
+  switch (s) {
+    case GFT_OK: return "GFT_OK";
+    case GFT_ERR_INVALID_ARG: return "GFT_ERR_INVALID_ARG";
+    case GFT_ERR_NOT_INVOLUTION: return "GFT_ERR_NOT_INVOLUTION";
+    case GFT_ERR_NOT_SYMMETRIC: return "GFT_ERR_NOT_SYMMETRIC";
+    case GFT_ERR_EIG_NOCONVERGE: return "GFT_ERR_EIG_NOCONVERGE";
+    case GFT_ERR_ALIGNMENT: return "GFT_ERR_ALIGNMENT";
+    case GFT_ERR_UNSUPPORTED: return "GFT_ERR_UNSUPPORTED";
+    case GFT_ERR_CUDA: return "GFT_ERR_CUDA";
+    case GFT_ERR_NOMEM: return "GFT_ERR_NOMEM";
+    case GFT_ERR_COMPILE: return "GFT_ERR_COMPILE";
+    case GFT_ERR_NO_DEVICE: return "GFT_ERR_NO_DEVICE";
+  }
+  return "GFT_ERR_UNKNOWN";
+}
+
+const char* gft_last_error(void) { return g_last_error.c_str(); }
+
+int32_t gft_abi_version(void) { return GFT_ABI_VERSION; }
+
+}  // extern "C"

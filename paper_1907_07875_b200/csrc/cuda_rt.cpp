@@ -1,0 +1,383 @@
+// cuda_rt.cpp — device runtime: driver API + NVRTC loaded with dlopen (so the library
+// loads on a CPU-only host), cubin cache / NVRTC compilation, module loading per
+// CUDA context, TMA tensor-map encoding and kernel launch.
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <sstream>
+
+#include "../../include/gft.h"
+#include "kernels.hpp"
+
+namespace gft {
+namespace {
+
+struct Driver {
+  bool tried = false, ok = false;
+  std::string err;
+  CUresult (*cuInit)(unsigned);
+  CUresult (*cuGetErrorString)(CUresult, const char**);
+  CUresult (*cuCtxGetCurrent)(CUcontext*);
+  CUresult (*cuCtxSetCurrent)(CUcontext);
+  CUresult (*cuCtxGetDevice)(CUdevice*);
+  CUresult (*cuStreamGetCtx)(CUstream, CUcontext*);
+  CUresult (*cuDeviceGet)(CUdevice*, int);
+  CUresult (*cuDeviceGetCount)(int*);
+  CUresult (*cuDeviceGetAttribute)(int*, CUdevice_attribute, CUdevice);
+  CUresult (*cuDevicePrimaryCtxRetain)(CUcontext*, CUdevice);
+  CUresult (*cuModuleLoadData)(CUmodule*, const void*);
+  CUresult (*cuModuleUnload)(CUmodule);
+  CUresult (*cuModuleGetFunction)(CUfunction*, CUmodule, const char*);
+  CUresult (*cuFuncSetAttribute)(CUfunction, CUfunction_attribute, int);
+  CUresult (*cuFuncGetAttribute)(int*, CUfunction_attribute, CUfunction);
+  CUresult (*cuOccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t);
+  CUresult (*cuLaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                             unsigned, CUstream, void**, void**);
+  CUresult (*cuTensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                     const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  CUresult (*cuMemcpyHtoDAsync)(CUdeviceptr, const void*, size_t, CUstream);
+  CUresult (*cuMemcpyDtoHAsync)(void*, CUdeviceptr, size_t, CUstream);
+  CUresult (*cuStreamCreate)(CUstream*, unsigned);
+  CUresult (*cuEventCreate)(CUevent*, unsigned);
+  CUresult (*cuEventRecord)(CUevent, CUstream);
+  CUresult (*cuStreamWaitEvent)(CUstream, CUevent, unsigned);
+};
+
+struct Nvrtc {
+  bool tried = false, ok = false;
+  std::string err;
+  nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*);
+  nvrtcResult (*compile)(nvrtcProgram, int, const char* const*);
+  nvrtcResult (*log_size)(nvrtcProgram, size_t*);
+  nvrtcResult (*log)(nvrtcProgram, char*);
+  nvrtcResult (*cubin_size)(nvrtcProgram, size_t*);
+  nvrtcResult (*cubin)(nvrtcProgram, char*);
+  nvrtcResult (*destroy)(nvrtcProgram*);
+  const char* (*errstr)(nvrtcResult);
+};
+
+std::mutex g_init_mu;
+
+Driver& drv() {
+  static Driver d;
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  if (d.tried) return d;
+  d.tried = true;
+  void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) { d.err = std::string("cannot load libcuda.so.1: ") + dlerror(); return d; }
+  typedef CUresult (*GetProc)(const char*, void**, int, cuuint64_t, CUdriverProcAddressQueryResult*);
+  GetProc gp = (GetProc)dlsym(h, "cuGetProcAddress_v2");
+  if (!gp) { d.err = "libcuda has no cuGetProcAddress_v2"; return d; }
+  bool ok = true;
+  auto get = [&](const char* name, void** slot) {
+    CUdriverProcAddressQueryResult q;
+    if (gp(name, slot, 12000, CU_GET_PROC_ADDRESS_DEFAULT, &q) != CUDA_SUCCESS || !*slot) {
+      ok = false;
+      d.err = std::string("driver symbol missing: ") + name;
+    }
+  };
+#define GFT_GET(fn) get(#fn, reinterpret_cast<void**>(&d.fn))
+  GFT_GET(cuInit); GFT_GET(cuGetErrorString); GFT_GET(cuCtxGetCurrent); GFT_GET(cuCtxSetCurrent);
+  GFT_GET(cuCtxGetDevice); GFT_GET(cuStreamGetCtx); GFT_GET(cuDeviceGet); GFT_GET(cuDeviceGetCount);
+  GFT_GET(cuDeviceGetAttribute); GFT_GET(cuDevicePrimaryCtxRetain); GFT_GET(cuModuleLoadData);
+  GFT_GET(cuModuleUnload); GFT_GET(cuModuleGetFunction); GFT_GET(cuFuncSetAttribute);
+  GFT_GET(cuFuncGetAttribute); GFT_GET(cuOccupancyMaxActiveBlocksPerMultiprocessor);
+  GFT_GET(cuLaunchKernel); GFT_GET(cuTensorMapEncodeTiled); GFT_GET(cuMemcpyHtoDAsync);
+  GFT_GET(cuMemcpyDtoHAsync); GFT_GET(cuStreamCreate); GFT_GET(cuEventCreate);
+  GFT_GET(cuEventRecord); GFT_GET(cuStreamWaitEvent);
+#undef GFT_GET
+  if (!ok) return d;
+  CUresult r = d.cuInit(0);
+  if (r != CUDA_SUCCESS) { d.err = "cuInit failed (" + std::to_string((int)r) + ")"; return d; }
+  int cnt = 0;
+  if (d.cuDeviceGetCount(&cnt) != CUDA_SUCCESS || cnt == 0) { d.err = "no CUDA device"; return d; }
+  d.ok = true;
+  return d;
+}
+
+Nvrtc& rtc() {
+  static Nvrtc n;
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  if (n.tried) return n;
+  n.tried = true;
+  const char* cands[] = {getenv("GFT_NVRTC_LIB"), "/usr/local/cuda/lib64/libnvrtc.so.12",
+                         "libnvrtc.so.12", "libnvrtc.so"};
+  void* h = nullptr;
+  for (const char* c : cands)
+    if (c && (h = dlopen(c, RTLD_NOW | RTLD_LOCAL))) break;
+  if (!h) { n.err = "cannot load libnvrtc.so.12"; return n; }
+  bool ok = true;
+  auto get = [&](const char* name, void** slot) {
+    *slot = dlsym(h, name);
+    if (!*slot) { ok = false; n.err = std::string("nvrtc symbol missing: ") + name; }
+  };
+  get("nvrtcCreateProgram", reinterpret_cast<void**>(&n.create));
+  get("nvrtcCompileProgram", reinterpret_cast<void**>(&n.compile));
+  get("nvrtcGetProgramLogSize", reinterpret_cast<void**>(&n.log_size));
+  get("nvrtcGetProgramLog", reinterpret_cast<void**>(&n.log));
+  get("nvrtcGetCUBINSize", reinterpret_cast<void**>(&n.cubin_size));
+  get("nvrtcGetCUBIN", reinterpret_cast<void**>(&n.cubin));
+  get("nvrtcDestroyProgram", reinterpret_cast<void**>(&n.destroy));
+  get("nvrtcGetErrorString", reinterpret_cast<void**>(&n.errstr));
+  n.ok = ok;
+  return n;
+}
+
+void ck(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return;
+  const char* s = nullptr;
+  drv().cuGetErrorString(r, &s);
+  fail(GFT_ERR_CUDA, std::string(what) + ": " + (s ? s : "unknown CUDA error") + " (" +
+                         std::to_string((int)r) + ")");
+}
+
+Driver& need_driver() {
+  Driver& d = drv();
+  if (!d.ok) fail(GFT_ERR_NO_DEVICE, d.err);
+  return d;
+}
+
+std::string lib_dir() {
+  Dl_info info;
+  if (dladdr(reinterpret_cast<void*>(&lib_dir), &info) && info.dli_fname) {
+    std::string p(info.dli_fname);
+    size_t s = p.rfind('/');
+    if (s != std::string::npos) return p.substr(0, s);
+  }
+  return ".";
+}
+
+bool read_file(const std::string& path, std::string& out) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return false;
+  std::ostringstream ss;
+  ss << f.rdbuf();
+  out = ss.str();
+  return !out.empty();
+}
+
+CUcontext current_ctx(void* stream) {
+  Driver& d = need_driver();
+  CUcontext ctx = nullptr;
+  if (stream) ck(d.cuStreamGetCtx((CUstream)stream, &ctx), "cuStreamGetCtx");
+  else ck(d.cuCtxGetCurrent(&ctx), "cuCtxGetCurrent");
+  if (!ctx) {
+    CUdevice dev;
+    ck(d.cuDeviceGet(&dev, 0), "cuDeviceGet");
+    ck(d.cuDevicePrimaryCtxRetain(&ctx, dev), "cuDevicePrimaryCtxRetain");
+  }
+  CUcontext cur = nullptr;
+  d.cuCtxGetCurrent(&cur);
+  if (cur != ctx) ck(d.cuCtxSetCurrent(ctx), "cuCtxSetCurrent");
+  return ctx;
+}
+
+LoadedFn& ensure_loaded(Kernel& k, CUcontext ctx, bool allow_cache) {
+  std::lock_guard<std::mutex> lk(k.mu);
+  auto it = k.loaded.find(ctx);
+  if (it != k.loaded.end()) return it->second;
+  if (k.cubin.empty()) compile_kernel(k, allow_cache);
+  Driver& d = need_driver();
+  LoadedFn L;
+  CUmodule mod;
+  ck(d.cuModuleLoadData(&mod, k.cubin.data()), "cuModuleLoadData");
+  CUfunction fn;
+  ck(d.cuModuleGetFunction(&fn, mod, k.name.c_str()), "cuModuleGetFunction");
+  const int smem = k.cfg.smem_bytes();
+  ck(d.cuFuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem),
+     "cuFuncSetAttribute(max dynamic smem)");
+  int occ = 0;
+  ck(d.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, k.cfg.warps * 32, smem), "occupancy");
+  if (occ < 1) fail(GFT_ERR_CUDA, "kernel " + k.name + " cannot be resident (occupancy 0)");
+  CUdevice dev;
+  ck(d.cuCtxGetDevice(&dev), "cuCtxGetDevice");
+  int sms = 0;
+  ck(d.cuDeviceGetAttribute(&sms, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev), "SM count");
+  d.cuFuncGetAttribute(&L.regs, CU_FUNC_ATTRIBUTE_NUM_REGS, fn);
+  L.module = mod;
+  L.fn = fn;
+  L.grid_max = sms * occ;
+  return k.loaded.emplace(ctx, L).first->second;
+}
+
+void encode_map(CUtensorMap* m, const Kernel& k, const void* ptr, int64_t rows) {
+  Driver& d = need_driver();
+  const KernelCfg& c = k.cfg;
+  cuuint64_t dims[2] = {(cuuint64_t)c.n, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)c.n * c.elem};
+  cuuint32_t box[2] = {(cuuint32_t)c.boxc, (cuuint32_t)c.tile_rows()};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle sw = c.swz_mask == 7 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : c.swz_mask == 3 ? CU_TENSOR_MAP_SWIZZLE_64B
+                          : c.swz_mask == 1 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
+  ck(d.cuTensorMapEncodeTiled(m, c.elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                              2, const_cast<void*>(ptr), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+     "cuTensorMapEncodeTiled");
+}
+
+// max rows per launch: TMA coordinates are int32
+constexpr int64_t kMaxRowsPerLaunch = (int64_t)1 << 30;
+
+}  // namespace
+
+std::string cubin_cache_dir() {
+  const char* e = getenv("GFT_CUBIN_DIR");
+  if (e && *e) return e;
+  return lib_dir() + "/kernels";
+}
+
+void compile_kernel(Kernel& k, bool allow_cache) {
+  if (!k.cubin.empty()) return;
+  if (allow_cache) {
+    std::string path = cubin_cache_dir() + "/" + k.name + ".cubin";
+    if (read_file(path, k.cubin)) { k.cubin_origin = "aot-cache"; return; }
+  }
+  Nvrtc& n = rtc();
+  if (!n.ok) fail(GFT_ERR_COMPILE, n.err);
+  nvrtcProgram prog;
+  nvrtcResult r = n.create(&prog, k.source.c_str(), (k.name + ".cu").c_str(), 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) fail(GFT_ERR_COMPILE, std::string("nvrtcCreateProgram: ") + n.errstr(r));
+  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-DNDEBUG", "--fmad=true"};
+  r = n.compile(prog, 5, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t ls = 0;
+    n.log_size(prog, &ls);
+    std::string log(ls, '\0');
+    if (ls) n.log(prog, &log[0]);
+    n.destroy(&prog);
+    fail(GFT_ERR_COMPILE, "NVRTC failed for " + k.name + ": " + log.substr(0, 2000));
+  }
+  size_t cs = 0;
+  n.cubin_size(prog, &cs);
+  k.cubin.assign(cs, '\0');
+  n.cubin(prog, &k.cubin[0]);
+  n.destroy(&prog);
+  k.cubin_origin = "nvrtc";
+}
+
+void kernel_launch_config(Kernel& k, int64_t batch, int* grid, int* block, int* smem, int* regs,
+                          bool allow_cache) {
+  CUcontext ctx = current_ctx(nullptr);
+  LoadedFn& L = ensure_loaded(k, ctx, allow_cache);
+  const int64_t rows = std::min<int64_t>(batch, kMaxRowsPerLaunch);
+  const int64_t tiles = (rows + k.cfg.tile_rows() - 1) / k.cfg.tile_rows();
+  const int64_t ctas = (tiles + k.cfg.warps - 1) / k.cfg.warps;
+  if (grid) *grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, L.grid_max));
+  if (block) *block = k.cfg.warps * 32;
+  if (smem) *smem = k.cfg.smem_bytes();
+  if (regs) *regs = L.regs;
+}
+
+void launch_kernel(Kernel& k, const void* in, void* out, int64_t batch, void* stream,
+                   bool allow_cache) {
+  if (batch <= 0) return;
+  Driver& d = need_driver();
+  CUcontext ctx = current_ctx(stream);
+  LoadedFn& L = ensure_loaded(k, ctx, allow_cache);
+  const KernelCfg& c = k.cfg;
+  const size_t row_bytes = (size_t)c.n * c.elem;
+  for (int64_t off = 0; off < batch; off += kMaxRowsPerLaunch) {
+    const int64_t rows = std::min<int64_t>(batch - off, kMaxRowsPerLaunch);
+    const unsigned char* pin = static_cast<const unsigned char*>(in) + off * row_bytes;
+    unsigned char* pout = static_cast<unsigned char*>(out) + off * row_bytes;
+    alignas(64) CUtensorMap tin, tout;
+    std::memset(&tin, 0, sizeof tin);
+    std::memset(&tout, 0, sizeof tout);
+    if (c.mode == 0) {
+      encode_map(&tin, k, pin, rows);
+      encode_map(&tout, k, pout, rows);
+    }
+    const int64_t tiles = (rows + c.tile_rows() - 1) / c.tile_rows();
+    const int64_t ctas = (tiles + c.warps - 1) / c.warps;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, L.grid_max));
+    long long nrows = rows;
+    const void* xin = pin;
+    void* xout = pout;
+    void* args[] = {&tin, &tout, &xin, &xout, &nrows};
+    ck(d.cuLaunchKernel((CUfunction)L.fn, grid, 1, 1, c.warps * 32, 1, 1, c.smem_bytes(),
+                        (CUstream)stream, args, nullptr),
+       "cuLaunchKernel");
+  }
+}
+
+void unload_kernel(Kernel& k) {
+  Driver& d = drv();
+  if (!d.ok) return;
+  std::lock_guard<std::mutex> lk(k.mu);
+  for (auto& kv : k.loaded) {
+    CUcontext cur = nullptr;
+    d.cuCtxGetCurrent(&cur);
+    if (cur != (CUcontext)kv.first) d.cuCtxSetCurrent((CUcontext)kv.first);
+    d.cuModuleUnload((CUmodule)kv.second.module);
+    if (cur && cur != (CUcontext)kv.first) d.cuCtxSetCurrent(cur);
+  }
+  k.loaded.clear();
+}
+
+namespace {
+struct HostStreams {
+  CUstream s[2];
+  CUevent start, done[2];
+};
+std::mutex g_hs_mu;
+std::map<CUcontext, HostStreams> g_hs;
+HostStreams& host_streams(CUcontext ctx) {
+  std::lock_guard<std::mutex> lk(g_hs_mu);
+  auto it = g_hs.find(ctx);
+  if (it != g_hs.end()) return it->second;
+  Driver& d = need_driver();
+  HostStreams h;
+  for (int i = 0; i < 2; ++i) ck(d.cuStreamCreate(&h.s[i], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+  ck(d.cuEventCreate(&h.start, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+  for (int i = 0; i < 2; ++i) ck(d.cuEventCreate(&h.done[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+  return g_hs.emplace(ctx, h).first->second;
+}
+}  // namespace
+
+void execute_host(Kernel& k, const void* in_host, void* out_host, int64_t batch, void* workspace,
+                  size_t workspace_bytes, int64_t chunk_rows, void* stream, bool allow_cache) {
+  if (batch <= 0) return;
+  if (chunk_rows <= 0) fail(GFT_ERR_INVALID_ARG, "chunk_rows must be > 0");
+  const size_t row_bytes = (size_t)k.cfg.n * k.cfg.elem;
+  const size_t chunk_bytes = (size_t)chunk_rows * row_bytes;
+  if (!workspace || workspace_bytes < 2 * chunk_bytes)
+    fail(GFT_ERR_INVALID_ARG, "workspace smaller than 2 * chunk_rows * n * sizeof(dtype)");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) || (chunk_bytes & 15))
+    fail(GFT_ERR_ALIGNMENT, "workspace / chunk not 16-byte aligned");
+  Driver& d = need_driver();
+  CUcontext ctx = current_ctx(stream);
+  HostStreams& hs = host_streams(ctx);
+  ck(d.cuEventRecord(hs.start, (CUstream)stream), "cuEventRecord");
+  for (int i = 0; i < 2; ++i) ck(d.cuStreamWaitEvent(hs.s[i], hs.start, 0), "cuStreamWaitEvent");
+  int64_t c = 0;
+  for (int64_t off = 0; off < batch; off += chunk_rows, ++c) {
+    const int slot = (int)(c & 1);
+    const int64_t rows = std::min<int64_t>(chunk_rows, batch - off);
+    CUstream s = hs.s[slot];
+    unsigned char* buf = static_cast<unsigned char*>(workspace) + slot * chunk_bytes;
+    ck(d.cuMemcpyHtoDAsync((CUdeviceptr)buf, static_cast<const unsigned char*>(in_host) + off * row_bytes,
+                           rows * row_bytes, s),
+       "cuMemcpyHtoDAsync");
+    launch_kernel(k, buf, buf, rows, s, allow_cache);
+    ck(d.cuMemcpyDtoHAsync(static_cast<unsigned char*>(out_host) + off * row_bytes, (CUdeviceptr)buf,
+                           rows * row_bytes, s),
+       "cuMemcpyDtoHAsync");
+  }
+  for (int i = 0; i < 2; ++i) {
+    ck(d.cuEventRecord(hs.done[i], hs.s[i]), "cuEventRecord");
+    ck(d.cuStreamWaitEvent((CUstream)stream, hs.done[i], 0), "cuStreamWaitEvent");
+  }
+}
+
+}  // namespace gft

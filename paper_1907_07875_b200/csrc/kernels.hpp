@@ -1,0 +1,68 @@
+// kernels.hpp — per-plan CUDA code generation and the device runtime (NVRTC + driver API).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace gft {
+
+enum KernelKind { K_FAST_FWD = 0, K_FAST_INV = 1, K_DENSE_FWD = 2, K_DENSE_INV = 3, K_NUM = 4 };
+
+// Launch/layout geometry of one generated kernel (see kernel_skeleton.cuh).
+struct KernelCfg {
+  int n = 0, elem = 4;          // signal length, bytes per element
+  int R = 1, warps = 4, stages = 3;
+  int mode = 0;                 // 0 TMA tensor 2-D + swizzle, 1 bulk 1-D
+  int boxc = 0, swz_mask = 0;   // TMA box columns, swizzle mask (7/3/1/0)
+  int vec = 1;                  // elements per SMEM vector access
+  int tile_rows() const { return 32 * R; }
+  int tile_bytes() const { return tile_rows() * n * elem; }
+  int smem_bytes() const { return warps * stages * tile_bytes() + warps * stages * 8 + 1024; }
+  int swizzle_bytes() const { return swz_mask == 7 ? 128 : swz_mask == 3 ? 64 : swz_mask == 1 ? 32 : 0; }
+};
+
+KernelCfg choose_cfg(int n, int dtype);
+
+struct LoadedFn {
+  void* module = nullptr;   // CUmodule
+  void* fn = nullptr;       // CUfunction
+  int grid_max = 0;         // SMs * resident CTAs
+  int regs = 0;
+};
+
+struct Kernel {
+  int kind = 0, dtype = 0;
+  KernelCfg cfg;
+  std::string name, source;
+  std::string cubin;        // filled by compile()
+  std::string cubin_origin; // "aot-cache" | "nvrtc"
+  std::mutex mu;
+  std::map<void*, LoadedFn> loaded;   // per CUcontext
+};
+
+// Emits the full CUDA source (prelude + gft_body + skeleton) for a plan.
+void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k);
+
+// Compiles k.source to an sm_100a cubin (AOT cache lookup first unless disabled).
+void compile_kernel(Kernel& k, bool allow_cache);
+
+// Launches `k` on `stream` (a CUstream / cudaStream_t) over `batch` rows.
+void launch_kernel(Kernel& k, const void* in, void* out, int64_t batch, void* stream, bool allow_cache);
+void kernel_launch_config(Kernel& k, int64_t batch, int* grid, int* block, int* smem, int* regs,
+                          bool allow_cache);
+void unload_kernel(Kernel& k);
+
+// Host<->device pipelined execution (gft_execute_host).
+struct HostExec;
+void execute_host(Kernel& k, const void* in_host, void* out_host, int64_t batch, void* workspace,
+                  size_t workspace_bytes, int64_t chunk_rows, void* stream, bool allow_cache);
+
+std::string cubin_cache_dir();
+
+}  // namespace gft

@@ -1,0 +1,526 @@
+// plan.cpp — graph validation, Theorem 4 decomposition, recursion, leaf solves,
+// realisation / canonicalisation / ordering, sqrt2 folding (see plan.hpp for the map).
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <numeric>
+#include <utility>
+
+#include "../../include/gft.h"
+
+namespace gft {
+
+[[noreturn]] void fail(int status, const std::string& msg) { throw Error{status, msg}; }
+
+static const double kSqrt2 = 1.41421356237309504880;
+
+std::vector<double> SubGraph::laplacian() const {
+  // eq:l_from_sw
+  std::vector<double> L((size_t)k * k, 0.0);
+  for (int i = 0; i < k; ++i) {
+    double d = s[i];
+    for (int j = 0; j < k; ++j) {
+      if (j == i) continue;
+      L[(size_t)i * k + j] = -w(i, j);
+      d += w(i, j);
+    }
+    L[(size_t)i * k + i] = d;
+  }
+  return L;
+}
+
+double SubGraph::scale() const {
+  double m = 0;
+  for (double v : W) m = std::max(m, std::fabs(v));
+  for (double v : s) m = std::max(m, std::fabs(v));
+  return m > 0 ? m : 1e-300;
+}
+
+SubGraph subgraph_from_laplacian(int n, const double* L) {
+  // eq:sw_from_l: s_i = sum_j l_ij, w_ij = -l_ij
+  SubGraph g;
+  g.k = n;
+  g.W.assign((size_t)n * n, 0.0);
+  g.s.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double rs = 0;
+    for (int j = 0; j < n; ++j) {
+      double v = L[(size_t)i * n + j];
+      if (!std::isfinite(v)) fail(GFT_ERR_INVALID_ARG, "non-finite Laplacian entry");
+      rs += v;
+      if (j != i) g.W[(size_t)i * n + j] = -v;
+    }
+    g.s[i] = rs;
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j) {
+      double a = g.W[(size_t)i * n + j], b = g.W[(size_t)j * n + i];
+      if (std::fabs(a - b) > 1e-12 * std::max(1.0, std::max(std::fabs(a), std::fabs(b))))
+        fail(GFT_ERR_INVALID_ARG, "Laplacian is not symmetric");
+      double m = 0.5 * (a + b);
+      g.W[(size_t)i * n + j] = g.W[(size_t)j * n + i] = m;
+    }
+  return g;
+}
+
+SubGraph graph_from_edges(int n, int64_t n_edges, const int32_t* src, const int32_t* dst,
+                          const double* w, const double* self_loops) {
+  if (n < 1) fail(GFT_ERR_INVALID_ARG, "n must be >= 1");
+  if (n > 8192) fail(GFT_ERR_UNSUPPORTED, "n > 8192 not supported by the dense planner");
+  if (n_edges < 0) fail(GFT_ERR_INVALID_ARG, "n_edges < 0");
+  if (n_edges > 0 && (!src || !dst || !w)) fail(GFT_ERR_INVALID_ARG, "NULL edge arrays");
+  SubGraph g;
+  g.k = n;
+  g.W.assign((size_t)n * n, 0.0);
+  g.s.assign(n, 0.0);
+  std::vector<char> seen((size_t)n * n, 0);
+  for (int64_t e = 0; e < n_edges; ++e) {
+    int i = src[e], j = dst[e];
+    double wt = w[e];
+    if (i < 0 || i >= n || j < 0 || j >= n)
+      fail(GFT_ERR_INVALID_ARG, "edge " + std::to_string(e) + ": node index out of range");
+    if (i == j)
+      fail(GFT_ERR_INVALID_ARG, "edge " + std::to_string(e) + ": self-edge (use self_loops)");
+    if (!std::isfinite(wt)) fail(GFT_ERR_INVALID_ARG, "edge " + std::to_string(e) + ": non-finite weight");
+    size_t a = (size_t)std::min(i, j) * n + std::max(i, j);
+    if (seen[a]) fail(GFT_ERR_INVALID_ARG, "edge " + std::to_string(e) + ": duplicate node pair");
+    seen[a] = 1;
+    if (wt == 0.0) continue;   // zero weight = no edge
+    g.W[(size_t)i * n + j] = wt;
+    g.W[(size_t)j * n + i] = wt;
+  }
+  if (self_loops) {
+    for (int i = 0; i < n; ++i) {
+      if (!std::isfinite(self_loops[i])) fail(GFT_ERR_INVALID_ARG, "non-finite self-loop");
+      g.s[i] = self_loops[i];
+    }
+  }
+  return g;
+}
+
+void check_involution(int n, const int32_t* phi) {
+  // Definition 1: a permutation with phi(phi(i)) = i.
+  for (int i = 0; i < n; ++i) {
+    int j = phi[i];
+    if (j < 0 || j >= n) fail(GFT_ERR_NOT_INVOLUTION, "phi[" + std::to_string(i) + "] out of range");
+    if (phi[j] != i)
+      fail(GFT_ERR_NOT_INVOLUTION, "phi(phi(" + std::to_string(i) + ")) != " + std::to_string(i));
+  }
+}
+
+bool is_phi_symmetric(const SubGraph& g, const std::vector<int>& phi, double rtol) {
+  // Definition 2, including self-loops s_i = s_phi(i).
+  const double tol = rtol * g.scale();
+  for (int i = 0; i < g.k; ++i) {
+    if (std::fabs(g.s[i] - g.s[phi[i]]) > tol) return false;
+    for (int j = i + 1; j < g.k; ++j)
+      if (std::fabs(g.w(i, j) - g.w(phi[i], phi[j])) > tol) return false;
+  }
+  return true;
+}
+
+std::vector<int> orient_pairs(const SubGraph& g, const std::vector<int>& phi, bool smaller_index) {
+  const int k = g.k;
+  std::vector<int> side(k, -1);   // 0 = V_X, 1 = V_Y
+  for (int a = 0; a < k; ++a) {
+    if (phi[a] == a || side[a] >= 0) continue;
+    side[a] = 0;
+    side[phi[a]] = 1;
+    if (smaller_index) continue;
+    std::vector<int> q{a, phi[a]};
+    for (size_t h = 0; h < q.size(); ++h) {
+      const int u = q[h];
+      for (int v = 0; v < k; ++v) {
+        if (v == u || phi[v] == v || v == phi[u] || side[v] >= 0 || g.w(u, v) == 0.0) continue;
+        side[v] = side[u];            // same side as its neighbour (edge does not cross the axis)
+        side[phi[v]] = 1 - side[u];
+        q.push_back(v);
+        q.push_back(phi[v]);
+      }
+    }
+  }
+  std::vector<int> X;
+  for (int i = 0; i < k; ++i)
+    if (side[i] == 0) X.push_back(i);
+  return X;
+}
+
+void theorem4(const SubGraph& g, const std::vector<int>& phi, const std::vector<int>& Xin,
+              double flush, SubGraph& plus, SubGraph& minus, std::vector<int>& plus_nodes,
+              std::vector<int>& minus_nodes) {
+  // Node partition: V_Z fixed points, V_X = Xin (one node of every
+  // pair), V_Y = phi(V_X).  G+ lives on V_X u V_Z, G- on V_Y.
+  const int k = g.k;
+  std::vector<int> X(Xin), Y, Z;
+  std::vector<char> inX(k, 0), inZ(k, 0);
+  for (int i = 0; i < k; ++i)
+    if (phi[i] == i) { Z.push_back(i); inZ[i] = 1; }
+  for (int x : X) {
+    if (phi[x] == x || inX[x] || inX[phi[x]]) fail(GFT_ERR_INVALID_ARG, "bad V_X for theorem4");
+    inX[x] = 1;
+  }
+  if ((int)(2 * X.size() + Z.size()) != k) fail(GFT_ERR_INVALID_ARG, "V_X does not cover every pair");
+  for (int x : X) Y.push_back(phi[x]);
+  plus_nodes = X;
+  plus_nodes.insert(plus_nodes.end(), Z.begin(), Z.end());
+  minus_nodes = Y;
+  const int kp = (int)plus_nodes.size(), km = (int)minus_nodes.size();
+  auto fl = [flush](double v) { return std::fabs(v) <= flush ? 0.0 : v; };
+
+  // ---- G+ (Theorem 4) ----
+  plus.k = kp;
+  plus.W.assign((size_t)kp * kp, 0.0);
+  plus.s.assign(kp, 0.0);
+  for (int a = 0; a < kp; ++a) {
+    const int i = plus_nodes[a];
+    for (int b = a + 1; b < kp; ++b) {
+      const int j = plus_nodes[b];
+      double v;
+      if (inX[i] && inX[j]) v = g.w(i, j) + g.w(i, phi[j]);          // X-X
+      else if (inZ[i] && inZ[j]) v = g.w(i, j);                        // Z-Z
+      else v = kSqrt2 * g.w(i, j);                                     // X-Z / Z-X
+      v = fl(v);
+      plus.W[(size_t)a * kp + b] = plus.W[(size_t)b * kp + a] = v;
+    }
+    double sv;
+    if (inX[i]) {
+      double sz = 0;
+      for (int z : Z) sz += g.w(i, z);
+      sv = g.s[i] - (kSqrt2 - 1.0) * sz;                               // s+_i, i in V_X
+    } else {
+      double sx = 0;
+      for (int x : X) sx += g.w(i, x);
+      sv = g.s[i] + (2.0 - kSqrt2) * sx;                               // s+_i, i in V_Z
+    }
+    plus.s[a] = fl(sv);
+  }
+  // ---- G- (Theorem 4) ----
+  minus.k = km;
+  minus.W.assign((size_t)km * km, 0.0);
+  minus.s.assign(km, 0.0);
+  for (int a = 0; a < km; ++a) {
+    const int i = minus_nodes[a];
+    for (int b = a + 1; b < km; ++b) {
+      const int j = minus_nodes[b];
+      double v = fl(g.w(i, j) - g.w(i, phi[j]));
+      minus.W[(size_t)a * km + b] = minus.W[(size_t)b * km + a] = v;
+    }
+    double sx = 0, sz = 0;
+    for (int x : X) sx += g.w(i, x);
+    for (int z : Z) sz += g.w(i, z);
+    minus.s[a] = fl(g.s[i] + 2.0 * sx + sz);
+  }
+}
+
+std::vector<std::vector<int>> components(const SubGraph& g) {
+  std::vector<int> comp(g.k, -1);
+  std::vector<std::vector<int>> out;
+  for (int r = 0; r < g.k; ++r) {
+    if (comp[r] >= 0) continue;
+    std::vector<int> members{r};
+    comp[r] = (int)out.size();
+    for (size_t q = 0; q < members.size(); ++q) {
+      int u = members[q];
+      for (int v = 0; v < g.k; ++v)
+        if (v != u && comp[v] < 0 && g.w(u, v) != 0.0) {
+          comp[v] = comp[r];
+          members.push_back(v);
+        }
+    }
+    std::sort(members.begin(), members.end());
+    out.push_back(members);
+  }
+  return out;
+}
+
+static SubGraph induced(const SubGraph& g, const std::vector<int>& nodes) {
+  SubGraph h;
+  h.k = (int)nodes.size();
+  h.W.assign((size_t)h.k * h.k, 0.0);
+  h.s.assign(h.k, 0.0);
+  for (int a = 0; a < h.k; ++a) {
+    h.s[a] = g.s[nodes[a]];
+    for (int b = 0; b < h.k; ++b)
+      if (a != b) h.W[(size_t)a * h.k + b] = g.w(nodes[a], nodes[b]);
+  }
+  return h;
+}
+
+// ---------------------------------------------------------------------------------
+// Recursive builder
+// ---------------------------------------------------------------------------------
+namespace {
+struct Builder {
+  const PlanOptions& opt;
+  Plan& P;
+  std::vector<int> d;   // running Haar scale exponent per position
+
+  Builder(const PlanOptions& o, Plan& p) : opt(o), P(p), d(p.n, 0) {}
+
+  double internal_rtol() const { return std::max(opt.sym_rtol, 1e-10); }
+
+  void emit_leaf(const SubGraph& g, const std::vector<int>& pos, int depth) {
+    Leaf lf;
+    lf.k = g.k;
+    lf.pos = pos;
+    lf.level = depth;
+    jacobi_eigh(g.k, g.laplacian(), lf.lam, lf.V);
+    P.leaves.push_back(std::move(lf));
+  }
+
+  void emit_stage(const SubGraph& g, const std::vector<int>& pos, int depth,
+                  const std::vector<int>& phi) {
+    int p = 0, nz = 0;
+    for (int i = 0; i < g.k; ++i) nz += phi[i] == i;
+    const std::vector<int> X = orient_pairs(g, phi, false);
+    for (int i : X) {
+      ++p;
+      const int a = pos[i], b = pos[phi[i]];
+      if (d[a] != d[b]) {
+        // partners carry different deferred 2^(d/2) scales: equalise explicitly
+        const int lo = d[a] < d[b] ? a : b, hi = d[a] < d[b] ? b : a;
+        P.ops.push_back(Op{Op::FIX, lo, -1, d[hi] - d[lo], depth});
+        d[lo] = d[hi];
+        ++P.n_fix;
+      }
+      P.ops.push_back(Op{Op::UNIT, a, b, 0, depth});   // sum -> a (V_X), difference -> b (V_Y)
+      ++d[a];
+      ++d[b];
+    }
+    if ((int)P.units_per_level.size() <= depth) P.units_per_level.resize(depth + 1, 0);
+    P.units_per_level[depth] += p;
+    P.n_units += p;
+    P.n_vz_total += nz;
+    SubGraph plus, minus;
+    std::vector<int> pn, mn;
+    theorem4(g, phi, X, internal_rtol() * g.scale(), plus, minus, pn, mn);
+    std::vector<int> pos_plus(pn.size()), pos_minus(mn.size());
+    for (size_t a = 0; a < pn.size(); ++a) pos_plus[a] = pos[pn[a]];
+    for (size_t a = 0; a < mn.size(); ++a) pos_minus[a] = pos[mn[a]];
+    node(plus, pos_plus, depth + 1, nullptr);
+    node(minus, pos_minus, depth + 1, nullptr);
+  }
+
+  void node(const SubGraph& g, const std::vector<int>& pos, int depth, const int32_t* top_phi) {
+    if (g.k == 0) return;
+    const bool depth_ok = opt.max_depth < 0 || depth < opt.max_depth;
+    if (top_phi) {
+      std::vector<int> phi(top_phi, top_phi + g.k);
+      int p = 0;
+      for (int i = 0; i < g.k; ++i) p += phi[i] > i;
+      if (p > 0 && depth_ok) {
+        emit_stage(g, pos, depth, phi);
+        return;
+      }
+    }
+    // Split into connected components before searching (reading A-9)
+    auto comps = components(g);
+    if (comps.size() > 1) {
+      for (auto& c : comps) {
+        std::vector<int> cp(c.size());
+        for (size_t a = 0; a < c.size(); ++a) cp[a] = pos[c[a]];
+        node(induced(g, c), cp, depth, nullptr);
+      }
+      return;
+    }
+    if (g.k <= opt.min_leaf || !depth_ok) {
+      emit_leaf(g, pos, depth);
+      return;
+    }
+    SearchResult r = find_involution(g, internal_rtol(), opt.search_budget);
+    if (r.p == 0) {
+      emit_leaf(g, pos, depth);
+      return;
+    }
+    emit_stage(g, pos, depth, r.phi);
+  }
+};
+}  // namespace
+
+Plan build_plan(const SubGraph& g, const int32_t* user_phi, const PlanOptions& opt) {
+  Plan P;
+  P.n = g.k;
+  P.L = g.laplacian();
+  if (user_phi) {
+    check_involution(g.k, user_phi);
+    std::vector<int> phi(user_phi, user_phi + g.k);
+    if (!is_phi_symmetric(g, phi, opt.sym_rtol))
+      fail(GFT_ERR_NOT_SYMMETRIC, "graph is not phi-symmetric within sym_rtol (Definition 2)");
+  }
+  Builder B(opt, P);
+  std::vector<int> pos(g.k);
+  std::iota(pos.begin(), pos.end(), 0);
+  B.node(g, pos, 0, user_phi);
+  P.dexp = B.d;
+  P.depth = (int)P.units_per_level.size();
+  while (P.depth > 0 && P.units_per_level[P.depth - 1] == 0) --P.depth;
+  P.units_per_level.resize(P.depth);
+
+  const int n = P.n;
+  // ---- P6: realise columns u = B_1 ... B_D (embedded v), canonicalise signs ----
+  // Q = B_D...B_1 (normalised butterflies) so U = Q^T blockdiag(V) and Q^T applies the
+  // units in reverse order; each B_phi is symmetric.
+  struct Col { double lam; int leaf, r; };
+  std::vector<Col> cols;
+  std::vector<std::vector<double>> realised;   // per (leaf, r) in cols order
+  const double r2 = 1.0 / kSqrt2;
+  for (int l = 0; l < (int)P.leaves.size(); ++l) {
+    Leaf& lf = P.leaves[l];
+    P.max_leaf = std::max(P.max_leaf, lf.k);
+    P.sum_k2 += (int64_t)lf.k * lf.k;
+    P.sum_kk1 += (int64_t)lf.k * (lf.k - 1);
+    for (int r = 0; r < lf.k; ++r) {
+      std::vector<double> u(n, 0.0);
+      for (int c = 0; c < lf.k; ++c) u[lf.pos[c]] = lf.V[(size_t)c * lf.k + r];
+      for (auto it = P.ops.rbegin(); it != P.ops.rend(); ++it) {
+        if (it->kind != Op::UNIT) continue;
+        const double a = u[it->a], b = u[it->b];
+        u[it->a] = (a + b) * r2;
+        u[it->b] = (a - b) * r2;
+      }
+      // sign rule: first entry with |u_i| > 1e-8 positive (reading A-3)
+      for (int i = 0; i < n; ++i) {
+        if (std::fabs(u[i]) > 1e-8) {
+          if (u[i] < 0) {
+            for (double& v : u) v = -v;
+            for (int c = 0; c < lf.k; ++c) lf.V[(size_t)c * lf.k + r] = -lf.V[(size_t)c * lf.k + r];
+          }
+          break;
+        }
+      }
+      cols.push_back(Col{lf.lam[r], l, r});
+      realised.push_back(std::move(u));
+    }
+  }
+  std::vector<int> order(cols.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return cols[a].lam < cols[b].lam; });
+  P.lambda.assign(n, 0.0);
+  P.U.assign((size_t)n * n, 0.0);
+  for (auto& lf : P.leaves) lf.slot.assign(lf.k, -1);
+  for (int rank = 0; rank < (int)order.size(); ++rank) {
+    const Col& c = cols[order[rank]];
+    P.lambda[rank] = c.lam;
+    P.leaves[c.leaf].slot[c.r] = rank;
+    const auto& u = realised[order[rank]];
+    for (int i = 0; i < n; ++i) P.U[(size_t)i * n + rank] = u[i];
+  }
+  // ---- P7: fold 2^(-d/2) into the leaves: M[r][c] = v_r(c) * 2^(-d_pos(c)/2) ----
+  for (auto& lf : P.leaves) {
+    lf.M.assign((size_t)lf.k * lf.k, 0.0);
+    for (int r = 0; r < lf.k; ++r)
+      for (int c = 0; c < lf.k; ++c)
+        lf.M[(size_t)r * lf.k + c] =
+            lf.V[(size_t)c * lf.k + r] * std::pow(2.0, -0.5 * P.dexp[lf.pos[c]]);
+  }
+  // ---- self-check of the realised basis ----
+  double lmax = 0;
+  for (double v : P.L) lmax = std::max(lmax, std::fabs(v));
+  double res = 0, orth = 0;
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < n; ++k) {
+      double acc = 0;
+      for (int j = 0; j < n; ++j) acc += P.L[(size_t)i * n + j] * P.U[(size_t)j * n + k];
+      res = std::max(res, std::fabs(acc - P.U[(size_t)i * n + k] * P.lambda[k]));
+    }
+  for (int a = 0; a < n; ++a)
+    for (int b = a; b < n; ++b) {
+      double acc = 0;
+      for (int i = 0; i < n; ++i) acc += P.U[(size_t)i * n + a] * P.U[(size_t)i * n + b];
+      orth = std::max(orth, std::fabs(acc - (a == b ? 1.0 : 0.0)));
+    }
+  P.residual = res;
+  P.orth_error = orth;
+  if (!(res <= 1e-8 * std::max(1.0, lmax)) || !(orth <= 1e-10))
+    fail(GFT_ERR_EIG_NOCONVERGE, "realised basis failed self-check (residual " +
+                                     std::to_string(res) + ", orthogonality " +
+                                     std::to_string(orth) + ")");
+  // ---- clusters (reading A-5) ----
+  double lm = 0;
+  for (double v : P.lambda) lm = std::max(lm, std::fabs(v));
+  const double ctol = 1e-9 * std::max(1.0, lm);
+  P.n_clusters = n > 0 ? 1 : 0;
+  for (int k = 1; k < n; ++k)
+    if (P.lambda[k] - P.lambda[k - 1] > ctol) ++P.n_clusters;
+  return P;
+}
+
+// ---------------------------------------------------------------------------------
+// Cyclic-by-row Jacobi (classical two-sided rotations; stable tan formula)
+// ---------------------------------------------------------------------------------
+void jacobi_eigh(int k, const std::vector<double>& A0, std::vector<double>& lam,
+                 std::vector<double>& V) {
+  std::vector<double> a(A0);
+  V.assign((size_t)k * k, 0.0);
+  for (int i = 0; i < k; ++i) V[(size_t)i * k + i] = 1.0;
+  auto A = [&](int i, int j) -> double& { return a[(size_t)i * k + j]; };
+  bool converged = (k <= 1);
+  for (int sweep = 0; sweep < 100 && !converged; ++sweep) {
+    double off = 0, diag = 0;
+    for (int i = 0; i < k; ++i) {
+      diag += A(i, i) * A(i, i);
+      for (int j = i + 1; j < k; ++j) off += A(i, j) * A(i, j);
+    }
+    if (off == 0.0 || std::sqrt(off) <= 1e-17 * std::sqrt(diag + 2 * off)) {
+      converged = true;
+      break;
+    }
+    for (int p = 0; p < k - 1; ++p)
+      for (int q = p + 1; q < k; ++q) {
+        const double apq = A(p, q);
+        if (apq == 0.0) continue;
+        const double app = A(p, p), aqq = A(q, q);
+        // underflow rule: drop a_pq once it no longer changes the diagonal
+        if (sweep > 3 && std::fabs(app) + 100 * std::fabs(apq) == std::fabs(app) &&
+            std::fabs(aqq) + 100 * std::fabs(apq) == std::fabs(aqq)) {
+          A(p, q) = A(q, p) = 0.0;
+          continue;
+        }
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int r = 0; r < k; ++r) {              // columns p, q
+          const double xp = A(r, p), xq = A(r, q);
+          A(r, p) = c * xp - s * xq;
+          A(r, q) = s * xp + c * xq;
+        }
+        for (int r = 0; r < k; ++r) {              // rows p, q
+          const double xp = A(p, r), xq = A(q, r);
+          A(p, r) = c * xp - s * xq;
+          A(q, r) = s * xp + c * xq;
+        }
+        A(p, q) = A(q, p) = 0.0;
+        for (int r = 0; r < k; ++r) {
+          const double vp = V[(size_t)r * k + p], vq = V[(size_t)r * k + q];
+          V[(size_t)r * k + p] = c * vp - s * vq;
+          V[(size_t)r * k + q] = s * vp + c * vq;
+        }
+      }
+  }
+  if (!converged) {
+    double off = 0, fro = 0;
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j) {
+        fro += A(i, j) * A(i, j);
+        if (i != j) off += A(i, j) * A(i, j);
+      }
+    if (std::sqrt(off) > 1e-13 * std::sqrt(fro))
+      fail(GFT_ERR_EIG_NOCONVERGE, "Jacobi did not converge in 100 sweeps");
+  }
+  // ascending order (stable)
+  std::vector<int> idx(k);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return A(x, x) < A(y, y); });
+  lam.resize(k);
+  std::vector<double> Vs((size_t)k * k);
+  for (int r = 0; r < k; ++r) {
+    lam[r] = A(idx[r], idx[r]);
+    for (int c = 0; c < k; ++c) Vs[(size_t)c * k + r] = V[(size_t)c * k + idx[r]];
+  }
+  V.swap(Vs);
+}
+
+}  // namespace gft

@@ -1,0 +1,403 @@
+"""Thin ctypes binding of include/gft.h (argument marshalling only).
+
+Every function here has the name of the C entry point it wraps and does nothing but
+convert arguments, call the library and raise GFTError on a non-OK status.  All
+computation happens in libgft.so: the host planner in C++ and the transforms in the
+generated sm_100a kernels.  There is no CPU or PyTorch fallback: if the library or a
+CUDA device is missing the call raises.
+
+`Plan` is a convenience owner of a gft_plan handle whose methods are the same calls.
+torch is used only to hand device pointers and the current stream to the library.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int32, c_int64, c_size_t, c_uint32, c_void_p
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("GFT_LIB", os.path.join(_HERE, "_lib", "libgft.so"))
+
+GFT_F32, GFT_F64 = 0, 1
+GFT_FLAG_HOST_ONLY, GFT_FLAG_NO_CUBIN_CACHE = 1, 2
+K_FAST_FWD, K_FAST_INV, K_DENSE_FWD, K_DENSE_INV = 0, 1, 2, 3
+GFT_MAX_LEVELS = 64
+
+STATUS = {0: "GFT_OK", 1: "GFT_ERR_INVALID_ARG", 2: "GFT_ERR_NOT_INVOLUTION",
+          3: "GFT_ERR_NOT_SYMMETRIC", 4: "GFT_ERR_EIG_NOCONVERGE", 5: "GFT_ERR_ALIGNMENT",
+          6: "GFT_ERR_UNSUPPORTED", 7: "GFT_ERR_CUDA", 8: "GFT_ERR_NOMEM", 9: "GFT_ERR_COMPILE",
+          10: "GFT_ERR_NO_DEVICE"}
+
+# every symbol include/gft.h declares (checked by tests/test_abi.py)
+EXPORTS = ["gft_plan_opts_default", "gft_plan_create", "gft_plan_destroy", "gft_forward",
+           "gft_inverse", "gft_dense_forward", "gft_dense_inverse", "gft_execute_host",
+           "gft_plan_compile", "gft_plan_info_get", "gft_plan_eigenvalues", "gft_plan_basis",
+           "gft_plan_leaf_sizes", "gft_plan_kernel_source", "gft_plan_kernel_name",
+           "gft_plan_launch_config", "gft_laplacian", "gft_decompose", "gft_find_involution",
+           "gft_status_str", "gft_last_error", "gft_abi_version"]
+
+
+class GFTError(RuntimeError):
+    def __init__(self, status, msg):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__("%s: %s" % (self.name, msg))
+
+
+class gft_plan_opts(ctypes.Structure):
+    _fields_ = [("max_depth", c_int32), ("min_leaf", c_int32), ("search_budget", c_int64),
+                ("sym_rtol", c_double), ("dtypes", c_uint32), ("flags", c_uint32)]
+
+
+class gft_plan_info(ctypes.Structure):
+    _fields_ = [("n", c_int32), ("depth", c_int32), ("n_units", c_int32),
+                ("units_per_level", c_int32 * GFT_MAX_LEVELS), ("n_leaves", c_int32),
+                ("max_leaf", c_int32), ("n_scale_fix", c_int32), ("n_vz_total", c_int32),
+                ("sum_k2", c_int64), ("adds", c_int64), ("mults", c_int64), ("paper_mults", c_int64),
+                ("dense_adds", c_int64), ("dense_mults", c_int64), ("n_clusters", c_int32),
+                ("kernels_ready", c_int32), ("residual", c_double), ("orth_error", c_double)]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "units_per_level"}
+        d["units_per_level"] = list(self.units_per_level[: self.depth])
+        return d
+
+
+_lib = None
+
+
+def lib():
+    """Load libgft.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError("libgft.so not built: run `python -m paper_1907_07875_b200.build` "
+                          "(or __graft_entry__.build())")
+    L = ctypes.CDLL(LIB_PATH)
+    P = c_void_p
+    sig = {
+        "gft_plan_opts_default": (None, [POINTER(gft_plan_opts)]),
+        "gft_plan_create": (c_int32, [POINTER(c_void_p), c_int32, c_int64, P, P, P, P, P,
+                                      POINTER(gft_plan_opts)]),
+        "gft_plan_destroy": (c_int32, [P]),
+        "gft_forward": (c_int32, [P, P, P, c_int64, c_int32, P]),
+        "gft_inverse": (c_int32, [P, P, P, c_int64, c_int32, P]),
+        "gft_dense_forward": (c_int32, [P, P, P, c_int64, c_int32, P]),
+        "gft_dense_inverse": (c_int32, [P, P, P, c_int64, c_int32, P]),
+        "gft_execute_host": (c_int32, [P, c_int32, P, P, c_int64, c_int32, P, c_size_t, c_int64, P]),
+        "gft_plan_compile": (c_int32, [P, c_int32]),
+        "gft_plan_info_get": (c_int32, [P, POINTER(gft_plan_info)]),
+        "gft_plan_eigenvalues": (c_int32, [P, P]),
+        "gft_plan_basis": (c_int32, [P, P]),
+        "gft_plan_leaf_sizes": (c_int32, [P, P, c_int32, POINTER(c_int32)]),
+        "gft_plan_kernel_source": (c_int32, [P, c_int32, c_int32, c_char_p, c_size_t, POINTER(c_size_t)]),
+        "gft_plan_kernel_name": (c_int32, [P, c_int32, c_int32, c_char_p, c_size_t]),
+        "gft_plan_launch_config": (c_int32, [P, c_int32, c_int32, c_int64, POINTER(c_int32),
+                                             POINTER(c_int32), POINTER(c_int32), POINTER(c_int32)]),
+        "gft_laplacian": (c_int32, [c_int32, c_int64, P, P, P, P, P]),
+        "gft_decompose": (c_int32, [c_int32, P, P, c_double, P, P, POINTER(c_int32)]),
+        "gft_find_involution": (c_int32, [c_int32, P, c_double, c_int64, P, POINTER(c_int32),
+                                          POINTER(c_int32)]),
+        "gft_status_str": (c_char_p, [c_int32]),
+        "gft_last_error": (c_char_p, []),
+        "gft_abi_version": (c_int32, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(status):
+    if status != 0:
+        raise GFTError(status, lib().gft_last_error().decode())
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(c_void_p)
+
+
+def _dev_ptr(t):
+    """Device address of a torch tensor (or an int address)."""
+    if isinstance(t, int):
+        return c_void_p(t)
+    return c_void_p(t.data_ptr())
+
+
+def _stream_handle(stream):
+    if stream is None:
+        import torch
+        return c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return c_void_p(stream)
+    return c_void_p(stream.cuda_stream)
+
+
+def _dtype_code(dtype):
+    if dtype in (GFT_F32, GFT_F64):
+        return dtype
+    s = str(dtype)
+    if "64" in s or s in ("f64", "double"):
+        return GFT_F64
+    return GFT_F32
+
+
+# ----------------------------------------------------------------------------- C names
+def gft_abi_version():
+    return lib().gft_abi_version()
+
+
+def gft_status_str(s):
+    return lib().gft_status_str(s).decode()
+
+
+def gft_last_error():
+    return lib().gft_last_error().decode()
+
+
+def gft_plan_opts_default():
+    o = gft_plan_opts()
+    lib().gft_plan_opts_default(ctypes.byref(o))
+    return o
+
+
+def _edges_arrays(src, dst, w):
+    src = np.ascontiguousarray(src, dtype=np.int32)
+    dst = np.ascontiguousarray(dst, dtype=np.int32)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    if not (len(src) == len(dst) == len(w)):
+        raise ValueError("src, dst, w must have equal length")
+    return src, dst, w
+
+
+def gft_plan_create(n, src, dst, w, self_loops=None, phi=None, opts=None):
+    src, dst, w = _edges_arrays(src, dst, w)
+    s = None if self_loops is None else np.ascontiguousarray(self_loops, dtype=np.float64)
+    if s is not None and len(s) != n:
+        raise ValueError("self_loops must have length n")
+    p = None if phi is None else np.ascontiguousarray(phi, dtype=np.int32)
+    if p is not None and len(p) != n:
+        raise ValueError("phi must have length n")
+    h = c_void_p()
+    _check(lib().gft_plan_create(ctypes.byref(h), int(n), len(src), _ptr(src), _ptr(dst), _ptr(w),
+                                 _ptr(s), _ptr(p), None if opts is None else ctypes.byref(opts)))
+    return h
+
+
+def gft_plan_destroy(h):
+    _check(lib().gft_plan_destroy(h))
+
+
+def _run(fn, h, a, b, batch, dtype, stream):
+    _check(fn(h, _dev_ptr(a), _dev_ptr(b), int(batch), _dtype_code(dtype), _stream_handle(stream)))
+
+
+def gft_forward(h, X, Y, batch, dtype=GFT_F32, stream=None):
+    _run(lib().gft_forward, h, X, Y, batch, dtype, stream)
+
+
+def gft_inverse(h, Y, X, batch, dtype=GFT_F32, stream=None):
+    _run(lib().gft_inverse, h, Y, X, batch, dtype, stream)
+
+
+def gft_dense_forward(h, X, Y, batch, dtype=GFT_F32, stream=None):
+    _run(lib().gft_dense_forward, h, X, Y, batch, dtype, stream)
+
+
+def gft_dense_inverse(h, Y, X, batch, dtype=GFT_F32, stream=None):
+    _run(lib().gft_dense_inverse, h, Y, X, batch, dtype, stream)
+
+
+def gft_execute_host(h, direction, in_host, out_host, batch, dtype, workspace, workspace_bytes,
+                     chunk_rows, stream=None):
+    _check(lib().gft_execute_host(h, int(direction), c_void_p(in_host.data_ptr()),
+                                  c_void_p(out_host.data_ptr()), int(batch), _dtype_code(dtype),
+                                  _dev_ptr(workspace), int(workspace_bytes), int(chunk_rows),
+                                  _stream_handle(stream)))
+
+
+def gft_plan_compile(h, dtype):
+    _check(lib().gft_plan_compile(h, _dtype_code(dtype)))
+
+
+def gft_plan_info_get(h):
+    info = gft_plan_info()
+    _check(lib().gft_plan_info_get(h, ctypes.byref(info)))
+    return info
+
+
+def gft_plan_eigenvalues(h, n):
+    lam = np.empty(n, dtype=np.float64)
+    _check(lib().gft_plan_eigenvalues(h, _ptr(lam)))
+    return lam
+
+
+def gft_plan_basis(h, n):
+    U = np.empty((n, n), dtype=np.float64)
+    _check(lib().gft_plan_basis(h, _ptr(U)))
+    return U
+
+
+def gft_plan_leaf_sizes(h):
+    cnt = c_int32()
+    _check(lib().gft_plan_leaf_sizes(h, None, 0, ctypes.byref(cnt)))
+    out = np.zeros(cnt.value, dtype=np.int32)
+    _check(lib().gft_plan_leaf_sizes(h, _ptr(out), cnt.value, ctypes.byref(cnt)))
+    return out.tolist()
+
+
+def gft_plan_kernel_source(h, kind, dtype=GFT_F32):
+    ln = c_size_t()
+    _check(lib().gft_plan_kernel_source(h, int(kind), _dtype_code(dtype), None, 0, ctypes.byref(ln)))
+    buf = ctypes.create_string_buffer(ln.value + 1)
+    _check(lib().gft_plan_kernel_source(h, int(kind), _dtype_code(dtype), buf, ln.value + 1,
+                                        ctypes.byref(ln)))
+    return buf.value.decode()
+
+
+def gft_plan_kernel_name(h, kind, dtype=GFT_F32):
+    buf = ctypes.create_string_buffer(256)
+    _check(lib().gft_plan_kernel_name(h, int(kind), _dtype_code(dtype), buf, 256))
+    return buf.value.decode()
+
+
+def gft_plan_launch_config(h, kind, dtype, batch):
+    g, b, s, r = c_int32(), c_int32(), c_int32(), c_int32()
+    _check(lib().gft_plan_launch_config(h, int(kind), _dtype_code(dtype), int(batch), ctypes.byref(g),
+                                        ctypes.byref(b), ctypes.byref(s), ctypes.byref(r)))
+    return {"grid": g.value, "block": b.value, "smem": s.value, "regs": r.value}
+
+
+def gft_laplacian(n, src, dst, w, self_loops=None):
+    src, dst, w = _edges_arrays(src, dst, w)
+    s = None if self_loops is None else np.ascontiguousarray(self_loops, dtype=np.float64)
+    L = np.empty((n, n), dtype=np.float64)
+    _check(lib().gft_laplacian(int(n), len(src), _ptr(src), _ptr(dst), _ptr(w), _ptr(s), _ptr(L)))
+    return L
+
+
+def gft_decompose(L, phi, sym_rtol=1e-12):
+    L = np.ascontiguousarray(L, dtype=np.float64)
+    n = L.shape[0]
+    phi = np.ascontiguousarray(phi, dtype=np.int32)
+    p = int(np.sum(phi > np.arange(n)))
+    Lp = np.empty((n - p, n - p), dtype=np.float64)
+    Lm = np.empty((p, p), dtype=np.float64)
+    pout = c_int32()
+    _check(lib().gft_decompose(n, _ptr(L), _ptr(phi), float(sym_rtol), _ptr(Lp), _ptr(Lm),
+                               ctypes.byref(pout)))
+    return Lp, Lm
+
+
+def gft_find_involution(L, rtol=1e-10, budget=1000000):
+    L = np.ascontiguousarray(L, dtype=np.float64)
+    n = L.shape[0]
+    phi = np.empty(n, dtype=np.int32)
+    p, comp = c_int32(), c_int32()
+    _check(lib().gft_find_involution(n, _ptr(L), float(rtol), int(budget), _ptr(phi), ctypes.byref(p),
+                                     ctypes.byref(comp)))
+    return phi, p.value, bool(comp.value)
+
+
+# ----------------------------------------------------------------------------- Plan
+class Plan:
+    """Owner of a gft_plan.  Methods are the C calls of the same name."""
+
+    def __init__(self, n, src, dst, w, self_loops=None, phi=None, *, max_depth=-1, min_leaf=1,
+                 search_budget=1000000, sym_rtol=1e-12, dtypes=("f32", "f64"), host_only=False,
+                 no_cubin_cache=False):
+        o = gft_plan_opts_default()
+        o.max_depth = max_depth
+        o.min_leaf = min_leaf
+        o.search_budget = search_budget
+        o.sym_rtol = sym_rtol
+        o.dtypes = 0
+        for d in dtypes:
+            o.dtypes |= 1 << _dtype_code(d)
+        o.flags = (GFT_FLAG_HOST_ONLY if host_only else 0) | (GFT_FLAG_NO_CUBIN_CACHE if no_cubin_cache else 0)
+        self.n = int(n)
+        self._h = gft_plan_create(n, src, dst, w, self_loops, phi, o)
+
+    @classmethod
+    def from_config(cls, cfg, **kw):
+        kw.setdefault("max_depth", cfg.max_depth)
+        kw.setdefault("dtypes", cfg.dtypes)
+        return cls(cfg.n, cfg.src, cfg.dst, cfg.w, cfg.self_loops, cfg.phi, **kw)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            gft_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # hot path: torch CUDA tensors [batch, n], float32 or float64
+    def forward(self, X, Y=None, stream=None):
+        return self._apply(gft_forward, X, Y, stream)
+
+    def inverse(self, Y, X=None, stream=None):
+        return self._apply(gft_inverse, Y, X, stream)
+
+    def dense_forward(self, X, Y=None, stream=None):
+        return self._apply(gft_dense_forward, X, Y, stream)
+
+    def dense_inverse(self, Y, X=None, stream=None):
+        return self._apply(gft_dense_inverse, Y, X, stream)
+
+    def _apply(self, fn, a, b, stream):
+        import torch
+        if not a.is_cuda:
+            raise ValueError("device tensors required (use execute_host for host buffers)")
+        if a.dim() != 2 or a.shape[1] != self.n or not a.is_contiguous():
+            raise ValueError("expected a contiguous [batch, %d] tensor" % self.n)
+        if b is None:
+            b = torch.empty_like(a)
+        dt = GFT_F64 if a.dtype == torch.float64 else GFT_F32
+        if a.dtype not in (torch.float32, torch.float64) or b.dtype != a.dtype:
+            raise ValueError("float32/float64 tensors of equal dtype required")
+        fn(self._h, a, b, a.shape[0], dt, stream)
+        return b
+
+    def execute_host(self, direction, in_host, out_host, workspace, chunk_rows, stream=None):
+        import torch
+        dt = GFT_F64 if in_host.dtype == torch.float64 else GFT_F32
+        gft_execute_host(self._h, direction, in_host, out_host, in_host.shape[0], dt, workspace,
+                         workspace.numel() * workspace.element_size(), chunk_rows, stream)
+        return out_host
+
+    def compile(self, dtype="f32"):
+        gft_plan_compile(self._h, dtype)
+
+    def info(self):
+        return gft_plan_info_get(self._h).as_dict()
+
+    def eigenvalues(self):
+        return gft_plan_eigenvalues(self._h, self.n)
+
+    def basis(self):
+        return gft_plan_basis(self._h, self.n)
+
+    def leaf_sizes(self):
+        return gft_plan_leaf_sizes(self._h)
+
+    def kernel_source(self, kind, dtype="f32"):
+        return gft_plan_kernel_source(self._h, kind, dtype)
+
+    def kernel_name(self, kind, dtype="f32"):
+        return gft_plan_kernel_name(self._h, kind, dtype)
+
+    def launch_config(self, kind, dtype, batch):
+        return gft_plan_launch_config(self._h, kind, dtype, batch)

@@ -1,0 +1,149 @@
+"""C-ABI boundary tests that need no GPU: the library loads, exports every symbol the
+header declares, and reports errors as status codes (never aborts)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import workloads
+from paper_1907_07875_b200 import gft as G
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    with open(os.path.join(ROOT, "include", "gft.h")) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"^GFT_API\s+[\w\s\*]*?\b(gft_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    L = G.lib()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(L, s), s
+    assert sorted(G.EXPORTS) == syms
+    assert G.gft_abi_version() == 1
+
+
+def test_library_has_no_hard_cuda_dependency():
+    # libcuda / libnvrtc are dlopen-ed so the library loads on CPU-only hosts
+    import subprocess
+    out = subprocess.run(["ldd", G.LIB_PATH], capture_output=True, text=True).stdout
+    assert "libcuda" not in out and "libnvrtc" not in out
+
+
+def test_status_strings():
+    for code, name in G.STATUS.items():
+        assert G.gft_status_str(code) == name
+
+
+def _path(n):
+    return workloads.path_graph(n)
+
+
+@pytest.mark.parametrize("case,status", [
+    ("bad_index", "GFT_ERR_INVALID_ARG"),
+    ("self_edge", "GFT_ERR_INVALID_ARG"),
+    ("duplicate", "GFT_ERR_INVALID_ARG"),
+    ("nan", "GFT_ERR_INVALID_ARG"),
+    ("inf_loop", "GFT_ERR_INVALID_ARG"),
+    ("not_involution", "GFT_ERR_NOT_INVOLUTION"),
+    ("phi_range", "GFT_ERR_NOT_INVOLUTION"),
+    ("not_symmetric", "GFT_ERR_NOT_SYMMETRIC"),
+    ("loop_asym", "GFT_ERR_NOT_SYMMETRIC"),
+    ("n0", "GFT_ERR_INVALID_ARG"),
+])
+def test_plan_create_errors(case, status):
+    s, d, w = _path(5)
+    loops, phi, n = None, None, 5
+    if case == "bad_index":
+        d = d.copy(); d[0] = 7
+    elif case == "self_edge":
+        d = d.copy(); d[1] = s[1]
+    elif case == "duplicate":
+        s = np.append(s, 1); d = np.append(d, 0); w = np.append(w, 1.0)
+    elif case == "nan":
+        w = w.copy(); w[2] = np.nan
+    elif case == "inf_loop":
+        loops = np.zeros(5); loops[1] = np.inf
+    elif case == "not_involution":
+        phi = np.array([1, 2, 0, 3, 4])
+    elif case == "phi_range":
+        phi = np.array([4, 3, 2, 1, 9])
+    elif case == "not_symmetric":
+        w = w.copy(); w[0] = 2.0
+        phi = np.array([4, 3, 2, 1, 0])
+    elif case == "loop_asym":
+        loops = np.zeros(5); loops[0] = 1.0
+        phi = np.array([4, 3, 2, 1, 0])
+    elif case == "n0":
+        n = 0
+        s = d = np.zeros(0, np.int32); w = np.zeros(0)
+    with pytest.raises(G.GFTError) as ei:
+        G.Plan(n, s, d, w, loops, phi, host_only=True)
+    assert ei.value.name == status
+    assert G.gft_last_error() != ""
+
+
+def test_zero_weights_dropped_and_negative_accepted():
+    s, d, w = _path(4)
+    w = np.array([1.0, 0.0, -0.5])
+    p = G.Plan(4, s, d, w, host_only=True)
+    assert p.info()["residual"] < 1e-12
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    s, d, w = _path(8)
+    p = G.Plan(8, s, d, w, dtypes=("f32",))
+    with pytest.raises(G.GFTError) as ei:
+        G.gft_forward(p.handle, 16, 16, 4, G.GFT_F32, 0)
+    assert ei.value.name in ("GFT_ERR_NO_DEVICE", "GFT_ERR_COMPILE")
+    # batch == 0 is a no-op, NULL pointers are rejected before touching the device
+    G.gft_forward(p.handle, 16, 16, 0, G.GFT_F32, 0)
+    with pytest.raises(G.GFTError) as ei:
+        G.gft_forward(p.handle, 0, 16, 4, G.GFT_F32, 0)
+    assert ei.value.name == "GFT_ERR_INVALID_ARG"
+    with pytest.raises(G.GFTError) as ei:
+        G.gft_forward(p.handle, 17, 16, 4, G.GFT_F32, 0)
+    assert ei.value.name == "GFT_ERR_ALIGNMENT"
+    with pytest.raises(G.GFTError) as ei:
+        G.gft_forward(p.handle, 16, 16, 4, G.GFT_F64, 0)    # f64 not prepared
+    assert ei.value.name == "GFT_ERR_UNSUPPORTED"
+
+
+def test_host_only_plan_has_no_kernels():
+    s, d, w = _path(6)
+    p = G.Plan(6, s, d, w, host_only=True)
+    with pytest.raises(G.GFTError) as ei:
+        p.kernel_source(0, "f32")
+    assert ei.value.name == "GFT_ERR_UNSUPPORTED"
+
+
+def test_kernel_source_is_plan_specialised():
+    cfg = workloads.config("cfg1")
+    p = G.Plan.from_config(cfg)
+    src = p.kernel_source(G.K_FAST_FWD, "f32")
+    name = p.kernel_name(G.K_FAST_FWD, "f32")
+    assert name in src and "gft_body" in src and "cp.async.bulk" in src
+    # 7 Haar units -> 7 add/sub pairs, leaves 1,1,2,4 -> 22 multiplies (FMA immediates)
+    assert src.count("= a_ + b_;") == 7
+    assert src.count("__fmul_rn(") + src.count("__fmaf_rn(") == 22
+    # inverse and dense kernels differ
+    assert p.kernel_name(G.K_FAST_INV, "f32") != name
+    assert p.kernel_source(G.K_DENSE_FWD, "f32").count("__fmaf_rn(") + \
+        p.kernel_source(G.K_DENSE_FWD, "f32").count("__fmul_rn(") == 64
+
+
+def test_nvrtc_compiles_generated_kernels_on_cpu():
+    """Kernel generation + NVRTC compilation need no GPU (module loading does)."""
+    cfg = workloads.config("cfg2b")
+    p = G.Plan.from_config(cfg, no_cubin_cache=True, dtypes=("f32",))
+    p.compile("f32")
+    assert p.info()["kernels_ready"] & 1
