@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the fused fast-GFT hot path on B200 (contract: see DESIGN.md §Measurement).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config cfg2] [--impl ours|reference]
+
+One step = one fast forward GFT + one fast inverse GFT over the config's whole batch
+(rows H1-H6 of SURVEY §8(a)); the dense U^T x kernel (H7) is timed beside it.
+Default workload = BASELINE.json configs[1] (cfg2: symmetric line N=16, 2^22 signals).
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "fast-GFT signals/sec and achieved HBM GB/s (% roofline) vs dense Uᵀx"
+KIND_NAMES = {0: "fast_fwd", 1: "fast_inv", 2: "dense_fwd", 3: "dense_inv"}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy kernel, measured)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def load_traffic(kernel_prefix, config):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        for row in d.get("kernels", []):
+            if row.get("config") == config and row.get("kind") == kernel_prefix:
+                return row.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks / throttle reasons while the GPU works."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index):
+        self.samples = []
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                t = time.perf_counter()
+                sm = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                fn = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    self.nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                rs = fn(self.h)
+                self.samples.append((t, sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def start(self):
+        if self.ok:
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
+
+    def stop(self):
+        if self.ok:
+            self._stop.set()
+            self.th.join()
+
+    def summary(self, t0, t1):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "nvml unavailable"}
+        win = [s for s in self.samples if t0 <= s[0] <= t1]
+        note = "samples inside timed region"
+        if not win:   # timed region shorter than the sampling period: nearest samples
+            win = sorted(self.samples, key=lambda s: min(abs(s[0] - t0), abs(s[0] - t1)))[:5]
+            note = "timed region shorter than sampling period; nearest samples"
+        reasons = set()
+        for _, _, r in win:
+            for bit, name in self.REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median([s[1] for s in win]) if win else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons), "samples": len(win),
+                "note": note}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def time_kernel(fn, stream, warmup, iters):
+    import torch
+    for _ in range(warmup):
+        fn()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record(stream)
+    for _ in range(iters):
+        fn()
+    e.record(stream)
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def config_table(args, stream, hbm, device):
+    """Every BASELINE config: fast fwd/inv and dense fwd/inv, device-resident N(0,1)."""
+    import torch
+    import workloads
+    from paper_1907_07875_b200 import gft
+    rows = []
+    for name, dtype in (("cfg1", "f32"), ("cfg2", "f32"), ("cfg2b", "f32"), ("cfg3", "f32"),
+                        ("cfg4", "f32"), ("cfg4", "f64"), ("cfg5a", "f32"), ("cfg5b", "f32")):
+        cfg = workloads.config(name)
+        plan = gft.Plan.from_config(cfg, dtypes=(dtype,))
+        tdt = torch.float64 if dtype == "f64" else torch.float32
+        g = torch.Generator(device=device).manual_seed(cfg.seed)
+        X = torch.randn(cfg.batch, cfg.n, generator=g, device=device, dtype=tdt)
+        Y = torch.empty_like(X)
+        esz = X.element_size()
+        nbytes = 2 * cfg.batch * cfg.n * esz
+        row = {"config": name, "dtype": dtype, "n": cfg.n, "batch": cfg.batch,
+               "units_per_level": plan.info()["units_per_level"], "leaves": plan.leaf_sizes()}
+        for kind, f in ((0, plan.forward), (1, plan.inverse), (2, plan.dense_forward),
+                        (3, plan.dense_inverse)):
+            ms = time_kernel(lambda: f(X, Y, stream), stream, 3, args.table_iters)
+            row[KIND_NAMES[kind]] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
+                                     "frac": round(nbytes / ms / 1e6 / hbm, 4),
+                                     "signals_per_s": cfg.batch / ms * 1e3}
+        row["fast_vs_dense_fwd"] = round(row["dense_fwd"]["ms"] / row["fast_fwd"]["ms"], 3)
+        row["fast_vs_dense_inv"] = round(row["dense_inv"]["ms"] / row["fast_inv"]["ms"], 3)
+        rows.append(row)
+        del X, Y
+        plan.close()
+    return rows
+
+
+def cpu_oracle_step_time(cfg, X_cpu, budget_s):
+    """The oracle (as it stands) on the host: dense fp64 forward + inverse."""
+    import oracle
+    L = oracle.laplacian(cfg.n, cfg.src, cfg.dst, cfg.w, cfg.self_loops)
+    t = time.perf_counter()
+    lam, U = oracle.gft_basis(L)
+    t_eig = time.perf_counter() - t
+    Xn = X_cpu.numpy()
+    reps, spent, times = 0, 0.0, []
+    while spent < budget_s and reps < 50:
+        t = time.perf_counter()
+        Y = oracle.forward(Xn, U)
+        oracle.inverse(Y, U)
+        dt = time.perf_counter() - t
+        times.append(dt)
+        spent += dt
+        reps += 1
+    return min(times), statistics.median(times), reps, t_eig
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import workloads
+    cfg = workloads.config(args.config)
+    rows = min(cfg.batch, args.ref_rows)
+    X = workloads.signals(cfg, batch=rows, dtype="f32")
+    import oracle
+    L = oracle.laplacian(cfg.n, cfg.src, cfg.dst, cfg.w, cfg.self_loops)
+    lam, U = oracle.gft_basis(L)
+    Xn = X.numpy()
+    for _ in range(args.warmup):
+        oracle.inverse(oracle.forward(Xn, U), U)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.inverse(oracle.forward(Xn, U), U)
+    dt = (time.perf_counter() - t) / args.steps
+    value = rows / dt
+    cores = blas_threads()
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "signals/s",
+           "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": args.config, "batch": rows, "n": cfg.n},
+           "cpu_baseline": {"value": value, "unit": "signals/s", "cores": cores, "kind": "oracle",
+                            "sample": "%d of %d rows of %s, dense fp64 Y=XU then X=YU^T (numpy BLAS)"
+                                      % (rows, cfg.batch, args.config)},
+           "e2e": {"value": value, "unit": "signals/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-table", action="store_true", help="skip the all-config side table")
+    ap.add_argument("--table-iters", type=int, default=20)
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle CPU timing")
+    ap.add_argument("--ref-rows", type=int, default=1 << 20)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import workloads
+    from paper_1907_07875_b200 import gft
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    stream = torch.cuda.current_stream()
+    hbm, peak_src = load_peaks()
+
+    cfg = workloads.config(args.config)
+    dtype = cfg.dtypes[0]
+    plan = gft.Plan.from_config(cfg, dtypes=(dtype,))
+    # weak scaling: every rank transforms its own full batch (seed offset by rank)
+    X_cpu = workloads.signals(cfg, dtype=dtype, seed=cfg.seed + rank)
+    X = X_cpu.to(device)
+    Y = torch.empty_like(X)
+    Z = torch.empty_like(X)
+    B, n, esz = cfg.batch, cfg.n, X.element_size()
+
+    def step():
+        plan.forward(X, Y, stream)
+        plan.inverse(Y, Z, stream)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    t_start.record(stream)
+    for i in range(args.steps):
+        a, b, c = ev[i]
+        a.record(stream)
+        plan.forward(X, Y, stream)
+        b.record(stream)
+        plan.inverse(Y, Z, stream)
+        c.record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    w1 = time.perf_counter()
+    if dist:
+        dist.barrier()
+    sampler.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    fwd_ms = sum(ev[i][0].elapsed_time(ev[i][1]) for i in range(args.steps)) / args.steps
+    inv_ms = sum(ev[i][1].elapsed_time(ev[i][2]) for i in range(args.steps)) / args.steps
+    ms_step = total_ms / args.steps
+    if dist:
+        t = torch.tensor([ms_step], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = B * ws / (ms_step * 1e-3)
+    clocks = sampler.summary(w0, w1)
+
+    # dominant kernel roofline (algorithmic bytes: read x once + write y once)
+    bytes_per_launch = 2 * B * n * esz
+    dom_kind, dom_ms = (0, fwd_ms) if fwd_ms >= inv_ms else (1, inv_ms)
+    achieved = bytes_per_launch / (dom_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": load_traffic(KIND_NAMES[dom_kind], args.config),
+                "kernel": plan.kernel_name(dom_kind, dtype), "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": round(dom_ms, 5),
+                "nominal_8tbs_frac": round(achieved / 8000.0, 4)}
+
+    # dense U^T x comparison (same I/O, same stream)
+    dense_fwd = time_kernel(lambda: plan.dense_forward(X, Y, stream), stream, 3, 50)
+    dense_inv = time_kernel(lambda: plan.dense_inverse(Y, Z, stream), stream, 3, 50)
+
+    # end to end through the C ABI with pinned HOST buffers (H2D + kernel + D2H timed)
+    Xh = X_cpu.pin_memory()
+    Yh = torch.empty_like(Xh).pin_memory()
+    Zh = torch.empty_like(Xh).pin_memory()
+    chunk = 1 << 18
+    wsb = torch.empty(2 * chunk * n, dtype=X.dtype, device=device)
+
+    def e2e_step():
+        plan.execute_host(0, Xh, Yh, wsb, chunk, stream)
+        plan.execute_host(1, Yh, Zh, wsb, chunk, stream)
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    s_e, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s_e.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e_e.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = s_e.elapsed_time(e_e) / args.e2e_steps
+    if dist:
+        t = torch.tensor([e2e_ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    roundtrip_err = float(((Zh.double() - X_cpu.double()).norm(dim=1) / X_cpu.double().norm(dim=1)).max())
+
+    table = None
+    if rank == 0 and not args.no_table:
+        table = config_table(args, stream, hbm, device)
+
+    cpu = None
+    if rank == 0:
+        best, med, reps, t_eig = cpu_oracle_step_time(cfg, X_cpu, args.cpu_budget)
+        cpu = {"value": B / best, "unit": "signals/s", "cores": blas_threads(), "kind": "oracle",
+               "sample": "full %s batch (%d x %d), oracle dense fp64 forward+inverse, best of %d "
+                         "(median %.3fs); eigensolve %.3fs excluded" % (args.config, B, n, reps, med, t_eig)}
+
+    if dist:
+        dist.barrier()
+    if rank == 0:
+        info = plan.info()
+        out = {
+            "metric": METRIC, "value": value, "unit": "signals/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": "%s: %s" % (args.config, cfg.description), "n": n,
+                       "global_batch": B * ws, "per_gpu_batch": B,
+                       "step": "fast forward GFT + fast inverse GFT of the whole batch",
+                       "l2": "inputs larger than L2 (%d MiB read+written per launch)" % (bytes_per_launch >> 20),
+                       "units_per_level": info["units_per_level"], "leaves": plan.leaf_sizes(),
+                       "parallelism": "batch-sharded, no collective" if ws > 1 else "single GPU"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": B * ws / (e2e_ms * 1e-3), "unit": "signals/s",
+                    "h2d_bytes_per_step": 2 * B * n * esz, "d2h_bytes_per_step": 2 * B * n * esz,
+                    "ms_per_step": e2e_ms, "roundtrip_max_rel_err": roundtrip_err,
+                    "path": "gft_execute_host (pinned host, 2 streams, 2^18-row chunks)"},
+            "gpu_launches": 2 * args.steps,
+            "kernels": {"fast_fwd_ms": round(fwd_ms, 5), "fast_inv_ms": round(inv_ms, 5),
+                        "dense_fwd_ms": round(dense_fwd, 5), "dense_inv_ms": round(dense_inv, 5),
+                        "fast_vs_dense": round((dense_fwd + dense_inv) / (fwd_ms + inv_ms), 3)},
+            "clocks": clocks,
+            "configs_table": table,
+        }
+        print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+    plan.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
