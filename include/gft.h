@@ -78,6 +78,8 @@ typedef struct {
 
 #define GFT_FLAG_HOST_ONLY 1u      /* build the factorisation only; no kernel codegen (CPU use) */
 #define GFT_FLAG_NO_CUBIN_CACHE 2u /* always run NVRTC even if an AOT cubin for the plan exists */
+#define GFT_FLAG_NO_TENSOR_CORES 4u /* fp32 leaves >= 32 stay on CUDA-core FMA instead of
+                                       tcgen05 3xTF32 micro-GEMMs (ablation / comparison) */
 
 typedef struct {
   int32_t n;

@@ -32,20 +32,24 @@ SOURCES = ["plan.cpp", "search.cpp", "codegen.cpp", "cuda_rt.cpp", "capi.cpp"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
+SKELETONS = {"kernel_skeleton.cuh": "skeleton_inc.h", "kernel_tc_skeleton.cuh": "skeleton_tc_inc.h"}
+
+
 def _write_skeleton_inc():
-    with open(os.path.join(CSRC, "kernel_skeleton.cuh")) as f:
-        text = f.read()
-    assert ")GFTSKEL\"" not in text
-    out = os.path.join(CSRC, "skeleton_inc.h")
-    new = 'R"GFTSKEL(' + text + ')GFTSKEL"\n'
-    if not os.path.exists(out) or open(out).read() != new:
-        with open(out, "w") as f:
-            f.write(new)
+    for src, dst in SKELETONS.items():
+        with open(os.path.join(CSRC, src)) as f:
+            text = f.read()
+        assert ")GFTSKEL\"" not in text
+        out = os.path.join(CSRC, dst)
+        new = 'R"GFTSKEL(' + text + ')GFTSKEL"\n'
+        if not os.path.exists(out) or open(out).read() != new:
+            with open(out, "w") as f:
+                f.write(new)
 
 
 def _stamp():
     h = hashlib.sha256()
-    for s in SOURCES + ["plan.hpp", "kernels.hpp", "kernel_skeleton.cuh"]:
+    for s in SOURCES + ["plan.hpp", "kernels.hpp"] + list(SKELETONS):
         with open(os.path.join(CSRC, s), "rb") as f:
             h.update(f.read())
     with open(os.path.join(ROOT, "include", "gft.h"), "rb") as f:

@@ -7,6 +7,7 @@
 // becomes the register index the result is written to.  There are no
 // tables to fetch on the device: per signal the kernel executes exactly
 // 2*units + sum_k k^2 arithmetic instructions (+ explicit scale fixes, if any).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -17,9 +18,12 @@
 
 namespace gft {
 
-// The device skeleton, embedded at build time (build.py writes skeleton_inc.h).
+// The device skeletons, embedded at build time (build.py writes *_inc.h).
 static const char* kSkeleton =
 #include "skeleton_inc.h"
+    ;
+static const char* kSkeletonTC =
+#include "skeleton_tc_inc.h"
     ;
 
 KernelCfg choose_cfg(int n, int dtype) {
@@ -150,12 +154,259 @@ void emit_dense(std::ostringstream& o, const Plan& P, int dtype, bool forward) {
   }
 }
 
+// ------------------------------------------------------------------------------------
+// Tensor-core (tcgen05, 3xTF32) variant for plans with large leaves
+// ------------------------------------------------------------------------------------
+struct TcLeaf {
+  int leaf, k, kp8, kp32, np;
+  int hi_col, lo_col, d_col;     // TMEM columns
+  int bhi_off, blo_off;          // byte offsets in the SMEM B region
+};
+
+int ru(int v, int m) { return (v + m - 1) / m * m; }
+
+// host-side cvt.rna.tf32.f32: round to nearest (ties away) on the low 13 mantissa bits
+float tf32_rna_host(float v) {
+  uint32_t u;
+  std::memcpy(&u, &v, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return v;
+  u = (u + 0x1000u) & ~0x1fffu;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+bool plan_tc(const Plan& P, int dtype, int stages, std::vector<TcLeaf>& out, int& tmem_cols,
+             int& b_bytes) {
+  out.clear();
+  if (dtype != GFT_F32 || P.n % 32 != 0 || P.n > 256) return false;
+  std::vector<int> order;
+  for (int l = 0; l < (int)P.leaves.size(); ++l)
+    if (P.leaves[l].k >= 32) order.push_back(l);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return P.leaves[a].k > P.leaves[b].k; });
+  const int tile = 128 * P.n * 4;
+  int cols = 0, bytes = 0;
+  for (int l : order) {
+    TcLeaf t;
+    t.leaf = l;
+    t.k = P.leaves[l].k;
+    t.kp8 = ru(t.k, 8);
+    t.kp32 = ru(t.k, 32);
+    t.np = ru(t.k, 16);
+    const int need = 2 * ru(t.kp8, 32) + ru(t.np, 32);
+    const int bsz = 2 * t.np * t.kp32 * 4;
+    if (cols + need > 512 || stages * tile + bytes + bsz > 200 * 1024 || t.np > 256) continue;
+    t.hi_col = cols;
+    t.lo_col = cols + ru(t.kp8, 32);
+    t.d_col = cols + 2 * ru(t.kp8, 32);
+    cols += need;
+    t.bhi_off = bytes;
+    t.blo_off = bytes + bsz / 2;
+    bytes += bsz;
+    out.push_back(t);
+  }
+  if (out.empty()) return false;
+  tmem_cols = 32;
+  while (tmem_cols < cols) tmem_cols *= 2;
+  b_bytes = bytes;
+  return true;
+}
+
+void emit_tmem_st(std::ostringstream& o, const std::string& arr, int col0, int count) {
+  // split into power-of-two chunks <= 128 columns
+  int c = 0;
+  while (c < count) {
+    int w = 128;
+    while (w > count - c) w /= 2;
+    o << "  asm volatile(\"tcgen05.st.sync.aligned.32x32b.x" << w << ".b32 [%0], {";
+    for (int i = 0; i < w; ++i) o << (i ? ", " : "") << "%" << (i + 1);
+    o << "};\" :: \"r\"(tm + " << (col0 + c) << "u)";
+    for (int i = 0; i < w; ++i) o << ", \"r\"(" << arr << "[" << (c + i) << "])";
+    o << " : \"memory\");\n";
+    c += w;
+  }
+}
+
+void emit_tmem_ld(std::ostringstream& o, const std::string& arr, int col0, int count) {
+  int c = 0;
+  while (c < count) {
+    int w = 128;
+    while (w > count - c) w /= 2;
+    o << "  asm volatile(\"tcgen05.ld.sync.aligned.32x32b.x" << w << ".b32 {";
+    for (int i = 0; i < w; ++i) o << (i ? ", " : "") << "%" << i;
+    o << "}, [%" << w << "];\\n\\ttcgen05.wait::ld.sync.aligned;\" : ";
+    for (int i = 0; i < w; ++i) o << (i ? ", " : "") << "\"=r\"(" << arr << "[" << (c + i) << "])";
+    o << " : \"r\"(tm + " << (col0 + c) << "u) : \"memory\");\n";
+    c += w;
+  }
+}
+
+void emit_units(std::ostringstream& o, const Plan& P, const char* arr, bool reverse, int dtype) {
+  o << "  float a_, b_;\n";
+  auto one = [&](const Op& op) {
+    if (op.kind == Op::UNIT)
+      o << "  a_ = " << arr << "[" << op.a << "]; b_ = " << arr << "[" << op.b << "]; " << arr << "["
+        << op.a << "] = a_ + b_; " << arr << "[" << op.b << "] = a_ - b_;\n";
+    else
+      o << "  " << arr << "[" << op.a << "] = " << arr << "[" << op.a << "] * "
+        << lit(std::pow(2.0, 0.5 * op.m), dtype) << ";\n";
+  };
+  if (!reverse) for (const Op& op : P.ops) one(op);
+  else for (auto it = P.ops.rbegin(); it != P.ops.rend(); ++it) one(*it);
+  o << "  (void)a_; (void)b_;\n";
+}
+
+void generate_tc(const Plan& P, bool forward, const std::vector<TcLeaf>& T, std::ostringstream& o) {
+  const int dtype = GFT_F32;
+  std::vector<char> is_tc(P.leaves.size(), 0);
+  for (const auto& t : T) is_tc[t.leaf] = 1;
+  // ---- B operands, atom order (leaf, hi|lo, k-atom, row n, 32 k) ----
+  std::vector<float> B;
+  for (const auto& t : T) {
+    const Leaf& lf = P.leaves[t.leaf];
+    for (int part = 0; part < 2; ++part)
+      for (int a = 0; a < t.kp32 / 32; ++a)
+        for (int n = 0; n < t.np; ++n)
+          for (int kk = 32 * a; kk < 32 * a + 32; ++kk) {
+            float v = 0.f;
+            if (n < t.k && kk < t.k)   // forward: B[n=r][k=c] = M[r][c]; inverse: B[n=c][k=r] = M[r][c]
+              v = (float)(forward ? lf.M[(size_t)n * t.k + kk] : lf.M[(size_t)kk * t.k + n]);
+            const float hi = tf32_rna_host(v);
+            B.push_back(part == 0 ? hi : v - hi);
+          }
+  }
+  o << "#define GFT_B_FLOATS " << B.size() << "\n";
+  o << "__device__ __align__(16) const float gft_tcB[" << B.size() << "] = {\n";
+  for (size_t i = 0; i < B.size(); ++i) {
+    char buf[48];
+    std::snprintf(buf, sizeof buf, "%af,", (double)B[i]);
+    o << buf << ((i % 8 == 7) ? "\n" : "");
+  }
+  o << "};\n";
+  // ---- front ----
+  o << "static __device__ __forceinline__ void gft_front(float (&x)[GFT_N]) {\n";
+  if (forward) emit_units(o, P, "x", false, dtype);
+  o << "}\n";
+  // ---- stage A (hi/lo split of the big-leaf inputs -> TMEM) ----
+  o << "static __device__ __forceinline__ void gft_stage_a(const float (&x)[GFT_N], u32 tm) {\n";
+  for (const auto& t : T) {
+    const Leaf& lf = P.leaves[t.leaf];
+    for (int c0 = 0; c0 < t.kp8; c0 += 32) {   // 32-column chunks keep register pressure low
+      const int w = std::min(32, t.kp8 - c0);
+      o << "  { u32 h[" << w << "], l[" << w << "];\n";
+      for (int c = c0; c < c0 + w; ++c) {
+        if (c < t.k) {
+          const int src = forward ? lf.pos[c] : lf.slot[c];
+          o << "  h[" << c - c0 << "] = tf32_rna(x[" << src << "]); l[" << c - c0 << "] = __float_as_uint(x["
+            << src << "] - __uint_as_float(h[" << c - c0 << "]));\n";
+        } else {
+          o << "  h[" << c - c0 << "] = 0u; l[" << c - c0 << "] = 0u;\n";
+        }
+      }
+      emit_tmem_st(o, "h", t.hi_col + c0, w);
+      emit_tmem_st(o, "l", t.lo_col + c0, w);
+      o << "  }\n";
+    }
+  }
+  o << "}\n";
+  // ---- MMA issue (one thread) ----
+  o << "static __device__ __forceinline__ void gft_issue(u32 tm, u32 bsm) {\n";
+  for (const auto& t : T) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(t.np >> 3) << 17) | (8u << 24);
+    const int ksteps = t.kp8 / 8;
+    const int atom_bytes = t.np * 128;
+    for (int pass = 0; pass < 3; ++pass) {
+      // pass 0: A_hi B_hi, pass 1: A_hi B_lo, pass 2: A_lo B_hi
+      const int acol = pass == 2 ? t.lo_col : t.hi_col;
+      const int boff = pass == 1 ? t.blo_off : t.bhi_off;
+      for (int j = 0; j < ksteps; ++j) {
+        const int bo = boff + (j / 4) * atom_bytes + (j % 4) * 32;
+        o << "  mma_ts(tm + " << t.d_col << "u, tm + " << (acol + 8 * j) << "u, smem_desc_sw128(bsm + " << bo
+          << "u), " << idesc << "u, " << ((pass == 0 && j == 0) ? 0 : 1) << "u);\n";
+      }
+    }
+  }
+  o << "}\n";
+  // ---- small leaves on CUDA cores ----
+  o << "static __device__ __forceinline__ void gft_fma(const float (&x)[GFT_N], float (&y)[GFT_N]) {\n";
+  for (size_t l = 0; l < P.leaves.size(); ++l) {
+    if (is_tc[l]) continue;
+    const Leaf& lf = P.leaves[l];
+    std::vector<std::string> in(lf.k);
+    for (int i = 0; i < lf.k; ++i) in[i] = xs("x", forward ? lf.pos[i] : lf.slot[i]);
+    for (int i = 0; i < lf.k; ++i) {
+      std::vector<double> coef(lf.k);
+      for (int j = 0; j < lf.k; ++j) coef[j] = forward ? lf.M[(size_t)i * lf.k + j] : lf.M[(size_t)j * lf.k + i];
+      emit_dot(o, xs("y", forward ? lf.slot[i] : lf.pos[i]), coef, in, dtype);
+    }
+  }
+  o << "}\n";
+  // ---- epilogue: accumulators -> registers ----
+  o << "static __device__ __forceinline__ void gft_epi(u32 tm, float (&y)[GFT_N]) {\n";
+  for (const auto& t : T) {
+    const Leaf& lf = P.leaves[t.leaf];
+    for (int r0 = 0; r0 < t.k; r0 += 32) {
+      const int w = std::min(32, t.np - r0);
+      o << "  { u32 d[" << w << "];\n";
+      emit_tmem_ld(o, "d", t.d_col + r0, w);
+      for (int r = r0; r < std::min(t.k, r0 + w); ++r)
+        o << "  y[" << (forward ? lf.slot[r] : lf.pos[r]) << "] = __uint_as_float(d[" << r - r0 << "]);\n";
+      o << "  }\n";
+    }
+  }
+  o << "}\n";
+  // ---- back ----
+  o << "static __device__ __forceinline__ void gft_back(float (&y)[GFT_N]) {\n";
+  if (!forward) emit_units(o, P, "y", true, dtype);
+  o << "}\n";
+}
+
 }  // namespace
 
-void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k) {
+void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc) {
   k.kind = kind;
   k.dtype = dtype;
   k.cfg = choose_cfg(P.n, dtype);
+  static const char* kKindNameTC[] = {"fwdtc", "invtc"};
+  if (allow_tc && (kind == K_FAST_FWD || kind == K_FAST_INV)) {
+    std::vector<TcLeaf> T;
+    int tmem_cols = 0, b_bytes = 0;
+    const int stages = 2;
+    if (plan_tc(P, dtype, stages, T, tmem_cols, b_bytes)) {
+      KernelCfg& c = k.cfg;
+      c.tc = 1;
+      c.stages = stages;
+      c.mode = 0;
+      c.boxc = 32;
+      c.swz_mask = 7;
+      c.vec = 4;
+      c.R = 4;
+      c.warps = 5;
+      c.tc_b_bytes = b_bytes;
+      c.tc_tmem_cols = tmem_cols;
+      std::ostringstream gen;
+      generate_tc(P, kind == K_FAST_FWD, T, gen);
+      std::ostringstream pre;
+      pre << "#define GFT_N " << c.n << "\n#define GFT_STAGES " << c.stages << "\n#define GFT_TMEM_COLS "
+          << tmem_cols << "\n";
+      const std::string skel(kSkeletonTC);
+      const std::string marker = "// @@GFT_GENERATED@@";
+      const size_t at = skel.find(marker);
+      if (at == std::string::npos) fail(GFT_ERR_COMPILE, "TC skeleton marker missing");
+      const std::string key = pre.str() + gen.str() + skel;
+      char hbuf[32];
+      std::snprintf(hbuf, sizeof hbuf, "%016llx", (unsigned long long)fnv1a(key));
+      k.name = std::string("gft_") + kKindNameTC[kind] + "_f32_n" + std::to_string(c.n) + "_" + hbuf;
+      std::ostringstream src;
+      src << "// generated by paper_1907_07875_b200 codegen.cpp — plan-specialised GFT kernel with\n"
+          << "// tcgen05 3xTF32 leaves (" << T.size() << " tensor-core leaves)\n"
+          << pre.str() << "#define GFT_KNAME " << k.name << "\n"
+          << skel.substr(0, at) << gen.str() << skel.substr(at);
+      k.source = src.str();
+      return;
+    }
+  }
   const KernelCfg& c = k.cfg;
   std::ostringstream body;
   body << "static __device__ __forceinline__ void gft_body(elem_t (&x)[GFT_N], elem_t (&y)[GFT_N]) {\n";

@@ -195,7 +195,7 @@ LoadedFn& ensure_loaded(Kernel& k, CUcontext ctx, bool allow_cache) {
   ck(d.cuFuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem),
      "cuFuncSetAttribute(max dynamic smem)");
   int occ = 0;
-  ck(d.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, k.cfg.warps * 32, smem), "occupancy");
+  ck(d.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, k.cfg.threads(), smem), "occupancy");
   if (occ < 1) fail(GFT_ERR_CUDA, "kernel " + k.name + " cannot be resident (occupancy 0)");
   CUdevice dev;
   ck(d.cuCtxGetDevice(&dev), "cuCtxGetDevice");
@@ -272,9 +272,9 @@ void kernel_launch_config(Kernel& k, int64_t batch, int* grid, int* block, int* 
   LoadedFn& L = ensure_loaded(k, ctx, allow_cache);
   const int64_t rows = std::min<int64_t>(batch, kMaxRowsPerLaunch);
   const int64_t tiles = (rows + k.cfg.tile_rows() - 1) / k.cfg.tile_rows();
-  const int64_t ctas = (tiles + k.cfg.warps - 1) / k.cfg.warps;
+  const int64_t ctas = (tiles + k.cfg.tiles_per_cta() - 1) / k.cfg.tiles_per_cta();
   if (grid) *grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, L.grid_max));
-  if (block) *block = k.cfg.warps * 32;
+  if (block) *block = k.cfg.threads();
   if (smem) *smem = k.cfg.smem_bytes();
   if (regs) *regs = L.regs;
 }
@@ -299,13 +299,13 @@ void launch_kernel(Kernel& k, const void* in, void* out, int64_t batch, void* st
       encode_map(&tout, k, pout, rows);
     }
     const int64_t tiles = (rows + c.tile_rows() - 1) / c.tile_rows();
-    const int64_t ctas = (tiles + c.warps - 1) / c.warps;
+    const int64_t ctas = (tiles + c.tiles_per_cta() - 1) / c.tiles_per_cta();
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, L.grid_max));
     long long nrows = rows;
     const void* xin = pin;
     void* xout = pout;
     void* args[] = {&tin, &tout, &xin, &xout, &nrows};
-    ck(d.cuLaunchKernel((CUfunction)L.fn, grid, 1, 1, c.warps * 32, 1, 1, c.smem_bytes(),
+    ck(d.cuLaunchKernel((CUfunction)L.fn, grid, 1, 1, c.threads(), 1, 1, c.smem_bytes(),
                         (CUstream)stream, args, nullptr),
        "cuLaunchKernel");
   }

@@ -21,9 +21,19 @@ struct KernelCfg {
   int mode = 0;                 // 0 TMA tensor 2-D + swizzle, 1 bulk 1-D
   int boxc = 0, swz_mask = 0;   // TMA box columns, swizzle mask (7/3/1/0)
   int vec = 1;                  // elements per SMEM vector access
-  int tile_rows() const { return 32 * R; }
+  // tensor-core variant (kernel_tc_skeleton.cuh): one 128-row tile per CTA iteration,
+  // 4 compute warps + 1 TMA warp, big leaves as tcgen05 3xTF32 micro-GEMMs
+  int tc = 0;
+  int tc_b_bytes = 0;           // SMEM bytes of the B operands
+  int tc_tmem_cols = 0;         // TMEM columns allocated
+  int tile_rows() const { return tc ? 128 : 32 * R; }
   int tile_bytes() const { return tile_rows() * n * elem; }
-  int smem_bytes() const { return warps * stages * tile_bytes() + warps * stages * 8 + 1024; }
+  int threads() const { return tc ? 160 : warps * 32; }
+  int tiles_per_cta() const { return tc ? 1 : warps; }   // tiles processed concurrently per CTA
+  int smem_bytes() const {
+    if (tc) return stages * tile_bytes() + tc_b_bytes + (2 * stages + 1) * 8 + 16 + 1024;
+    return warps * stages * tile_bytes() + warps * stages * 8 + 1024;
+  }
   int swizzle_bytes() const { return swz_mask == 7 ? 128 : swz_mask == 3 ? 64 : swz_mask == 1 ? 32 : 0; }
 };
 
@@ -47,7 +57,8 @@ struct Kernel {
 };
 
 // Emits the full CUDA source (prelude + gft_body + skeleton) for a plan.
-void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k);
+// allow_tc: fast kernels of fp32 plans with leaves >= 32 use the tcgen05 3xTF32 skeleton.
+void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc);
 
 // Compiles k.source to an sm_100a cubin (AOT cache lookup first unless disabled).
 void compile_kernel(Kernel& k, bool allow_cache);

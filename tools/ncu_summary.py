@@ -1,0 +1,117 @@
+"""Summarise ncu captures (run here, on the CPU box) into profiles/.
+
+  python tools/ncu_summary.py --round r01 [--dir gpurun_out]
+
+For every gpurun_out/prof_<config>_k<kind>.ncu-rep: exports the raw page as CSV to
+profiles/<round>/raw_<config>_k<kind>.csv and collects the headline metrics into
+profiles/<round>/ncu_summary.md and profiles/ncu_summary.json (read by bench.py for the
+roofline "traffic" field: dram read+write bytes per launch).  The launch list
+(launches.csv, gpu__time_duration per launch) is copied and summarised as kernel shares.
+"""
+import argparse
+import csv
+import glob
+import io
+import json
+import os
+import re
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KIND = {"0": "fast_fwd", "1": "fast_inv", "2": "dense_fwd", "3": "dense_inv"}
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "dram read"),
+    ("dram__bytes_write.sum", "dram write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram % peak"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
+    ("launch__registers_per_thread", "regs"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+    ("smsp__inst_executed.sum", "instructions"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+]
+
+
+def to_bytes(val, unit):
+    v = float(val.replace(",", ""))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
+    return v * scale
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--round", default="r01")
+    ap.add_argument("--dir", default=os.path.join(ROOT, "gpurun_out"))
+    a = ap.parse_args()
+    outdir = os.path.join(ROOT, "profiles", a.round)
+    os.makedirs(outdir, exist_ok=True)
+    rows = []
+    for rep in sorted(glob.glob(os.path.join(a.dir, "prof_*.ncu-rep"))):
+        m = re.match(r"prof_(\w+?)_k(\d)(?:_(\w+))?\.ncu-rep", os.path.basename(rep))
+        if not m:
+            continue
+        cfg, kind, tag = m.group(1), m.group(2), m.group(3)
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        base = "raw_%s_k%s%s.csv" % (cfg, kind, "_" + tag if tag else "")
+        with open(os.path.join(outdir, base), "w") as f:
+            f.write(raw)
+        r = list(csv.reader(io.StringIO(raw)))
+        if len(r) < 3:
+            continue
+        hdr, units, vals = r[0], r[1], r[2]
+        get = lambda k: (vals[hdr.index(k)], units[hdr.index(k)]) if k in hdr else (None, None)
+        name = get("Kernel Name")[0]
+        row = {"config": cfg, "kind": KIND[kind], "tag": tag, "kernel": name}
+        for k, label in METRICS:
+            v, u = get(k)
+            row[label] = None if v is None else (v + (" " + u if u else ""))
+        rb, ru = get("dram__bytes_read.sum")
+        wb, wu = get("dram__bytes_write.sum")
+        if rb is not None:
+            row["dram_bytes_per_launch"] = to_bytes(rb, ru) + to_bytes(wb, wu)
+        rows.append(row)
+    # launch list
+    shares = {}
+    lc = os.path.join(a.dir, "launches.csv")
+    if os.path.exists(lc):
+        with open(lc) as f:
+            text = f.read()
+        with open(os.path.join(outdir, "launches.csv"), "w") as f:
+            f.write(text)
+        lines = [l for l in text.splitlines() if l.startswith('"')]
+        rd = list(csv.reader(io.StringIO("\n".join(lines))))
+        if rd:
+            h = rd[0]
+            for rr in rd[1:]:
+                if rr[h.index("Metric Name")] != "gpu__time_duration.sum":
+                    continue
+                nm = rr[h.index("Kernel Name")]
+                key = re.sub(r"_[0-9a-f]{16}$", "", nm)
+                shares[key] = shares.get(key, 0.0) + float(rr[h.index("Metric Value")].replace(",", ""))
+    tot = sum(shares.values()) or 1.0
+    with open(os.path.join(outdir, "ncu_summary.md"), "w") as f:
+        f.write("# ncu summary (%s)\n\nSource: `ncu --set full --clock-control none` captures of "
+                "`tools/profile_kernel.py` (one launch, cold cache, serialised).  Durations under ncu are "
+                "not bench numbers.\n\n" % a.round)
+        labels = ["config", "kind", "tag"] + [l for _, l in METRICS] + ["dram_bytes_per_launch"]
+        f.write("| " + " | ".join(labels) + " |\n|" + "---|" * len(labels) + "\n")
+        for r in rows:
+            f.write("| " + " | ".join(str(r.get(l)) for l in labels) + " |\n")
+        if shares:
+            f.write("\n## Launch list shares (bench.py run under `ncu --metrics gpu__time_duration.sum`)\n\n")
+            f.write("| kernel | total ns | share |\n|---|---|---|\n")
+            for k, v in sorted(shares.items(), key=lambda kv: -kv[1]):
+                f.write("| %s | %.0f | %.3f |\n" % (k, v, v / tot))
+    with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
+        json.dump({"round": a.round, "kernels": rows, "launch_shares": {k: v / tot for k, v in shares.items()}},
+                  f, indent=1)
+    print("wrote", outdir)
+
+
+if __name__ == "__main__":
+    main()

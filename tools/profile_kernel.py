@@ -1,0 +1,48 @@
+"""Launch one generated kernel a few times on a config's full batch (for ncu / timing).
+
+  python tools/profile_kernel.py --config cfg2 --kind 0 --dtype f32 --iters 5
+kind: 0 fast fwd, 1 fast inv, 2 dense fwd, 3 dense inv.  Prints per-launch CUDA-event
+times (never report a number taken under ncu)."""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--kind", type=int, default=0)
+    ap.add_argument("--dtype", default=None)
+    ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=None)
+    a = ap.parse_args()
+    import torch
+    import workloads
+    from paper_1907_07875_b200 import gft
+    cfg = workloads.config(a.config)
+    dt = a.dtype or cfg.dtypes[0]
+    plan = gft.Plan.from_config(cfg, dtypes=(dt,))
+    B = a.batch or cfg.batch
+    X = torch.randn(B, cfg.n, device="cuda", dtype=torch.float64 if dt == "f64" else torch.float32)
+    Y = torch.empty_like(X)
+    fn = [plan.forward, plan.inverse, plan.dense_forward, plan.dense_inverse][a.kind]
+    times = []
+    for _ in range(a.iters):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn(X, Y)
+        e.record()
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e))
+    nbytes = 2 * B * cfg.n * X.element_size()
+    print(json.dumps({"config": a.config, "kind": a.kind, "dtype": dt, "kernel": plan.kernel_name(a.kind, dt),
+                      "launch": plan.launch_config(a.kind, dt, B), "ms": times,
+                      "gbs_best": nbytes / min(times) / 1e6}))
+
+
+if __name__ == "__main__":
+    main()
