@@ -156,9 +156,10 @@ GFT_API gft_status gft_execute_host(gft_plan plan, int32_t direction, const void
                             void* workspace, size_t workspace_bytes, int64_t chunk_rows,
                             gft_stream stream);
 
-/* Compile (NVRTC, or load from the AOT cubin cache built by build()) all four kernels of
- * `dtype` now instead of at first launch.  Needs no GPU. */
-GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype);
+/* Compile (NVRTC, or load from the AOT cubin cache built by build()) the kernels of `dtype`
+ * selected by kinds_mask (bit k = kind k: 0 fast-fwd, 1 fast-inv, 2 dense-fwd, 3 dense-inv;
+ * 0 = all) now instead of at first launch, one host thread per kernel.  Needs no GPU. */
+GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask);
 
 /* ---- introspection (host) ------------------------------------------------------------ */
 

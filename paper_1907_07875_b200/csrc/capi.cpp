@@ -6,6 +6,8 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/gft.h"
 #include "kernels.hpp"
@@ -158,10 +160,27 @@ gft_status gft_execute_host(gft_plan plan, int32_t direction, const void* in_hos
   });
 }
 
-gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype) {
+gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask) {
   return guard([&] {
+    if (kinds_mask == 0) kinds_mask = (1u << gft::K_NUM) - 1;
+    std::vector<gft::Kernel*> ks;
     for (int kind = 0; kind < gft::K_NUM; ++kind)
-      gft::compile_kernel(kernel_of(plan, kind, dtype), !(plan->flags & GFT_FLAG_NO_CUBIN_CACHE));
+      if (kinds_mask & (1u << kind)) ks.push_back(&kernel_of(plan, kind, dtype));
+    const bool cache = !(plan->flags & GFT_FLAG_NO_CUBIN_CACHE);
+    std::vector<std::thread> th;
+    std::vector<gft::Error> errs(ks.size(), gft::Error{GFT_OK, ""});
+    for (size_t i = 0; i < ks.size(); ++i)
+      th.emplace_back([&, i] {
+        try {
+          std::lock_guard<std::mutex> lk(ks[i]->mu);
+          gft::compile_kernel(*ks[i], cache);
+        } catch (const gft::Error& e) {
+          errs[i] = e;
+        }
+      });
+    for (auto& t : th) t.join();
+    for (auto& e : errs)
+      if (e.status != GFT_OK) throw e;
   });
 }
 

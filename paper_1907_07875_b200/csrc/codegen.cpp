@@ -196,7 +196,7 @@ bool plan_tc(const Plan& P, int dtype, int stages, std::vector<TcLeaf>& out, int
     t.np = ru(t.k, 16);
     const int need = 2 * ru(t.kp8, 32) + ru(t.np, 32);
     const int bsz = 2 * t.np * t.kp32 * 4;
-    if (cols + need > 512 || stages * tile + bytes + bsz > 200 * 1024 || t.np > 256) continue;
+    if (cols + need > 512 || stages * tile + bytes + bsz + 2048 > 227 * 1024 || t.np > 256) continue;
     t.hi_col = cols;
     t.lo_col = cols + ru(t.kp8, 32);
     t.d_col = cols + 2 * ru(t.kp8, 32);

@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GFT_LIB", os.path.join(_HERE, "_lib", "libgft.so"))
 
 GFT_F32, GFT_F64 = 0, 1
-GFT_FLAG_HOST_ONLY, GFT_FLAG_NO_CUBIN_CACHE = 1, 2
+GFT_FLAG_HOST_ONLY, GFT_FLAG_NO_CUBIN_CACHE, GFT_FLAG_NO_TENSOR_CORES = 1, 2, 4
 K_FAST_FWD, K_FAST_INV, K_DENSE_FWD, K_DENSE_INV = 0, 1, 2, 3
 GFT_MAX_LEVELS = 64
 
@@ -88,7 +88,7 @@ def lib():
         "gft_dense_forward": (c_int32, [P, P, P, c_int64, c_int32, P]),
         "gft_dense_inverse": (c_int32, [P, P, P, c_int64, c_int32, P]),
         "gft_execute_host": (c_int32, [P, c_int32, P, P, c_int64, c_int32, P, c_size_t, c_int64, P]),
-        "gft_plan_compile": (c_int32, [P, c_int32]),
+        "gft_plan_compile": (c_int32, [P, c_int32, c_uint32]),
         "gft_plan_info_get": (c_int32, [P, POINTER(gft_plan_info)]),
         "gft_plan_eigenvalues": (c_int32, [P, P]),
         "gft_plan_basis": (c_int32, [P, P]),
@@ -221,8 +221,8 @@ def gft_execute_host(h, direction, in_host, out_host, batch, dtype, workspace, w
                                   _stream_handle(stream)))
 
 
-def gft_plan_compile(h, dtype):
-    _check(lib().gft_plan_compile(h, _dtype_code(dtype)))
+def gft_plan_compile(h, dtype, kinds_mask=0):
+    _check(lib().gft_plan_compile(h, _dtype_code(dtype), int(kinds_mask)))
 
 
 def gft_plan_info_get(h):
@@ -310,7 +310,7 @@ class Plan:
 
     def __init__(self, n, src, dst, w, self_loops=None, phi=None, *, max_depth=-1, min_leaf=1,
                  search_budget=1000000, sym_rtol=1e-12, dtypes=("f32", "f64"), host_only=False,
-                 no_cubin_cache=False):
+                 no_cubin_cache=False, no_tensor_cores=False):
         o = gft_plan_opts_default()
         o.max_depth = max_depth
         o.min_leaf = min_leaf
@@ -319,7 +319,8 @@ class Plan:
         o.dtypes = 0
         for d in dtypes:
             o.dtypes |= 1 << _dtype_code(d)
-        o.flags = (GFT_FLAG_HOST_ONLY if host_only else 0) | (GFT_FLAG_NO_CUBIN_CACHE if no_cubin_cache else 0)
+        o.flags = ((GFT_FLAG_HOST_ONLY if host_only else 0) | (GFT_FLAG_NO_CUBIN_CACHE if no_cubin_cache else 0)
+                   | (GFT_FLAG_NO_TENSOR_CORES if no_tensor_cores else 0))
         self.n = int(n)
         self._h = gft_plan_create(n, src, dst, w, self_loops, phi, o)
 
@@ -378,8 +379,8 @@ class Plan:
                          workspace.numel() * workspace.element_size(), chunk_rows, stream)
         return out_host
 
-    def compile(self, dtype="f32"):
-        gft_plan_compile(self._h, dtype)
+    def compile(self, dtype="f32", kinds=(0, 1, 2, 3)):
+        gft_plan_compile(self._h, dtype, sum(1 << k for k in kinds))
 
     def info(self):
         return gft_plan_info_get(self._h).as_dict()

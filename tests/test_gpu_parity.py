@@ -166,7 +166,7 @@ def test_random_symmetric_graphs_on_gpu():
         plan = G.Plan(n, s, d, w, loops, phi if trial % 2 else None, dtypes=("f32",))
         cases.append((n, s, d, w, loops, plan))
     with cf.ThreadPoolExecutor(16) as ex:       # NVRTC is thread-safe; ctypes drops the GIL
-        list(ex.map(lambda c: c[5].compile("f32"), cases))
+        list(ex.map(lambda c: c[5].compile("f32", kinds=(0, 1)), cases))
     worst = 0.0
     for n, s, d, w, loops, plan in cases:
         L = oracle.laplacian(n, s, d, w, loops)
@@ -179,6 +179,47 @@ def test_random_symmetric_graphs_on_gpu():
         worst = max(worst, e)
         assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
     assert worst < 1e-5
+
+
+def _random_big_leaf_graph(rng, n, sym):
+    """Random weighted graph whose leaves are large (>= 32) so the tcgen05 path is used;
+    sizes chosen to exercise K/N padding (k not a multiple of 16 or 32)."""
+    if sym:
+        s, d, w, loops, phi = workloads.random_symmetric_graph(rng, n, density=0.3, fixed_frac=0.0)
+        return s, d, w, loops, phi
+    pairs = [(i, j) for i in range(n) for j in range(i + 1, n) if rng.random() < 0.2]
+    s = np.array([p[0] for p in pairs], np.int32)
+    d = np.array([p[1] for p in pairs], np.int32)
+    w = rng.uniform(0.5, 2.0, len(pairs))
+    return s, d, w, rng.uniform(0, 0.5, n), None
+
+
+@pytest.mark.parametrize("n,sym", [(32, False), (64, False), (96, True), (128, True), (160, True)])
+def test_tensor_core_leaves_general(n, sym):
+    """tcgen05 3xTF32 leaves on random graphs (leaf sizes 32..80 incl. padded K/N), against
+    the oracle and against the same plan forced onto CUDA-core FMA."""
+    rng = np.random.default_rng(n)
+    s, d, w, loops, phi = _random_big_leaf_graph(rng, n, sym)
+    plan = G.Plan(n, s, d, w, loops, phi, dtypes=("f32",))
+    src = plan.kernel_source(G.K_FAST_FWD, "f32")
+    assert "tcgen05.mma" in src, plan.leaf_sizes()
+    plan.compile("f32", kinds=(0, 1))          # NVRTC, both directions in parallel
+    L = oracle.laplacian(n, s, d, w, loops)
+    lam_o, U_o = oracle.gft_basis(L)
+    X = torch.randn(3000, n, generator=torch.Generator().manual_seed(1), dtype=torch.float32)
+    Y = plan.forward(X.cuda())
+    Xr = plan.inverse(Y)
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
+    if n > 128:
+        return      # (mixed TC + FMA leaves; the all-FMA variant takes minutes to JIT)
+    # FMA-only variant of the same plan gives the same coefficients (to fp32 rounding)
+    fma = G.Plan(n, s, d, w, loops, phi, dtypes=("f32",), no_tensor_cores=True)
+    assert "tcgen05.mma" not in fma.kernel_source(G.K_FAST_FWD, "f32")
+    Yf = fma.forward(X.cuda())
+    torch.cuda.synchronize()
+    assert oracle.relative_error(Y.cpu().numpy(), Yf.cpu().numpy()).max() <= 2e-5
 
 
 @pytest.mark.parametrize("name,dtype", [("cfg2", "f32"), ("cfg3", "f32"), ("cfg4", "f32"),
