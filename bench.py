@@ -114,11 +114,7 @@ class ClockSampler:
                 "note": note}
 
 
-def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+from paper_1907_07875_b200.dist import barrier, dist_env, max_over_ranks  # noqa: E402
 
 
 def time_kernel(fn, stream, warmup, iters):
@@ -279,8 +275,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+    barrier(device)
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -297,17 +292,12 @@ def main():
     t_end.record(stream)
     torch.cuda.synchronize()
     w1 = time.perf_counter()
-    if dist:
-        dist.barrier()
+    barrier(device)
     sampler.stop()
     total_ms = t_start.elapsed_time(t_end)
     fwd_ms = sum(ev[i][0].elapsed_time(ev[i][1]) for i in range(args.steps)) / args.steps
     inv_ms = sum(ev[i][1].elapsed_time(ev[i][2]) for i in range(args.steps)) / args.steps
-    ms_step = total_ms / args.steps
-    if dist:
-        t = torch.tensor([ms_step], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
+    ms_step = max_over_ranks(total_ms / args.steps, device)
     value = B * ws / (ms_step * 1e-3)
     clocks = sampler.summary(w0, w1)
 
@@ -338,19 +328,14 @@ def main():
     for _ in range(3):
         e2e_step()
     torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+    barrier(device)
     s_e, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s_e.record(stream)
     for _ in range(args.e2e_steps):
         e2e_step()
     e_e.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = s_e.elapsed_time(e_e) / args.e2e_steps
-    if dist:
-        t = torch.tensor([e2e_ms], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(s_e.elapsed_time(e_e) / args.e2e_steps, device)
     roundtrip_err = float(((Zh.double() - X_cpu.double()).norm(dim=1) / X_cpu.double().norm(dim=1)).max())
 
     table = None

@@ -284,14 +284,15 @@ void generate_tc(const Plan& P, bool forward, const std::vector<TcLeaf>& T, std:
     o << buf << ((i % 8 == 7) ? "\n" : "");
   }
   o << "};\n";
-  // ---- front ----
-  o << "static __device__ __forceinline__ void gft_front(float (&x)[GFT_N]) {\n";
+  o << "#define GFT_NTC " << T.size() << "\n";
+  o << "static __device__ __forceinline__ void gft_tile(float (&x)[GFT_N], float (&y)[GFT_N], u32 tm,\n"
+       "    u32 tmem, u32 bsm, u32 mbar, u32 par, int tid) {\n";
+  // ---- front: butterflies (forward) ----
   if (forward) emit_units(o, P, "x", false, dtype);
-  o << "}\n";
-  // ---- stage A (hi/lo split of the big-leaf inputs -> TMEM) ----
-  o << "static __device__ __forceinline__ void gft_stage_a(const float (&x)[GFT_N], u32 tm) {\n";
-  for (const auto& t : T) {
+  for (size_t ti = 0; ti < T.size(); ++ti) {
+    const TcLeaf& t = T[ti];
     const Leaf& lf = P.leaves[t.leaf];
+    // ---- stage A: hi/lo split of the leaf inputs -> TMEM (this thread's lane) ----
     for (int c0 = 0; c0 < t.kp8; c0 += 32) {   // 32-column chunks keep register pressure low
       const int w = std::min(32, t.kp8 - c0);
       o << "  { u32 h[" << w << "], l[" << w << "];\n";
@@ -308,11 +309,9 @@ void generate_tc(const Plan& P, bool forward, const std::vector<TcLeaf>& T, std:
       emit_tmem_st(o, "l", t.lo_col + c0, w);
       o << "  }\n";
     }
-  }
-  o << "}\n";
-  // ---- MMA issue (one thread) ----
-  o << "static __device__ __forceinline__ void gft_issue(u32 tm, u32 bsm) {\n";
-  for (const auto& t : T) {
+    // ---- all 128 lanes staged -> one thread issues this leaf's MMAs and commits ----
+    o << "  tc_wait_st(); tc_fence_before(); named_bar(1, 128);\n";
+    o << "  if (tid == 0) {\n  tc_fence_after();\n";
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(t.np >> 3) << 17) | (8u << 24);
     const int ksteps = t.kp8 / 8;
     const int atom_bytes = t.np * 128;
@@ -322,14 +321,13 @@ void generate_tc(const Plan& P, bool forward, const std::vector<TcLeaf>& T, std:
       const int boff = pass == 1 ? t.blo_off : t.bhi_off;
       for (int j = 0; j < ksteps; ++j) {
         const int bo = boff + (j / 4) * atom_bytes + (j % 4) * 32;
-        o << "  mma_ts(tm + " << t.d_col << "u, tm + " << (acol + 8 * j) << "u, smem_desc_sw128(bsm + " << bo
+        o << "  mma_ts(tmem + " << t.d_col << "u, tmem + " << (acol + 8 * j) << "u, smem_desc_sw128(bsm + " << bo
           << "u), " << idesc << "u, " << ((pass == 0 && j == 0) ? 0 : 1) << "u);\n";
       }
     }
+    o << "  tc_commit(mbar + " << 8 * ti << "u);\n  }\n";
   }
-  o << "}\n";
-  // ---- small leaves on CUDA cores ----
-  o << "static __device__ __forceinline__ void gft_fma(const float (&x)[GFT_N], float (&y)[GFT_N]) {\n";
+  // ---- small leaves on CUDA cores (overlap the tensor-core work) ----
   for (size_t l = 0; l < P.leaves.size(); ++l) {
     if (is_tc[l]) continue;
     const Leaf& lf = P.leaves[l];
@@ -341,11 +339,11 @@ void generate_tc(const Plan& P, bool forward, const std::vector<TcLeaf>& T, std:
       emit_dot(o, xs("y", forward ? lf.slot[i] : lf.pos[i]), coef, in, dtype);
     }
   }
-  o << "}\n";
-  // ---- epilogue: accumulators -> registers ----
-  o << "static __device__ __forceinline__ void gft_epi(u32 tm, float (&y)[GFT_N]) {\n";
-  for (const auto& t : T) {
+  // ---- epilogue: per leaf, wait for its MMAs, accumulators -> registers ----
+  for (size_t ti = 0; ti < T.size(); ++ti) {
+    const TcLeaf& t = T[ti];
     const Leaf& lf = P.leaves[t.leaf];
+    o << "  mbar_wait(mbar + " << 8 * ti << "u, par); tc_fence_after();\n";
     for (int r0 = 0; r0 < t.k; r0 += 32) {
       const int w = std::min(32, t.np - r0);
       o << "  { u32 d[" << w << "];\n";
@@ -355,9 +353,7 @@ void generate_tc(const Plan& P, bool forward, const std::vector<TcLeaf>& T, std:
       o << "  }\n";
     }
   }
-  o << "}\n";
-  // ---- back ----
-  o << "static __device__ __forceinline__ void gft_back(float (&y)[GFT_N]) {\n";
+  // ---- back: reverse butterflies (inverse) ----
   if (!forward) emit_units(o, P, "y", true, dtype);
   o << "}\n";
 }

@@ -16,7 +16,8 @@
 //             -> bar(128) -> thread 0 issues tcgen05.mma (TS form: A in TMEM, B in SMEM)
 //             -> small leaves on FMA -> wait tcgen05.commit -> tcgen05.ld D -> SMEM row
 // The generated prelude defines GFT_N, GFT_STAGES, GFT_TMEM_COLS, GFT_B_FLOATS, GFT_KNAME,
-// and gft_front / gft_stage_a / gft_issue / gft_fma / gft_epi / gft_back + gft_tcB[].
+// GFT_NTC (number of tensor-core leaves, one MMA-completion mbarrier each), gft_tcB[]
+// and gft_tile() (the per-tile compute sequence).
 typedef unsigned int u32;
 typedef unsigned long long u64;
 typedef float elem_t;
@@ -118,7 +119,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   unsigned char* bsm = smem + GFT_STAGES * GFT_TILE_BYTES;            // B operands (1024-aligned)
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(bsm + GFT_B_FLOATS * 4);
   // bars: full[S], done[S], mma
-  u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * GFT_STAGES + 1);
+  u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * GFT_STAGES + GFT_NTC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const long long ntiles = (batch + GFT_TILE_ROWS - 1) / GFT_TILE_ROWS;
 
@@ -132,7 +133,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       mbar_init(smem_u32(&bars[s]), 1);
       mbar_init(smem_u32(&bars[GFT_STAGES + s]), 4);
     }
-    mbar_init(smem_u32(&bars[2 * GFT_STAGES]), 1);
+    for (int i = 0; i < GFT_NTC; ++i) mbar_init(smem_u32(&bars[2 * GFT_STAGES + i]), 1);
     fence_mbar_init();
   }
   // B operands (plan constants) -> SMEM, K-major 128B-swizzled atoms of [Np rows x 32 k]
@@ -195,21 +196,10 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       unsigned char* buf = stages + s * GFT_TILE_BYTES;
       float x[GFT_N], y[GFT_N];
       load_row(buf, tid, x);
-      gft_front(x);
-      gft_stage_a(x, tm_lane);
-      tc_wait_st();
-      tc_fence_before();
-      named_bar(1, 128);
-      if (tid == 0) {
-        tc_fence_after();
-        gft_issue(tmem, bsm_s);
-        tc_commit(smem_u32(&bars[2 * GFT_STAGES]));
-      }
-      gft_fma(x, y);
-      mbar_wait(smem_u32(&bars[2 * GFT_STAGES]), (u32)(it & 1));
-      tc_fence_after();
-      gft_epi(tm_lane, y);
-      gft_back(y);
+      // generated: butterflies; per big leaf: hi/lo -> TMEM, bar(128), thread 0 issues the
+      // leaf's MMAs + commit (the next leaf is staged while they run); small leaves on FMA;
+      // per big leaf: wait its commit, TMEM -> registers; reverse butterflies (inverse)
+      gft_tile(x, y, tm_lane, tmem, bsm_s, smem_u32(&bars[2 * GFT_STAGES]), (u32)(it & 1), tid);
       store_row(buf, tid, y);
       fence_proxy_async();
       tc_fence_before();

@@ -31,7 +31,7 @@ struct KernelCfg {
   int threads() const { return tc ? 160 : warps * 32; }
   int tiles_per_cta() const { return tc ? 1 : warps; }   // tiles processed concurrently per CTA
   int smem_bytes() const {
-    if (tc) return stages * tile_bytes() + tc_b_bytes + (2 * stages + 1) * 8 + 16 + 1024;
+    if (tc) return stages * tile_bytes() + tc_b_bytes + (2 * stages + 8) * 8 + 16 + 1024;
     return warps * stages * tile_bytes() + warps * stages * 8 + 1024;
   }
   int swizzle_bytes() const { return swz_mask == 7 ? 128 : swz_mask == 3 ? 64 : swz_mask == 1 ? 32 : 0; }
