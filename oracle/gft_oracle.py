@@ -155,6 +155,11 @@ def inverse(Y, U):
     return np.asarray(Y, dtype=np.float64) @ U.T
 
 
+def graph_filter(X, U, h):
+    """Graph spectral filtering: row b -> U diag(h) U^T x_b, i.e. X U diag(h) U^T."""
+    return ((np.asarray(X, dtype=np.float64) @ U) * np.asarray(h, dtype=np.float64)) @ U.T
+
+
 def forward_rows_loop(X, U):
     """Same as forward() but a plain per-row loop (used to time a bounded sample the
     way the paper's C 'matrix GFT' runs: one n x n matrix-vector product per signal)."""

@@ -234,6 +234,22 @@ def test_theorem3_offblocks_random():
     assert np.abs(G[np.ix_([0, 1, 2], [3, 4, 5])]).max() > 1e-4
 
 
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_graph_filter_closed_forms(name):
+    """U diag(h) U^T: h = 1 -> I, h = lambda -> L, h = lambda^2 -> L^2, h = exp(-t lambda) ->
+    expm(-t L) (SciPy's Pade expm, a library routine)."""
+    import scipy.linalg
+    cfg = workloads.config(name)
+    L = oracle.laplacian(cfg.n, *cfg.edges, cfg.self_loops)
+    lam, U = oracle.gft_basis(L)
+    X = workloads.signals(cfg, batch=32, dtype="f64").numpy()
+    assert np.abs(oracle.graph_filter(X, U, np.ones(cfg.n)) - X).max() < 1e-12
+    assert np.abs(oracle.graph_filter(X, U, lam) - X @ L).max() < 1e-11
+    assert np.abs(oracle.graph_filter(X, U, lam ** 2) - X @ L @ L).max() < 1e-10
+    t = 0.3
+    assert np.abs(oracle.graph_filter(X, U, np.exp(-t * lam)) - X @ scipy.linalg.expm(-t * L)).max() < 1e-12
+
+
 def test_cluster_metrics_are_sign_and_rotation_invariant():
     s, d, w = workloads.cycle_graph(8)
     lam, U = oracle.gft_basis_of_graph(8, s, d, w)
