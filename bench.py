@@ -157,8 +157,25 @@ def config_table(args, stream, hbm, device):
                                      "signals_per_s": cfg.batch / ms * 1e3}
         row["fast_vs_dense_fwd"] = round(row["dense_fwd"]["ms"] / row["fast_fwd"]["ms"], 3)
         row["fast_vs_dense_inv"] = round(row["dense_inv"]["ms"] / row["fast_inv"]["ms"], 3)
+        # fused graph filter U diag(exp(-lambda)) U^T (one pass) vs forward + inverse (two)
+        filt = gft.Filter(plan, np.exp(-plan.eigenvalues()), dtypes=(dtype,))
+        ms = time_kernel(lambda: filt.apply(X, Y, stream), stream, 3, args.table_iters)
+        row["filter"] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
+                         "frac": round(nbytes / ms / 1e6 / hbm, 4), "signals_per_s": cfg.batch / ms * 1e3,
+                         "kernel": filt.kernel_name(dtype)}
+        row["fused_filter_vs_two_pass"] = round((row["fast_fwd"]["ms"] + row["fast_inv"]["ms"]) / ms, 3)
+        # cuBLAS SGEMM/DGEMM with TF32 disabled (SURVEY §7 step 6 cross-check of "dense")
+        U = torch.from_numpy(plan.basis()).to(device=device, dtype=tdt)
+        tf32 = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
+        ms = time_kernel(lambda: torch.matmul(X, U, out=Y), stream, 3, args.table_iters)
+        torch.backends.cuda.matmul.allow_tf32 = tf32
+        row["cublas_fwd"] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
+                             "frac": round(nbytes / ms / 1e6 / hbm, 4)}
+        row["fast_vs_best_dense_fwd"] = round(min(row["dense_fwd"]["ms"], ms) / row["fast_fwd"]["ms"], 3)
         rows.append(row)
         del X, Y
+        filt.close()
         plan.close()
     return rows
 

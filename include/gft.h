@@ -156,6 +156,27 @@ GFT_API gft_status gft_execute_host(gft_plan plan, int32_t direction, const void
                             void* workspace, size_t workspace_bytes, int64_t chunk_rows,
                             gft_stream stream);
 
+/* ---- fused graph spectral filter ("graph spectral filtering",
+ *      PAPER.md:32) ------------------------------------------------------------------------
+ * y = U diag(h) U^T x in ONE HBM pass per tile: the plan's butterflies, then per leaf the
+ * k x k matrix F_l = M_l^T diag(h_l) M_l (M_l = folded leaf matrix), then the butterflies
+ * in reverse order — the cost of one transform instead of forward + inverse.
+ * h[n]: response per coefficient in the plan's ascending-eigenvalue order (e.g. h = g(lambda)
+ * from gft_plan_eigenvalues).  If h is not constant on a repeated eigenvalue the result
+ * depends on the plan's basis inside that eigenspace (it is still U_f diag(h) U_f^T).
+ * The filter copies what it needs: it stays valid after gft_plan_destroy(plan).
+ * dtypes: bitmask as in gft_plan_opts; flags: GFT_FLAG_NO_CUBIN_CACHE / _NO_TENSOR_CORES. */
+typedef struct gft_filter_s* gft_filter;
+GFT_API gft_status gft_filter_create(gft_filter* out, gft_plan plan, const double* h, uint32_t dtypes,
+                                     uint32_t flags);
+/* Y = filter(X), device pointers [batch, n], same rules as gft_forward (in place allowed). */
+GFT_API gft_status gft_filter_apply(gft_filter f, const void* X, void* Y, int64_t batch,
+                                    gft_dtype dtype, gft_stream stream);
+GFT_API gft_status gft_filter_kernel_name(gft_filter f, gft_dtype dtype, char* buf, size_t cap);
+GFT_API gft_status gft_filter_kernel_source(gft_filter f, gft_dtype dtype, char* buf, size_t cap,
+                                            size_t* len);
+GFT_API gft_status gft_filter_destroy(gft_filter f);
+
 /* Compile (NVRTC, or load from the AOT cubin cache built by build()) the kernels of `dtype`
  * selected by kinds_mask (bit k = kind k: 0 fast-fwd, 1 fast-inv, 2 dense-fwd, 3 dense-inv;
  * 0 = all) now instead of at first launch, one host thread per kernel.  Needs no GPU. */

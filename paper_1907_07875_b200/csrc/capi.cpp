@@ -20,6 +20,12 @@ struct gft_plan_s {
   std::unique_ptr<gft::Kernel> k[2][gft::K_NUM];
 };
 
+struct gft_filter_s {
+  gft::Plan P;              // the plan with leaf matrices replaced by F_l = M_l^T diag(h_l) M_l
+  uint32_t flags = 0;
+  std::unique_ptr<gft::Kernel> k[2];
+};
+
 namespace {
 thread_local std::string g_last_error;
 
@@ -157,6 +163,88 @@ gft_status gft_execute_host(gft_plan plan, int32_t direction, const void* in_hos
     if (!in_host || !out_host) gft::fail(GFT_ERR_INVALID_ARG, "NULL host pointer");
     gft::execute_host(k, in_host, out_host, batch, workspace, workspace_bytes, chunk_rows, stream,
                       !(plan->flags & GFT_FLAG_NO_CUBIN_CACHE));
+  });
+}
+
+gft_status gft_filter_create(gft_filter* out, gft_plan plan, const double* h, uint32_t dtypes,
+                             uint32_t flags) {
+  return guard([&] {
+    if (!out || !plan || !h) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
+    *out = nullptr;
+    if (dtypes == 0 || (dtypes & ~3u)) gft::fail(GFT_ERR_UNSUPPORTED, "bad dtypes mask");
+    if (plan->P.n > 256) gft::fail(GFT_ERR_UNSUPPORTED, "kernel generation supports n <= 256");
+    const int n = plan->P.n;
+    for (int i = 0; i < n; ++i)
+      if (!std::isfinite(h[i])) gft::fail(GFT_ERR_INVALID_ARG, "non-finite filter response");
+    std::unique_ptr<gft_filter_s> f(new gft_filter_s);
+    f->P = plan->P;
+    f->flags = flags;
+    for (auto& lf : f->P.leaves) {
+      const int k = lf.k;
+      std::vector<double> F((size_t)k * k, 0.0);
+      for (int r = 0; r < k; ++r) {
+        const double hr = h[lf.slot[r]];
+        if (hr == 0.0) continue;
+        for (int c = 0; c < k; ++c) {
+          const double a = lf.M[(size_t)r * k + c] * hr;
+          for (int c2 = 0; c2 < k; ++c2) F[(size_t)c * k + c2] += a * lf.M[(size_t)r * k + c2];
+        }
+      }
+      lf.M.swap(F);
+    }
+    for (int dt = 0; dt < 2; ++dt) {
+      if (!(dtypes & (1u << dt))) continue;
+      f->k[dt].reset(new gft::Kernel);
+      gft::generate_kernel(f->P, gft::K_FILTER, dt, *f->k[dt], !(flags & GFT_FLAG_NO_TENSOR_CORES));
+    }
+    *out = f.release();
+  });
+}
+
+gft_status gft_filter_apply(gft_filter f, const void* X, void* Y, int64_t batch, gft_dtype dtype,
+                            gft_stream stream) {
+  return guard([&] {
+    if (!f) gft::fail(GFT_ERR_INVALID_ARG, "NULL filter");
+    if (dtype != GFT_F32 && dtype != GFT_F64) gft::fail(GFT_ERR_UNSUPPORTED, "unsupported dtype");
+    if (!f->k[dtype]) gft::fail(GFT_ERR_UNSUPPORTED, "dtype not prepared in this filter");
+    if (batch < 0) gft::fail(GFT_ERR_INVALID_ARG, "batch < 0");
+    if (batch == 0) return;
+    check_io(X, Y);
+    gft::launch_kernel(*f->k[dtype], X, Y, batch, stream, !(f->flags & GFT_FLAG_NO_CUBIN_CACHE));
+  });
+}
+
+gft_status gft_filter_kernel_name(gft_filter f, gft_dtype dtype, char* buf, size_t cap) {
+  return guard([&] {
+    if (!f || !buf || cap == 0) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
+    if ((dtype != GFT_F32 && dtype != GFT_F64) || !f->k[dtype]) gft::fail(GFT_ERR_UNSUPPORTED, "dtype not prepared");
+    const std::string& nm = f->k[dtype]->name;
+    size_t m = std::min(cap - 1, nm.size());
+    std::memcpy(buf, nm.data(), m);
+    buf[m] = 0;
+  });
+}
+
+gft_status gft_filter_kernel_source(gft_filter f, gft_dtype dtype, char* buf, size_t cap, size_t* len) {
+  return guard([&] {
+    if (!f) gft::fail(GFT_ERR_INVALID_ARG, "NULL filter");
+    if ((dtype != GFT_F32 && dtype != GFT_F64) || !f->k[dtype]) gft::fail(GFT_ERR_UNSUPPORTED, "dtype not prepared");
+    const std::string& s = f->k[dtype]->source;
+    if (len) *len = s.size();
+    if (buf && cap) {
+      size_t m = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), m);
+      buf[m] = 0;
+    }
+  });
+}
+
+gft_status gft_filter_destroy(gft_filter f) {
+  return guard([&] {
+    if (!f) return;
+    for (auto& k : f->k)
+      if (k) gft::unload_kernel(*k);
+    delete f;
   });
 }
 

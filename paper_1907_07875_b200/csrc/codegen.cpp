@@ -90,56 +90,54 @@ void emit_dot(std::ostringstream& o, const std::string& out, const std::vector<d
 
 std::string xs(const char* arr, int i) { return std::string(arr) + "[" + std::to_string(i) + "]"; }
 
-void emit_fast_forward(std::ostringstream& o, const Plan& P, int dtype) {
-  o << "  elem_t a_, b_;\n";
+// Transform direction of a fast kernel: which index a leaf reads / writes and whether the
+// butterfly network runs before (forward) and / or reversed after (inverse) the leaves.
+//   FWD:    x -> units -> y[slot[r]] = sum_c M[r][c] x[pos[c]]
+//   INV:    y[pos[c]] = sum_r M[r][c] x[slot[r]] -> reverse units
+//   FILTER: x -> units -> y[pos[c]] = sum_c' F[c][c'] x[pos[c']] -> reverse units, with the
+//           leaf matrix field holding F = M^T diag(h) M (fused U diag(h) U^T)
+enum Dir { DIR_FWD = 0, DIR_INV = 1, DIR_FILTER = 2 };
+int in_idx(const Leaf& lf, Dir d, int i) { return d == DIR_INV ? lf.slot[i] : lf.pos[i]; }
+int out_idx(const Leaf& lf, Dir d, int o) { return d == DIR_FWD ? lf.slot[o] : lf.pos[o]; }
+double leaf_coef(const Leaf& lf, Dir d, int o, int i) {
+  return d == DIR_INV ? lf.M[(size_t)i * lf.k + o] : lf.M[(size_t)o * lf.k + i];
+}
+
+void emit_units_elem(std::ostringstream& o, const Plan& P, const char* arr, bool reverse, int dtype) {
+  o << "  { elem_t a_, b_;\n";
   int lvl = -1;
-  for (const Op& op : P.ops) {
-    if (op.level != lvl) { lvl = op.level; o << "  // ---- butterfly level " << lvl << "\n"; }
-    if (op.kind == Op::UNIT) {
-      o << "  a_ = x[" << op.a << "]; b_ = x[" << op.b << "]; x[" << op.a << "] = a_ + b_; x["
-        << op.b << "] = a_ - b_;\n";
-    } else {
-      o << "  x[" << op.a << "] = x[" << op.a << "] * " << lit(std::pow(2.0, 0.5 * op.m), dtype)
-        << ";  // equalise deferred scale\n";
+  auto one = [&](const Op& op) {
+    if (op.level != lvl) {
+      lvl = op.level;
+      o << "  // ---- butterfly level " << lvl << (reverse ? " (reverse)" : "") << "\n";
     }
-  }
-  for (size_t l = 0; l < P.leaves.size(); ++l) {
-    const Leaf& lf = P.leaves[l];
-    o << "  // ---- leaf " << l << " (k=" << lf.k << ")\n";
-    std::vector<std::string> in(lf.k);
-    for (int c = 0; c < lf.k; ++c) in[c] = xs("x", lf.pos[c]);
-    for (int r = 0; r < lf.k; ++r) {
-      std::vector<double> coef(lf.M.begin() + (size_t)r * lf.k, lf.M.begin() + (size_t)(r + 1) * lf.k);
-      emit_dot(o, xs("y", lf.slot[r]), coef, in, dtype);
-    }
+    if (op.kind == Op::UNIT)
+      o << "  a_ = " << arr << "[" << op.a << "]; b_ = " << arr << "[" << op.b << "]; " << arr << "["
+        << op.a << "] = a_ + b_; " << arr << "[" << op.b << "] = a_ - b_;\n";
+    else
+      o << "  " << arr << "[" << op.a << "] = " << arr << "[" << op.a << "] * "
+        << lit(std::pow(2.0, 0.5 * op.m), dtype) << ";  // equalise deferred scale\n";
+  };
+  if (!reverse) for (const Op& op : P.ops) one(op);
+  else for (auto it = P.ops.rbegin(); it != P.ops.rend(); ++it) one(*it);
+  o << "  (void)a_; (void)b_; }\n";
+}
+
+void emit_leaf_fma(std::ostringstream& o, const Leaf& lf, size_t l, Dir d, int dtype) {
+  o << "  // ---- leaf " << l << " (k=" << lf.k << ")\n";
+  std::vector<std::string> in(lf.k);
+  for (int i = 0; i < lf.k; ++i) in[i] = xs("x", in_idx(lf, d, i));
+  for (int r = 0; r < lf.k; ++r) {
+    std::vector<double> coef(lf.k);
+    for (int i = 0; i < lf.k; ++i) coef[i] = leaf_coef(lf, d, r, i);
+    emit_dot(o, xs("y", out_idx(lf, d, r)), coef, in, dtype);
   }
 }
 
-void emit_fast_inverse(std::ostringstream& o, const Plan& P, int dtype) {
-  // x holds coefficients (ascending eigenvalue order); y receives the signal.
-  for (size_t l = 0; l < P.leaves.size(); ++l) {
-    const Leaf& lf = P.leaves[l];
-    o << "  // ---- leaf " << l << " (k=" << lf.k << ", transposed)\n";
-    std::vector<std::string> in(lf.k);
-    for (int r = 0; r < lf.k; ++r) in[r] = xs("x", lf.slot[r]);
-    for (int c = 0; c < lf.k; ++c) {
-      std::vector<double> coef(lf.k);
-      for (int r = 0; r < lf.k; ++r) coef[r] = lf.M[(size_t)r * lf.k + c];
-      emit_dot(o, xs("y", lf.pos[c]), coef, in, dtype);
-    }
-  }
-  o << "  elem_t a_, b_;\n";
-  int lvl = -1;
-  for (auto it = P.ops.rbegin(); it != P.ops.rend(); ++it) {
-    const Op& op = *it;
-    if (op.level != lvl) { lvl = op.level; o << "  // ---- butterfly level " << lvl << " (reverse)\n"; }
-    if (op.kind == Op::UNIT) {
-      o << "  a_ = y[" << op.a << "]; b_ = y[" << op.b << "]; y[" << op.a << "] = a_ + b_; y["
-        << op.b << "] = a_ - b_;\n";
-    } else {
-      o << "  y[" << op.a << "] = y[" << op.a << "] * " << lit(std::pow(2.0, 0.5 * op.m), dtype) << ";\n";
-    }
-  }
+void emit_fast(std::ostringstream& o, const Plan& P, int dtype, Dir d) {
+  if (d != DIR_INV) emit_units_elem(o, P, "x", false, dtype);
+  for (size_t l = 0; l < P.leaves.size(); ++l) emit_leaf_fma(o, P.leaves[l], l, d, dtype);
+  if (d != DIR_FWD) emit_units_elem(o, P, "y", true, dtype);
 }
 
 void emit_dense(std::ostringstream& o, const Plan& P, int dtype, bool forward) {
@@ -243,7 +241,7 @@ void emit_tmem_ld(std::ostringstream& o, const std::string& arr, int col0, int c
 }
 
 void emit_units(std::ostringstream& o, const Plan& P, const char* arr, bool reverse, int dtype) {
-  o << "  float a_, b_;\n";
+  o << "  { float a_, b_;\n";
   auto one = [&](const Op& op) {
     if (op.kind == Op::UNIT)
       o << "  a_ = " << arr << "[" << op.a << "]; b_ = " << arr << "[" << op.b << "]; " << arr << "["
@@ -254,10 +252,10 @@ void emit_units(std::ostringstream& o, const Plan& P, const char* arr, bool reve
   };
   if (!reverse) for (const Op& op : P.ops) one(op);
   else for (auto it = P.ops.rbegin(); it != P.ops.rend(); ++it) one(*it);
-  o << "  (void)a_; (void)b_;\n";
+  o << "  (void)a_; (void)b_; }\n";
 }
 
-void generate_tc(const Plan& P, bool forward, const std::vector<TcLeaf>& T, std::ostringstream& o) {
+void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, std::ostringstream& o) {
   const int dtype = GFT_F32;
   std::vector<char> is_tc(P.leaves.size(), 0);
   for (const auto& t : T) is_tc[t.leaf] = 1;
@@ -270,8 +268,8 @@ void generate_tc(const Plan& P, bool forward, const std::vector<TcLeaf>& T, std:
         for (int n = 0; n < t.np; ++n)
           for (int kk = 32 * a; kk < 32 * a + 32; ++kk) {
             float v = 0.f;
-            if (n < t.k && kk < t.k)   // forward: B[n=r][k=c] = M[r][c]; inverse: B[n=c][k=r] = M[r][c]
-              v = (float)(forward ? lf.M[(size_t)n * t.k + kk] : lf.M[(size_t)kk * t.k + n]);
+            if (n < t.k && kk < t.k)   // B[n = output][k = input]
+              v = (float)leaf_coef(lf, d, n, kk);
             const float hi = tf32_rna_host(v);
             B.push_back(part == 0 ? hi : v - hi);
           }
@@ -288,7 +286,7 @@ void generate_tc(const Plan& P, bool forward, const std::vector<TcLeaf>& T, std:
   o << "static __device__ __forceinline__ void gft_tile(float (&x)[GFT_N], float (&y)[GFT_N], u32 tm,\n"
        "    u32 tmem, u32 bsm, u32 mbar, u32 par, int tid) {\n";
   // ---- front: butterflies (forward) ----
-  if (forward) emit_units(o, P, "x", false, dtype);
+  if (d != DIR_INV) emit_units(o, P, "x", false, dtype);
   for (size_t ti = 0; ti < T.size(); ++ti) {
     const TcLeaf& t = T[ti];
     const Leaf& lf = P.leaves[t.leaf];
@@ -298,7 +296,7 @@ void generate_tc(const Plan& P, bool forward, const std::vector<TcLeaf>& T, std:
       o << "  { u32 h[" << w << "], l[" << w << "];\n";
       for (int c = c0; c < c0 + w; ++c) {
         if (c < t.k) {
-          const int src = forward ? lf.pos[c] : lf.slot[c];
+          const int src = in_idx(lf, d, c);
           o << "  h[" << c - c0 << "] = tf32_rna(x[" << src << "]); l[" << c - c0 << "] = __float_as_uint(x["
             << src << "] - __uint_as_float(h[" << c - c0 << "]));\n";
         } else {
@@ -328,17 +326,8 @@ void generate_tc(const Plan& P, bool forward, const std::vector<TcLeaf>& T, std:
     o << "  tc_commit(mbar + " << 8 * ti << "u);\n  }\n";
   }
   // ---- small leaves on CUDA cores (overlap the tensor-core work) ----
-  for (size_t l = 0; l < P.leaves.size(); ++l) {
-    if (is_tc[l]) continue;
-    const Leaf& lf = P.leaves[l];
-    std::vector<std::string> in(lf.k);
-    for (int i = 0; i < lf.k; ++i) in[i] = xs("x", forward ? lf.pos[i] : lf.slot[i]);
-    for (int i = 0; i < lf.k; ++i) {
-      std::vector<double> coef(lf.k);
-      for (int j = 0; j < lf.k; ++j) coef[j] = forward ? lf.M[(size_t)i * lf.k + j] : lf.M[(size_t)j * lf.k + i];
-      emit_dot(o, xs("y", forward ? lf.slot[i] : lf.pos[i]), coef, in, dtype);
-    }
-  }
+  for (size_t l = 0; l < P.leaves.size(); ++l)
+    if (!is_tc[l]) emit_leaf_fma(o, P.leaves[l], l, d, dtype);
   // ---- epilogue: per leaf, wait for its MMAs, accumulators -> registers ----
   for (size_t ti = 0; ti < T.size(); ++ti) {
     const TcLeaf& t = T[ti];
@@ -349,12 +338,12 @@ void generate_tc(const Plan& P, bool forward, const std::vector<TcLeaf>& T, std:
       o << "  { u32 d[" << w << "];\n";
       emit_tmem_ld(o, "d", t.d_col + r0, w);
       for (int r = r0; r < std::min(t.k, r0 + w); ++r)
-        o << "  y[" << (forward ? lf.slot[r] : lf.pos[r]) << "] = __uint_as_float(d[" << r - r0 << "]);\n";
+        o << "  y[" << out_idx(lf, d, r) << "] = __uint_as_float(d[" << r - r0 << "]);\n";
       o << "  }\n";
     }
   }
   // ---- back: reverse butterflies (inverse) ----
-  if (!forward) emit_units(o, P, "y", true, dtype);
+  if (d != DIR_FWD) emit_units(o, P, "y", true, dtype);
   o << "}\n";
 }
 
@@ -364,8 +353,9 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
   k.kind = kind;
   k.dtype = dtype;
   k.cfg = choose_cfg(P.n, dtype);
-  static const char* kKindNameTC[] = {"fwdtc", "invtc"};
-  if (allow_tc && (kind == K_FAST_FWD || kind == K_FAST_INV)) {
+  static const char* kKindNameTC[] = {"fwdtc", "invtc", "", "", "filttc"};
+  const Dir dir = kind == K_FAST_INV ? DIR_INV : kind == K_FILTER ? DIR_FILTER : DIR_FWD;
+  if (allow_tc && (kind == K_FAST_FWD || kind == K_FAST_INV || kind == K_FILTER)) {
     std::vector<TcLeaf> T;
     int tmem_cols = 0, b_bytes = 0;
     const int stages = 2;
@@ -382,7 +372,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
       c.tc_b_bytes = b_bytes;
       c.tc_tmem_cols = tmem_cols;
       std::ostringstream gen;
-      generate_tc(P, kind == K_FAST_FWD, T, gen);
+      generate_tc(P, dir, T, gen);
       std::ostringstream pre;
       pre << "#define GFT_N " << c.n << "\n#define GFT_STAGES " << c.stages << "\n#define GFT_TMEM_COLS "
           << tmem_cols << "\n";
@@ -407,14 +397,15 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
   std::ostringstream body;
   body << "static __device__ __forceinline__ void gft_body(elem_t (&x)[GFT_N], elem_t (&y)[GFT_N]) {\n";
   switch (kind) {
-    case K_FAST_FWD: emit_fast_forward(body, P, dtype); break;
-    case K_FAST_INV: emit_fast_inverse(body, P, dtype); break;
+    case K_FAST_FWD:
+    case K_FAST_INV:
+    case K_FILTER: emit_fast(body, P, dtype, dir); break;
     case K_DENSE_FWD: emit_dense(body, P, dtype, true); break;
     case K_DENSE_INV: emit_dense(body, P, dtype, false); break;
     default: fail(GFT_ERR_INVALID_ARG, "bad kernel kind");
   }
   body << "}\n";
-  static const char* kKindName[] = {"fwd", "inv", "dfwd", "dinv"};
+  static const char* kKindName[] = {"fwd", "inv", "dfwd", "dinv", "filt"};
   std::ostringstream pre;
   pre << "#define GFT_ELEM " << (dtype == GFT_F64 ? "double" : "float") << "\n";
   if (dtype == GFT_F64) pre << "#define GFT_ELEM_IS_DOUBLE 1\n";

@@ -12,7 +12,8 @@
 
 namespace gft {
 
-enum KernelKind { K_FAST_FWD = 0, K_FAST_INV = 1, K_DENSE_FWD = 2, K_DENSE_INV = 3, K_NUM = 4 };
+// K_NUM kinds per plan; K_FILTER kernels belong to a gft_filter (fused U diag(h) U^T)
+enum KernelKind { K_FAST_FWD = 0, K_FAST_INV = 1, K_DENSE_FWD = 2, K_DENSE_INV = 3, K_NUM = 4, K_FILTER = 4 };
 
 // Launch/layout geometry of one generated kernel (see kernel_skeleton.cuh).
 struct KernelCfg {

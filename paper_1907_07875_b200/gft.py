@@ -36,7 +36,8 @@ EXPORTS = ["gft_plan_opts_default", "gft_plan_create", "gft_plan_destroy", "gft_
            "gft_plan_compile", "gft_plan_info_get", "gft_plan_eigenvalues", "gft_plan_basis",
            "gft_plan_leaf_sizes", "gft_plan_kernel_source", "gft_plan_kernel_name",
            "gft_plan_launch_config", "gft_laplacian", "gft_decompose", "gft_find_involution",
-           "gft_status_str", "gft_last_error", "gft_abi_version"]
+           "gft_status_str", "gft_last_error", "gft_abi_version", "gft_filter_create",
+           "gft_filter_apply", "gft_filter_kernel_name", "gft_filter_kernel_source", "gft_filter_destroy"]
 
 
 class GFTError(RuntimeError):
@@ -104,6 +105,11 @@ def lib():
         "gft_status_str": (c_char_p, [c_int32]),
         "gft_last_error": (c_char_p, []),
         "gft_abi_version": (c_int32, []),
+        "gft_filter_create": (c_int32, [POINTER(c_void_p), P, P, c_uint32, c_uint32]),
+        "gft_filter_apply": (c_int32, [P, P, P, c_int64, c_int32, P]),
+        "gft_filter_kernel_name": (c_int32, [P, c_int32, c_char_p, c_size_t]),
+        "gft_filter_kernel_source": (c_int32, [P, c_int32, c_char_p, c_size_t, POINTER(c_size_t)]),
+        "gft_filter_destroy": (c_int32, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -302,6 +308,77 @@ def gft_find_involution(L, rtol=1e-10, budget=1000000):
     _check(lib().gft_find_involution(n, _ptr(L), float(rtol), int(budget), _ptr(phi), ctypes.byref(p),
                                      ctypes.byref(comp)))
     return phi, p.value, bool(comp.value)
+
+
+def gft_filter_create(plan_h, h, dtypes=("f32", "f64"), flags=0):
+    h = np.ascontiguousarray(h, dtype=np.float64)
+    mask = 0
+    for d in dtypes:
+        mask |= 1 << _dtype_code(d)
+    fh = c_void_p()
+    _check(lib().gft_filter_create(ctypes.byref(fh), plan_h, _ptr(h), mask, int(flags)))
+    return fh
+
+
+def gft_filter_apply(fh, X, Y, batch, dtype=GFT_F32, stream=None):
+    _run(lib().gft_filter_apply, fh, X, Y, batch, dtype, stream)
+
+
+def gft_filter_kernel_name(fh, dtype=GFT_F32):
+    buf = ctypes.create_string_buffer(256)
+    _check(lib().gft_filter_kernel_name(fh, _dtype_code(dtype), buf, 256))
+    return buf.value.decode()
+
+
+def gft_filter_kernel_source(fh, dtype=GFT_F32):
+    ln = c_size_t()
+    _check(lib().gft_filter_kernel_source(fh, _dtype_code(dtype), None, 0, ctypes.byref(ln)))
+    buf = ctypes.create_string_buffer(ln.value + 1)
+    _check(lib().gft_filter_kernel_source(fh, _dtype_code(dtype), buf, ln.value + 1, ctypes.byref(ln)))
+    return buf.value.decode()
+
+
+def gft_filter_destroy(fh):
+    _check(lib().gft_filter_destroy(fh))
+
+
+class Filter:
+    """Owner of a gft_filter: fused y = U diag(h) U^T x (one HBM pass)."""
+
+    def __init__(self, plan, h, dtypes=("f32", "f64"), no_cubin_cache=False, no_tensor_cores=False):
+        if len(h) != plan.n:
+            raise ValueError("h must have length n")
+        self.n = plan.n
+        flags = (GFT_FLAG_NO_CUBIN_CACHE if no_cubin_cache else 0) | \
+                (GFT_FLAG_NO_TENSOR_CORES if no_tensor_cores else 0)
+        self._h = gft_filter_create(plan.handle, h, dtypes, flags)
+
+    def apply(self, X, Y=None, stream=None):
+        import torch
+        if not X.is_cuda or X.dim() != 2 or X.shape[1] != self.n or not X.is_contiguous():
+            raise ValueError("expected a contiguous CUDA [batch, %d] tensor" % self.n)
+        if Y is None:
+            Y = torch.empty_like(X)
+        dt = GFT_F64 if X.dtype == torch.float64 else GFT_F32
+        gft_filter_apply(self._h, X, Y, X.shape[0], dt, stream)
+        return Y
+
+    def kernel_name(self, dtype="f32"):
+        return gft_filter_kernel_name(self._h, dtype)
+
+    def kernel_source(self, dtype="f32"):
+        return gft_filter_kernel_source(self._h, dtype)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            gft_filter_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ----------------------------------------------------------------------------- Plan
