@@ -78,6 +78,9 @@ typedef struct {
 
 #define GFT_FLAG_HOST_ONLY 1u      /* build the factorisation only; no kernel codegen (CPU use) */
 #define GFT_FLAG_NO_CUBIN_CACHE 2u /* always run NVRTC even if an AOT cubin for the plan exists */
+#define GFT_FLAG_NORMALIZED 8u      /* GFT of the symmetric normalised Laplacian D^-1/2 L D^-1/2
+                                       (Theorem 3 holds for it);
+                                       every degree d_i = l_ii must be > 0 */
 #define GFT_FLAG_NO_TENSOR_CORES 4u /* fp32 leaves >= 32 stay on CUDA-core FMA instead of
                                        tcgen05 3xTF32 micro-GEMMs (ablation / comparison) */
 

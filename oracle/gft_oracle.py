@@ -58,6 +58,16 @@ def laplacian(n, src, dst, w, self_loops=None):
     return L
 
 
+def normalized_laplacian(L):
+    """Symmetric normalised Laplacian D^{-1/2} L D^{-1/2} with
+    d_i = sum_j w_ij, w_ii = s_i, which equals the diagonal l_ii."""
+    d = np.diag(L).astype(np.float64)
+    if np.any(d <= 0):
+        raise ValueError("normalized Laplacian needs positive degrees")
+    r = 1.0 / np.sqrt(d)
+    return L * r[:, None] * r[None, :]
+
+
 def quadratic_form_edges(n, src, dst, w, self_loops, f):
     """f^T L f evaluated edge by edge: sum_e w (f_i - f_j)^2 + sum_k s_k f_k^2 (eq:lqf)."""
     tot = 0.0

@@ -106,6 +106,7 @@ gft_status gft_plan_create(gft_plan* out, int32_t n, int64_t n_edges, const int3
     po.min_leaf = o.min_leaf < 1 ? 1 : o.min_leaf;
     po.search_budget = o.search_budget;
     po.sym_rtol = o.sym_rtol;
+    po.normalized = (o.flags & GFT_FLAG_NORMALIZED) != 0;
     gft::SubGraph g = gft::graph_from_edges(n, n_edges, src, dst, w, self_loops);
     std::unique_ptr<gft_plan_s> p(new gft_plan_s);
     p->P = gft::build_plan(g, phi, po);

@@ -339,16 +339,47 @@ struct Builder {
 };
 }  // namespace
 
-Plan build_plan(const SubGraph& g, const int32_t* user_phi, const PlanOptions& opt) {
+SubGraph normalized_graph(const SubGraph& g) {
+  // symmetric normalised Laplacian D^{-1/2} L D^{-1/2}, d_i = sum_j w_ij with
+  // w_ii = s_i, i.e. d_i = l_ii; returned in (W, s) form via eq:sw_from_l
+  const int k = g.k;
+  std::vector<double> L = g.laplacian(), isd(k);
+  for (int i = 0; i < k; ++i) {
+    const double d = L[(size_t)i * k + i];
+    if (!(d > 0) || !std::isfinite(d))
+      fail(GFT_ERR_INVALID_ARG, "normalized Laplacian needs positive degrees (node " + std::to_string(i) + ")");
+    isd[i] = 1.0 / std::sqrt(d);
+  }
+  SubGraph h;
+  h.k = k;
+  h.W.assign((size_t)k * k, 0.0);
+  h.s.assign(k, 0.0);
+  for (int i = 0; i < k; ++i) {
+    double rs = 0;
+    for (int j = 0; j < k; ++j) {
+      const double v = L[(size_t)i * k + j] * isd[i] * isd[j];
+      rs += v;
+      if (j != i) h.W[(size_t)i * k + j] = -v;
+    }
+    h.s[i] = rs;
+  }
+  return h;
+}
+
+Plan build_plan(const SubGraph& g0, const int32_t* user_phi, const PlanOptions& opt) {
   Plan P;
-  P.n = g.k;
-  P.L = g.laplacian();
+  P.n = g0.k;
   if (user_phi) {
-    check_involution(g.k, user_phi);
-    std::vector<int> phi(user_phi, user_phi + g.k);
-    if (!is_phi_symmetric(g, phi, opt.sym_rtol))
+    check_involution(g0.k, user_phi);
+    std::vector<int> phi(user_phi, user_phi + g0.k);
+    if (!is_phi_symmetric(g0, phi, opt.sym_rtol))
       fail(GFT_ERR_NOT_SYMMETRIC, "graph is not phi-symmetric within sym_rtol (Definition 2)");
   }
+  // Theorem 3 "holds for normalized Laplacian as well": the same
+  // decomposition runs on the (W, s) form of D^{-1/2} L D^{-1/2}, which is phi-symmetric
+  // whenever the graph is (degrees are phi-invariant)
+  const SubGraph g = opt.normalized ? normalized_graph(g0) : g0;
+  P.L = g.laplacian();
   Builder B(opt, P);
   std::vector<int> pos(g.k);
   std::iota(pos.begin(), pos.end(), 0);

@@ -67,6 +67,7 @@ struct PlanOptions {
   int min_leaf = 1;
   int64_t search_budget = 1000000;
   double sym_rtol = 1e-12;
+  bool normalized = false;   // GFT of D^{-1/2} L D^{-1/2}
 };
 
 struct Plan {

@@ -181,6 +181,21 @@ def test_random_symmetric_graphs_on_gpu():
     assert worst < 1e-5
 
 
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_normalized_laplacian_gft(name):
+    """GFT of D^{-1/2} L D^{-1/2} through the same fused kernels."""
+    cfg = workloads.config(name)
+    plan = G.Plan.from_config(cfg, dtypes=("f32",), normalized=True)
+    L = oracle.normalized_laplacian(oracle.laplacian(cfg.n, cfg.src, cfg.dst, cfg.w, cfg.self_loops))
+    lam_o, U_o = oracle.gft_basis(L)
+    X = workloads.signals(cfg, batch=3001, dtype="f32")
+    Y = plan.forward(X.cuda())
+    Xr = plan.inverse(Y)
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
+
+
 def _random_big_leaf_graph(rng, n, sym):
     """Random weighted graph whose leaves are large (>= 32) so the tcgen05 path is used;
     sizes chosen to exercise K/N padding (k not a multiple of 16 or 32)."""

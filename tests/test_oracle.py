@@ -234,6 +234,28 @@ def test_theorem3_offblocks_random():
     assert np.abs(G[np.ix_([0, 1, 2], [3, 4, 5])]).max() > 1e-4
 
 
+def test_normalized_laplacian_pins():
+    """D^{-1/2} L D^{-1/2}: for a k-regular loop-free graph it is L/k (the
+    cycle C12 is 2-regular); for a bipartite graph its spectrum is symmetric about 1
+    (lambda <-> 2 - lambda, the normalised counterpart of Lemma 1 / Theorem 2)."""
+    s, d, w = workloads.cycle_graph(12)
+    L = oracle.laplacian(12, s, d, w)
+    N = oracle.normalized_laplacian(L)
+    assert np.abs(N - L / 2).max() < 1e-15
+    rng = np.random.default_rng(4)
+    pairs = [(a, 6 + b) for a in range(6) for b in range(7) if rng.random() < 0.6]
+    pairs += [(a, 6 + a) for a in range(6)]                     # keep it connected-ish
+    pairs = sorted(set(pairs))
+    s = np.array([p[0] for p in pairs]); d = np.array([p[1] for p in pairs])
+    w = rng.uniform(0.5, 2.0, len(pairs))
+    L = oracle.laplacian(13, s, d, w)
+    lam, U = oracle.gft_basis(oracle.normalized_laplacian(L))
+    assert np.abs(np.sort(2 - lam) - lam).max() < 1e-12
+    assert np.abs(lam).min() < 1e-12                              # D^{1/2} 1 is in the kernel
+    with pytest.raises(ValueError):
+        oracle.normalized_laplacian(np.zeros((2, 2)))
+
+
 @pytest.mark.parametrize("name", ["cfg3", "cfg4"])
 def test_graph_filter_closed_forms(name):
     """U diag(h) U^T: h = 1 -> I, h = lambda -> L, h = lambda^2 -> L^2, h = exp(-t lambda) ->

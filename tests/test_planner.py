@@ -210,6 +210,36 @@ def test_random_symmetric_graphs_plan_exact():
         check_basis_against_oracle(n, s, d, w, loops, plan, atol=1e-9)
 
 
+@pytest.mark.parametrize("name", ["cfg1", "cfg3", "cfg4", "cfg5a"])
+def test_normalized_laplacian_plans(name):
+    """GFT of D^{-1/2} L D^{-1/2} (NEXT-3): same decomposition, realised basis vs oracle."""
+    cfg = workloads.config(name)
+    plan = G.Plan.from_config(cfg, host_only=True, normalized=True)
+    L = oracle.normalized_laplacian(oracle.laplacian(cfg.n, cfg.src, cfg.dst, cfg.w, cfg.self_loops))
+    lam_o, U_o = oracle.gft_basis(L)
+    lam_f, U_f = plan.eigenvalues(), plan.basis()
+    assert np.abs(lam_f - lam_o).max() < 1e-12
+    assert np.abs(L @ U_f - U_f * lam_f).max() < 1e-12
+    for C in oracle.clusters(lam_o):
+        if len(C) == 1:
+            assert np.abs(U_f[:, C[0]] - U_o[:, C[0]]).max() < 1e-10
+        else:
+            assert np.abs(_proj(U_f, C) - _proj(U_o, C)).max() < 1e-10
+    if name == "cfg5a":   # 2-regular: normalised GFT = GFT with halved eigenvalues
+        plain = G.Plan.from_config(cfg, host_only=True)
+        assert np.abs(plain.eigenvalues() / 2 - lam_f).max() < 1e-13
+    # the top-level symmetry survives normalisation (degrees are phi-invariant); deeper
+    # sub-graph symmetries may not, since D^{-1/2} reweights non-regular graphs
+    assert plan.info()["units_per_level"][0] == G.Plan.from_config(cfg, host_only=True).info()["units_per_level"][0]
+
+
+def test_normalized_rejects_zero_degree():
+    s, d, w = workloads.path_graph(3)
+    with pytest.raises(G.GFTError) as e:
+        G.Plan(4, s, d, w, host_only=True, normalized=True)     # node 3 isolated
+    assert e.value.name == "GFT_ERR_INVALID_ARG"
+
+
 def test_disconnected_and_isolated_nodes():
     # two identical paths + an isolated node: components are split before searching
     s = np.array([0, 1, 3, 4], np.int32); d = np.array([1, 2, 4, 5], np.int32)
