@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -50,6 +51,11 @@ KernelCfg choose_cfg(int n, int dtype) {
   c.warps = 4;
   c.stages = 4;
   while (c.stages > 2 && c.warps * c.stages * c.tile_bytes() > 100 * 1024) --c.stages;
+  // tuning knobs for experiments (GFT_TUNE_R / _STAGES / _WARPS); defaults above
+  auto env_int = [](const char* k, int v) { const char* e = getenv(k); return (e && *e) ? atoi(e) : v; };
+  c.R = std::max(1, std::min(8, env_int("GFT_TUNE_R", c.R)));
+  c.stages = std::max(2, std::min(8, env_int("GFT_TUNE_STAGES", c.stages)));
+  c.warps = std::max(1, std::min(16, env_int("GFT_TUNE_WARPS", c.warps)));
   if (c.smem_bytes() > 227 * 1024) c.stages = 2;
   if (c.smem_bytes() > 227 * 1024) c.warps = 2;
   return c;

@@ -39,6 +39,7 @@ struct Driver {
   CUresult (*cuOccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t);
   CUresult (*cuLaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                              unsigned, CUstream, void**, void**);
+  CUresult (*cuLaunchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**);
   CUresult (*cuTensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -90,7 +91,7 @@ Driver& drv() {
   GFT_GET(cuDeviceGetAttribute); GFT_GET(cuDevicePrimaryCtxRetain); GFT_GET(cuModuleLoadData);
   GFT_GET(cuModuleUnload); GFT_GET(cuModuleGetFunction); GFT_GET(cuFuncSetAttribute);
   GFT_GET(cuFuncGetAttribute); GFT_GET(cuOccupancyMaxActiveBlocksPerMultiprocessor);
-  GFT_GET(cuLaunchKernel); GFT_GET(cuTensorMapEncodeTiled); GFT_GET(cuMemcpyHtoDAsync);
+  GFT_GET(cuLaunchKernel); GFT_GET(cuLaunchKernelEx); GFT_GET(cuTensorMapEncodeTiled); GFT_GET(cuMemcpyHtoDAsync);
   GFT_GET(cuMemcpyDtoHAsync); GFT_GET(cuStreamCreate); GFT_GET(cuEventCreate);
   GFT_GET(cuEventRecord); GFT_GET(cuStreamWaitEvent);
 #undef GFT_GET
@@ -226,6 +227,15 @@ void encode_map(CUtensorMap* m, const Kernel& k, const void* ptr, int64_t rows) 
      "cuTensorMapEncodeTiled");
 }
 
+// PDL on by default; GFT_PDL=0 disables it (ablation)
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("GFT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // max rows per launch: TMA coordinates are int32
 constexpr int64_t kMaxRowsPerLaunch = (int64_t)1 << 30;
 
@@ -305,9 +315,20 @@ void launch_kernel(Kernel& k, const void* in, void* out, int64_t batch, void* st
     const void* xin = pin;
     void* xout = pout;
     void* args[] = {&tin, &tout, &xin, &xout, &nrows};
-    ck(d.cuLaunchKernel((CUfunction)L.fn, grid, 1, 1, c.threads(), 1, 1, c.smem_bytes(),
-                        (CUstream)stream, args, nullptr),
-       "cuLaunchKernel");
+    // Programmatic dependent launch: the kernel may be scheduled while the previous kernel
+    // in the stream drains; it executes griddepcontrol.wait before its first global read.
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    CUlaunchConfig lc;
+    std::memset(&lc, 0, sizeof lc);
+    lc.gridDimX = grid; lc.gridDimY = 1; lc.gridDimZ = 1;
+    lc.blockDimX = c.threads(); lc.blockDimY = 1; lc.blockDimZ = 1;
+    lc.sharedMemBytes = c.smem_bytes();
+    lc.hStream = (CUstream)stream;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    ck(d.cuLaunchKernelEx(&lc, (CUfunction)L.fn, args, nullptr), "cuLaunchKernelEx");
   }
 }
 

@@ -141,6 +141,10 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   const long long ntiles = (batch + GFT_TILE_ROWS - 1) / GFT_TILE_ROWS;
   const long long gw = (long long)blockIdx.x * GFT_WARPS + warp;
   const long long nw = (long long)gridDim.x * GFT_WARPS;
+  // programmatic dependent launch: everything above overlaps the previous kernel's tail;
+  // no global memory is touched before the previous grid has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (gw >= ntiles) return;
 
   // partial tiles can only be handled by TMA tensor copies (OOB fill / clip); in bulk

@@ -122,6 +122,9 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * GFT_STAGES + GFT_NTC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const long long ntiles = (batch + GFT_TILE_ROWS - 1) / GFT_TILE_ROWS;
+  // programmatic dependent launch: wait for the previous grid before touching global memory
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {   // TMEM allocation (whole warp), then release the permit
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
