@@ -51,6 +51,13 @@ KernelCfg choose_cfg(int n, int dtype) {
   c.warps = 4;
   c.stages = 4;
   while (c.stages > 2 && c.warps * c.stages * c.tile_bytes() > 100 * 1024) --c.stages;
+  // measured geometry for this (n, dtype) if the tuning table has one (tools/gpu_autotune.py)
+  int tR, tS, tW;
+  if (tuned_geometry(n, dtype, tR, tS, tW)) {
+    c.R = tR;
+    c.stages = tS;
+    c.warps = tW;
+  }
   // tuning knobs for experiments (GFT_TUNE_R / _STAGES / _WARPS); defaults above
   auto env_int = [](const char* k, int v) { const char* e = getenv(k); return (e && *e) ? atoi(e) : v; };
   c.R = std::max(1, std::min(8, env_int("GFT_TUNE_R", c.R)));

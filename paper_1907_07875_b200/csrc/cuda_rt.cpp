@@ -241,6 +241,33 @@ constexpr int64_t kMaxRowsPerLaunch = (int64_t)1 << 30;
 
 }  // namespace
 
+bool tuned_geometry(int n, int dtype, int& R, int& S, int& W) {
+  struct Entry { int n, dt, R, S, W; };
+  static const std::vector<Entry> table = [] {
+    std::vector<Entry> t;
+    const char* e = getenv("GFT_TUNING_FILE");
+    std::string path = (e && *e) ? std::string(e) : lib_dir() + "/../tuning.tsv";
+    if (path == "none") return t;
+    std::ifstream f(path);
+    std::string line;
+    while (std::getline(f, line)) {
+      std::istringstream ss(line);
+      std::string mode, dt;
+      Entry x;
+      if (!(ss >> mode >> x.n >> dt >> x.R >> x.S >> x.W) || mode != "fma") continue;
+      x.dt = dt == "f64" ? GFT_F64 : GFT_F32;
+      t.push_back(x);
+    }
+    return t;
+  }();
+  for (const Entry& x : table)
+    if (x.n == n && x.dt == dtype) {
+      R = x.R; S = x.S; W = x.W;
+      return true;
+    }
+  return false;
+}
+
 std::string cubin_cache_dir() {
   const char* e = getenv("GFT_CUBIN_DIR");
   if (e && *e) return e;

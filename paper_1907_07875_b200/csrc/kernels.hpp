@@ -77,4 +77,9 @@ void execute_host(Kernel& k, const void* in_host, void* out_host, int64_t batch,
 
 std::string cubin_cache_dir();
 
+// Measured geometry table (paper_1907_07875_b200/tuning.tsv, written by
+// tools/gpu_autotune.py on a B200): lines "fma <n> <f32|f64> <R> <S> <W>".  Returns false
+// if (n, dtype) has no entry.  GFT_TUNING_FILE overrides the path ("none" disables).
+bool tuned_geometry(int n, int dtype, int& R, int& S, int& W);
+
 }  // namespace gft

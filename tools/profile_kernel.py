@@ -39,9 +39,17 @@ def main():
         torch.cuda.synchronize()
         times.append(s.elapsed_time(e))
     nbytes = 2 * B * cfg.n * X.element_size()
+    # back-to-back launches between two events (no idle gaps between kernels)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(20):
+        fn(X, Y)
+    e.record()
+    torch.cuda.synchronize()
+    b2b = s.elapsed_time(e) / 20
     print(json.dumps({"config": a.config, "kind": a.kind, "dtype": dt, "kernel": plan.kernel_name(a.kind, dt),
                       "launch": plan.launch_config(a.kind, dt, B), "ms": times,
-                      "gbs_best": nbytes / min(times) / 1e6}))
+                      "gbs_best": nbytes / min(times) / 1e6, "b2b_ms": b2b, "b2b_gbs": nbytes / b2b / 1e6}))
 
 
 if __name__ == "__main__":
