@@ -46,11 +46,12 @@ KernelCfg choose_cfg(int n, int dtype) {
     // odd row pitch in vector units makes thread-per-row accesses conflict-free
     c.vec = (c.elem == 4 && n % 2 == 0) ? 2 : 1;
   }
+  // Default geometry (what the B200 sweeps in profiles/r01/autotune favour): warp tiles of
+  // ~8 KiB, double-buffered, up to 8 warps = ~128 KiB SMEM and one persistent CTA per SM.
   c.R = 1;
-  while (c.R < 8 && c.tile_bytes() < 4096) c.R *= 2;
-  c.warps = 4;
-  c.stages = 4;
-  while (c.stages > 2 && c.warps * c.stages * c.tile_bytes() > 100 * 1024) --c.stages;
+  while (c.R < 8 && c.tile_bytes() < 8192 && 2 * c.tile_bytes() <= 16384) c.R *= 2;
+  c.stages = 2;
+  c.warps = std::max(2, std::min(8, (128 * 1024) / (c.stages * c.tile_bytes())));
   // measured geometry for this (n, dtype) if the tuning table has one (tools/gpu_autotune.py)
   int tR, tS, tW;
   if (tuned_geometry(n, dtype, tR, tS, tW)) {
