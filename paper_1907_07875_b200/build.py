@@ -32,7 +32,8 @@ SOURCES = ["plan.cpp", "search.cpp", "codegen.cpp", "cuda_rt.cpp", "capi.cpp"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
-SKELETONS = {"kernel_skeleton.cuh": "skeleton_inc.h", "kernel_tc_skeleton.cuh": "skeleton_tc_inc.h"}
+SKELETONS = {"kernel_skeleton.cuh": "skeleton_inc.h", "kernel_tc_skeleton.cuh": "skeleton_tc_inc.h",
+             "kernel_tc2_skeleton.cuh": "skeleton_tc2_inc.h"}
 
 
 def _write_skeleton_inc():

@@ -26,6 +26,9 @@ static const char* kSkeleton =
 static const char* kSkeletonTC =
 #include "skeleton_tc_inc.h"
     ;
+static const char* kSkeletonTC2 =
+#include "skeleton_tc2_inc.h"
+    ;
 
 KernelCfg choose_cfg(int n, int dtype) {
   KernelCfg c;
@@ -188,7 +191,8 @@ float tf32_rna_host(float v) {
   return r;
 }
 
-bool plan_tc(const Plan& P, int dtype, int stages, std::vector<TcLeaf>& out, int& tmem_cols,
+// pair: CTA-pair (cta_group::2) variant -- each CTA stores half of every B operand.
+bool plan_tc(const Plan& P, int dtype, int stages, bool pair, std::vector<TcLeaf>& out, int& tmem_cols,
              int& b_bytes) {
   out.clear();
   if (dtype != GFT_F32 || P.n % 32 != 0 || P.n > 256) return false;
@@ -207,7 +211,7 @@ bool plan_tc(const Plan& P, int dtype, int stages, std::vector<TcLeaf>& out, int
     t.kp32 = ru(t.k, 32);
     t.np = ru(t.k, 16);
     const int need = 2 * ru(t.kp8, 32) + ru(t.np, 32);
-    const int bsz = 2 * t.np * t.kp32 * 4;
+    const int bsz = 2 * t.np * t.kp32 * 4 / (pair ? 2 : 1);
     if (cols + need > 512 || stages * tile + bytes + bsz + 2048 > 227 * 1024 || t.np > 256) continue;
     t.hi_col = cols;
     t.lo_col = cols + ru(t.kp8, 32);
@@ -269,27 +273,35 @@ void emit_units(std::ostringstream& o, const Plan& P, const char* arr, bool reve
   o << "  (void)a_; (void)b_; }\n";
 }
 
-void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, std::ostringstream& o) {
+void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, bool pair, std::ostringstream& o) {
   const int dtype = GFT_F32;
   std::vector<char> is_tc(P.leaves.size(), 0);
   for (const auto& t : T) is_tc[t.leaf] = 1;
-  // ---- B operands, atom order (leaf, hi|lo, k-atom, row n, 32 k) ----
+  // ---- B operands, atom order (CTA half, leaf, hi|lo, k-atom, row n, 32 k) ----
+  // single CTA: all Np rows; CTA pair: rank r keeps rows [r*Np/2, (r+1)*Np/2)
   std::vector<float> B;
-  for (const auto& t : T) {
-    const Leaf& lf = P.leaves[t.leaf];
-    for (int part = 0; part < 2; ++part)
-      for (int a = 0; a < t.kp32 / 32; ++a)
-        for (int n = 0; n < t.np; ++n)
-          for (int kk = 32 * a; kk < 32 * a + 32; ++kk) {
-            float v = 0.f;
-            if (n < t.k && kk < t.k)   // B[n = output][k = input]
-              v = (float)leaf_coef(lf, d, n, kk);
-            const float hi = tf32_rna_host(v);
-            B.push_back(part == 0 ? hi : v - hi);
-          }
-  }
-  o << "#define GFT_B_FLOATS " << B.size() << "\n";
-  o << "__device__ __align__(16) const float gft_tcB[" << B.size() << "] = {\n";
+  const int halves = pair ? 2 : 1;
+  for (int r = 0; r < halves; ++r)
+    for (const auto& t : T) {
+      const Leaf& lf = P.leaves[t.leaf];
+      const int rows = t.np / halves;
+      for (int part = 0; part < 2; ++part)
+        for (int a = 0; a < t.kp32 / 32; ++a)
+          for (int n = r * rows; n < (r + 1) * rows; ++n)
+            for (int kk = 32 * a; kk < 32 * a + 32; ++kk) {
+              float v = 0.f;
+              if (n < t.k && kk < t.k)   // B[n = output][k = input]
+                v = (float)leaf_coef(lf, d, n, kk);
+              const float hi = tf32_rna_host(v);
+              B.push_back(part == 0 ? hi : v - hi);
+            }
+    }
+  const size_t per_cta = B.size() / halves;
+  o << "#define GFT_B_FLOATS " << per_cta << "\n";
+  if (pair)
+    o << "__device__ __align__(16) const float gft_tcB[2][" << per_cta << "] = {\n";
+  else
+    o << "__device__ __align__(16) const float gft_tcB[" << per_cta << "] = {\n";
   for (size_t i = 0; i < B.size(); ++i) {
     char buf[48];
     std::snprintf(buf, sizeof buf, "%af,", (double)B[i]);
@@ -297,10 +309,15 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, std::ostrin
   }
   o << "};\n";
   o << "#define GFT_NTC " << T.size() << "\n";
-  o << "static __device__ __forceinline__ void gft_tile(float (&x)[GFT_N], float (&y)[GFT_N], u32 tm,\n"
-       "    u32 tmem, u32 bsm, u32 mbar, u32 par, int tid) {\n";
+  if (pair)
+    o << "static __device__ __forceinline__ void gft_tile(float (&x)[GFT_N], float (&y)[GFT_N], u32 tm,\n"
+         "    u32 tmem, u32 bsm, u32 mbar, u32 staged0, u32 staged_local, u32 par, int tid, u32 rank) {\n";
+  else
+    o << "static __device__ __forceinline__ void gft_tile(float (&x)[GFT_N], float (&y)[GFT_N], u32 tm,\n"
+         "    u32 tmem, u32 bsm, u32 mbar, u32 par, int tid) {\n";
   // ---- front: butterflies (forward) ----
   if (d != DIR_INV) emit_units(o, P, "x", false, dtype);
+  std::ostringstream iss;   // body of gft_issue_pair (CTA-pair variant)
   for (size_t ti = 0; ti < T.size(); ++ti) {
     const TcLeaf& t = T[ti];
     const Leaf& lf = P.leaves[t.leaf];
@@ -321,32 +338,45 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, std::ostrin
       emit_tmem_st(o, "l", t.lo_col + c0, w);
       o << "  }\n";
     }
-    // ---- all 128 lanes staged -> one thread issues this leaf's MMAs and commits ----
-    o << "  tc_wait_st(); tc_fence_before(); named_bar(1, 128);\n";
-    o << "  if (tid == 0) {\n  tc_fence_after();\n";
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(t.np >> 3) << 17) | (8u << 24);
+    // ---- this leaf's MMAs (issued by one thread once all lanes are staged) ----
+    std::ostringstream mm;
+    const uint32_t mdim = pair ? 16u : 8u;   // M = 256 (pair) or 128
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(t.np >> 3) << 17) | (mdim << 24);
     const int ksteps = t.kp8 / 8;
-    const int atom_bytes = t.np * 128;
+    const int atom_bytes = (t.np / (pair ? 2 : 1)) * 128;
     for (int pass = 0; pass < 3; ++pass) {
       // pass 0: A_hi B_hi, pass 1: A_hi B_lo, pass 2: A_lo B_hi
       const int acol = pass == 2 ? t.lo_col : t.hi_col;
       const int boff = pass == 1 ? t.blo_off : t.bhi_off;
       for (int j = 0; j < ksteps; ++j) {
         const int bo = boff + (j / 4) * atom_bytes + (j % 4) * 32;
-        o << "  mma_ts(tmem + " << t.d_col << "u, tmem + " << (acol + 8 * j) << "u, smem_desc_sw128(bsm + " << bo
-          << "u), " << idesc << "u, " << ((pass == 0 && j == 0) ? 0 : 1) << "u);\n";
+        mm << (pair ? "  mma_ts2(" : "  mma_ts(") << "tmem + " << t.d_col << "u, tmem + " << (acol + 8 * j)
+           << "u, smem_desc_sw128(bsm + " << bo << "u), " << idesc << "u, " << ((pass == 0 && j == 0) ? 0 : 1)
+           << "u);\n";
       }
     }
-    o << "  tc_commit(mbar + " << 8 * ti << "u);\n  }\n";
+    if (pair) {
+      // 8 warps of the pair arrive on the leader's `staged` barrier; the leader's issuer warp
+      // (gft_issue_pair) waits for it and issues -- compute warps never block on the issue
+      if (ti + 1 == T.size()) o << "  signal_staged(staged0);\n";   // one arrive per warp per tile
+      if (ti == 0) iss << "  mbar_wait_acq_cluster(staged_local, par); tc_fence_after();\n";
+      iss << mm.str();
+      if (ti + 1 == T.size()) iss << "  tc_commit_pair(mbar);\n";   // tracks all MMAs issued before it
+    } else {
+      o << "  tc_wait_st(); tc_fence_before(); named_bar(1, 128);\n";
+      o << "  if (tid == 0) {\n  tc_fence_after();\n" << mm.str();
+      o << "  tc_commit(mbar + " << 8 * ti << "u);\n  }\n";
+    }
   }
   // ---- small leaves on CUDA cores (overlap the tensor-core work) ----
   for (size_t l = 0; l < P.leaves.size(); ++l)
     if (!is_tc[l]) emit_leaf_fma(o, P.leaves[l], l, d, dtype);
   // ---- epilogue: per leaf, wait for its MMAs, accumulators -> registers ----
+  if (pair) o << "  mbar_wait(mbar, par); tc_fence_after();\n";
   for (size_t ti = 0; ti < T.size(); ++ti) {
     const TcLeaf& t = T[ti];
     const Leaf& lf = P.leaves[t.leaf];
-    o << "  mbar_wait(mbar + " << 8 * ti << "u, par); tc_fence_after();\n";
+    if (!pair) o << "  mbar_wait(mbar + " << 8 * ti << "u, par); tc_fence_after();\n";
     for (int r0 = 0; r0 < t.k; r0 += 32) {
       const int w = std::min(32, t.np - r0);
       o << "  { u32 d[" << w << "];\n";
@@ -359,6 +389,10 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, std::ostrin
   // ---- back: reverse butterflies (inverse) ----
   if (d != DIR_FWD) emit_units(o, P, "y", true, dtype);
   o << "}\n";
+  if (pair) {
+    o << "static __device__ __forceinline__ void gft_issue_pair(u32 tmem, u32 bsm, u32 mbar, u32 staged_local,\n"
+         "    u32 par) {\n" << iss.str() << "}\n";
+  }
 }
 
 }  // namespace
@@ -371,11 +405,26 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
   const Dir dir = kind == K_FAST_INV ? DIR_INV : kind == K_FILTER ? DIR_FILTER : DIR_FWD;
   if (allow_tc && (kind == K_FAST_FWD || kind == K_FAST_INV || kind == K_FILTER)) {
     std::vector<TcLeaf> T;
-    int tmem_cols = 0, b_bytes = 0;
-    const int stages = 2;
-    if (plan_tc(P, dtype, stages, T, tmem_cols, b_bytes)) {
+    int tmem_cols = 0, b_bytes = 0, stages = 3;
+    bool pair = false, ok = false;
+    // CTA pair first (3 tile buffers if they fit, else 2), then the single-CTA variant;
+    // every big leaf must land on the tensor core for the pair variant to be chosen
+    int nbig = 0;
+    for (const auto& lf : P.leaves) nbig += lf.k >= 32;
+    for (int st = 3; st >= 2 && !ok; --st)
+      if (plan_tc(P, dtype, st, true, T, tmem_cols, b_bytes) && (int)T.size() == nbig &&
+          getenv("GFT_NO_CTA_PAIR") == nullptr) {
+        ok = pair = true;
+        stages = st;
+      }
+    if (!ok) {
+      stages = 2;
+      ok = plan_tc(P, dtype, stages, false, T, tmem_cols, b_bytes);
+    }
+    if (ok) {
       KernelCfg& c = k.cfg;
       c.tc = 1;
+      c.tc_pair = pair ? 1 : 0;
       c.stages = stages;
       c.mode = 0;
       c.boxc = 32;
@@ -386,18 +435,18 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
       c.tc_b_bytes = b_bytes;
       c.tc_tmem_cols = tmem_cols;
       std::ostringstream gen;
-      generate_tc(P, dir, T, gen);
+      generate_tc(P, dir, T, pair, gen);
       std::ostringstream pre;
       pre << "#define GFT_N " << c.n << "\n#define GFT_STAGES " << c.stages << "\n#define GFT_TMEM_COLS "
           << tmem_cols << "\n";
-      const std::string skel(kSkeletonTC);
+      const std::string skel(pair ? kSkeletonTC2 : kSkeletonTC);
       const std::string marker = "// @@GFT_GENERATED@@";
       const size_t at = skel.find(marker);
       if (at == std::string::npos) fail(GFT_ERR_COMPILE, "TC skeleton marker missing");
       const std::string key = pre.str() + gen.str() + skel;
       char hbuf[32];
       std::snprintf(hbuf, sizeof hbuf, "%016llx", (unsigned long long)fnv1a(key));
-      k.name = std::string("gft_") + kKindNameTC[kind] + "_f32_n" + std::to_string(c.n) + "_" + hbuf;
+      k.name = std::string("gft_") + kKindNameTC[kind] + (pair ? "2" : "") + "_f32_n" + std::to_string(c.n) + "_" + hbuf;
       std::ostringstream src;
       src << "// generated by paper_1907_07875_b200 codegen.cpp — plan-specialised GFT kernel with\n"
           << "// tcgen05 3xTF32 leaves (" << T.size() << " tensor-core leaves)\n"

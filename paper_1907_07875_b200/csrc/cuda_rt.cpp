@@ -195,9 +195,11 @@ LoadedFn& ensure_loaded(Kernel& k, CUcontext ctx, bool allow_cache) {
   const int smem = k.cfg.smem_bytes();
   ck(d.cuFuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem),
      "cuFuncSetAttribute(max dynamic smem)");
-  int occ = 0;
-  ck(d.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, k.cfg.threads(), smem), "occupancy");
-  if (occ < 1) fail(GFT_ERR_CUDA, "kernel " + k.name + " cannot be resident (occupancy 0)");
+  int occ = 1;
+  if (!k.cfg.tc_pair) {   // (cluster kernels: one CTA per SM by construction)
+    ck(d.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, k.cfg.threads(), smem), "occupancy");
+    if (occ < 1) fail(GFT_ERR_CUDA, "kernel " + k.name + " cannot be resident (occupancy 0)");
+  }
   CUdevice dev;
   ck(d.cuCtxGetDevice(&dev), "cuCtxGetDevice");
   int sms = 0;
@@ -206,6 +208,7 @@ LoadedFn& ensure_loaded(Kernel& k, CUcontext ctx, bool allow_cache) {
   L.module = mod;
   L.fn = fn;
   L.grid_max = sms * occ;
+  if (k.cfg.tc_pair) L.grid_max &= ~1;
   return k.loaded.emplace(ctx, L).first->second;
 }
 
@@ -336,8 +339,9 @@ void launch_kernel(Kernel& k, const void* in, void* out, int64_t batch, void* st
       encode_map(&tout, k, pout, rows);
     }
     const int64_t tiles = (rows + c.tile_rows() - 1) / c.tile_rows();
-    const int64_t ctas = (tiles + c.tiles_per_cta() - 1) / c.tiles_per_cta();
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, L.grid_max));
+    int64_t ctas = (tiles + c.tiles_per_cta() - 1) / c.tiles_per_cta();
+    if (c.tc_pair) ctas = (ctas + 1) & ~int64_t(1);
+    const unsigned grid = (unsigned)std::max<int64_t>(c.tc_pair ? 2 : 1, std::min<int64_t>(ctas, L.grid_max));
     long long nrows = rows;
     const void* xin = pin;
     void* xout = pout;

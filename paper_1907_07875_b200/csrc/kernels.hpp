@@ -25,11 +25,12 @@ struct KernelCfg {
   // tensor-core variant (kernel_tc_skeleton.cuh): one 128-row tile per CTA iteration,
   // 4 compute warps + 1 TMA warp, big leaves as tcgen05 3xTF32 micro-GEMMs
   int tc = 0;
+  int tc_pair = 0;              // CTA-pair (cta_group::2, cluster of 2) variant, grid must be even
   int tc_b_bytes = 0;           // SMEM bytes of the B operands
   int tc_tmem_cols = 0;         // TMEM columns allocated
   int tile_rows() const { return tc ? 128 : 32 * R; }
   int tile_bytes() const { return tile_rows() * n * elem; }
-  int threads() const { return tc ? 160 : warps * 32; }
+  int threads() const { return tc ? (tc_pair ? 192 : 160) : warps * 32; }
   int tiles_per_cta() const { return tc ? 1 : warps; }   // tiles processed concurrently per CTA
   int smem_bytes() const {
     if (tc) return stages * tile_bytes() + tc_b_bytes + (2 * stages + 8) * 8 + 16 + 1024;

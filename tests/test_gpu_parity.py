@@ -181,6 +181,27 @@ def test_random_symmetric_graphs_on_gpu():
     assert worst < 1e-5
 
 
+def test_tensor_core_single_cta_and_pair_variants_agree(monkeypatch):
+    """cfg5b through both tcgen05 variants: the CTA-pair (cta_group::2, default) kernel and
+    the single-CTA kernel (GFT_NO_CTA_PAIR=1) against the oracle and each other."""
+    cfg = workloads.config("cfg5b")
+    pair = G.Plan.from_config(cfg, dtypes=("f32",), no_cubin_cache=True)
+    monkeypatch.setenv("GFT_NO_CTA_PAIR", "1")
+    single = G.Plan.from_config(cfg, dtypes=("f32",), no_cubin_cache=True)
+    monkeypatch.delenv("GFT_NO_CTA_PAIR")
+    assert "tc2_" in pair.kernel_name(G.K_FAST_FWD) and "tc_" in single.kernel_name(G.K_FAST_FWD)
+    lam_o, U_o = oracle_basis("cfg5b")
+    X = workloads.signals(cfg, batch=1000, dtype="f32")   # ragged: 1000 = 3 pair tiles + 232 rows
+    Xd = X.cuda()
+    for plan in (pair, single):
+        Y = plan.forward(Xd)
+        Xr = plan.inverse(Y)
+        torch.cuda.synchronize()
+        check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
+        assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
+    assert oracle.relative_error(pair.forward(Xd).cpu().numpy(), single.forward(Xd).cpu().numpy()).max() < 1e-6
+
+
 @pytest.mark.parametrize("name", ["cfg3", "cfg4"])
 def test_normalized_laplacian_gft(name):
     """GFT of D^{-1/2} L D^{-1/2} through the same fused kernels."""
