@@ -37,14 +37,17 @@ def load_peaks():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def load_traffic(kernel_prefix, config):
-    """dram bytes per launch from the committed ncu --set full summary, if any."""
+def load_traffic(kernel_prefix, config, dtype="f32", kernel_name=None):
+    """dram bytes per launch from the committed ncu --set full summary, if any (only when
+    the captured kernel is the one being timed: same generated-kernel name)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
         for row in d.get("kernels", []):
-            if row.get("config") == config and row.get("kind") == kernel_prefix:
+            if (row.get("config") == config and row.get("kind") == kernel_prefix
+                    and row.get("tag") in (None, dtype)
+                    and (kernel_name is None or row.get("kernel") == kernel_name)):
                 return row.get("dram_bytes_per_launch")
     except Exception:
         pass
@@ -345,7 +348,8 @@ def main():
     dom_kind, dom_ms = (0, fwd_ms) if fwd_ms >= inv_ms else (1, inv_ms)
     achieved = bytes_per_launch / (dom_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": load_traffic(KIND_NAMES[dom_kind], args.config),
+                "frac": round(achieved / hbm, 4),
+                "traffic": load_traffic(KIND_NAMES[dom_kind], args.config, dtype, plan.kernel_name(dom_kind, dtype)),
                 "kernel": plan.kernel_name(dom_kind, dtype), "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": round(dom_ms, 5),
                 "nominal_8tbs_frac": round(achieved / 8000.0, 4)}
