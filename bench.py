@@ -198,6 +198,15 @@ def config_table(args, stream, hbm, device):
         row["cublas_fwd"] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
                              "frac": round(nbytes / ms / 1e6 / hbm, 4)}
         row["fast_vs_best_dense_fwd"] = round(min(row["dense_fwd"]["ms"], ms) / row["fast_fwd"]["ms"], 3)
+        if dtype == "f32" and cfg.n % 32 == 0:
+            # dense U^T x as one tcgen05 3xTF32 leaf: the strongest dense kernel (HBM-bound too)
+            dplan = gft.Plan.from_config(cfg, dtypes=(dtype,), dense_tc=True)
+            ms = time_kernel(lambda: dplan.dense_forward(X, Y, stream), stream, 3, args.table_iters)
+            row["dense_tc_fwd"] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
+                                   "frac": round(nbytes / ms / 1e6 / hbm, 4),
+                                   "kernel": dplan.kernel_name(2, dtype)}
+            row["fast_vs_dense_tc_fwd"] = round(ms / row["fast_fwd"]["ms"], 3)
+            dplan.close()
         rows.append(row)
         del X, Y
         filt.close()

@@ -123,6 +123,12 @@ def build_aot_cubins(jobs=8, verbose=True):
                 # the fused heat-kernel filter exp(-lambda) timed by bench.py
                 filt = G.Filter(plan, np.exp(-plan.eigenvalues()), dtypes=(dt,))
                 todo.setdefault(filt.kernel_name(dt), filt.kernel_source(dt))
+                if dt == "f32" and cfg.n % 32 == 0:
+                    # tensor-core dense comparison kernels timed by bench.py
+                    dplan = G.Plan(cfg.n, cfg.src, cfg.dst, cfg.w, cfg.self_loops, cfg.phi, max_depth=md,
+                                   dtypes=(dt,), dense_tc=True)
+                    for kind in (2, 3):
+                        todo.setdefault(dplan.kernel_name(kind, dt), dplan.kernel_source(kind, dt))
     nvcc = os.path.join(CUDA_HOME, "bin", "nvcc")
     pending = [(n, s) for n, s in todo.items() if not os.path.exists(os.path.join(KDIR, n + ".cubin"))]
     with tempfile.TemporaryDirectory() as td:

@@ -118,7 +118,8 @@ gft_status gft_plan_create(gft_plan* out, int32_t n, int64_t n_edges, const int3
         if (!(o.dtypes & (1u << dt))) continue;
         for (int kind = 0; kind < gft::K_NUM; ++kind) {
           p->k[dt][kind].reset(new gft::Kernel);
-          gft::generate_kernel(p->P, kind, dt, *p->k[dt][kind], !(o.flags & GFT_FLAG_NO_TENSOR_CORES));
+          gft::generate_kernel(p->P, kind, dt, *p->k[dt][kind], !(o.flags & GFT_FLAG_NO_TENSOR_CORES),
+                               (o.flags & GFT_FLAG_DENSE_TC) != 0);
         }
       }
     }

@@ -397,7 +397,29 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, bool pair, 
 
 }  // namespace
 
-void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc) {
+void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc, bool dense_tc) {
+  if (dense_tc && allow_tc && (kind == K_DENSE_FWD || kind == K_DENSE_INV)) {
+    // dense U^T x on tensor cores: the whole basis as ONE leaf (no butterflies), generated by
+    // the same tcgen05 path -- the strongest dense comparison for n >= 32
+    Plan D;
+    D.n = P.n;
+    Leaf lf;
+    lf.k = P.n;
+    for (int i = 0; i < P.n; ++i) { lf.pos.push_back(i); lf.slot.push_back(i); }
+    lf.M.assign((size_t)P.n * P.n, 0.0);
+    for (int r = 0; r < P.n; ++r)
+      for (int c = 0; c < P.n; ++c) lf.M[(size_t)r * P.n + c] = P.U[(size_t)c * P.n + r];   // M = U^T
+    D.leaves.push_back(lf);
+    generate_kernel(D, kind == K_DENSE_FWD ? K_FAST_FWD : K_FAST_INV, dtype, k, true, false);
+    if (k.cfg.tc) {
+      k.kind = kind;
+      const std::string old = k.name;
+      k.name = "gft_d" + old.substr(4);                      // gft_fwdtc... -> gft_dfwdtc...
+      size_t at;
+      while ((at = k.source.find(old)) != std::string::npos) k.source.replace(at, old.size(), k.name);
+      return;
+    }
+  }
   k.kind = kind;
   k.dtype = dtype;
   k.cfg = choose_cfg(P.n, dtype);

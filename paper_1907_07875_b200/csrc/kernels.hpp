@@ -60,7 +60,8 @@ struct Kernel {
 
 // Emits the full CUDA source (prelude + gft_body + skeleton) for a plan.
 // allow_tc: fast kernels of fp32 plans with leaves >= 32 use the tcgen05 3xTF32 skeleton.
-void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc);
+// dense_tc: the dense comparison kernels use the tcgen05 path (whole basis as one leaf).
+void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc, bool dense_tc = false);
 
 // Compiles k.source to an sm_100a cubin (AOT cache lookup first unless disabled).
 void compile_kernel(Kernel& k, bool allow_cache);

@@ -22,6 +22,7 @@ LIB_PATH = os.environ.get("GFT_LIB", os.path.join(_HERE, "_lib", "libgft.so"))
 
 GFT_F32, GFT_F64 = 0, 1
 GFT_FLAG_HOST_ONLY, GFT_FLAG_NO_CUBIN_CACHE, GFT_FLAG_NO_TENSOR_CORES, GFT_FLAG_NORMALIZED = 1, 2, 4, 8
+GFT_FLAG_DENSE_TC = 16
 K_FAST_FWD, K_FAST_INV, K_DENSE_FWD, K_DENSE_INV = 0, 1, 2, 3
 GFT_MAX_LEVELS = 64
 
@@ -387,7 +388,7 @@ class Plan:
 
     def __init__(self, n, src, dst, w, self_loops=None, phi=None, *, max_depth=-1, min_leaf=1,
                  search_budget=1000000, sym_rtol=1e-12, dtypes=("f32", "f64"), host_only=False,
-                 no_cubin_cache=False, no_tensor_cores=False, normalized=False):
+                 no_cubin_cache=False, no_tensor_cores=False, normalized=False, dense_tc=False):
         o = gft_plan_opts_default()
         o.max_depth = max_depth
         o.min_leaf = min_leaf
@@ -398,7 +399,7 @@ class Plan:
             o.dtypes |= 1 << _dtype_code(d)
         o.flags = ((GFT_FLAG_HOST_ONLY if host_only else 0) | (GFT_FLAG_NO_CUBIN_CACHE if no_cubin_cache else 0)
                    | (GFT_FLAG_NO_TENSOR_CORES if no_tensor_cores else 0)
-                   | (GFT_FLAG_NORMALIZED if normalized else 0))
+                   | (GFT_FLAG_NORMALIZED if normalized else 0) | (GFT_FLAG_DENSE_TC if dense_tc else 0))
         self.n = int(n)
         self._h = gft_plan_create(n, src, dst, w, self_loops, phi, o)
 

@@ -111,6 +111,21 @@ def test_dense_kernel_vs_oracle(name, dtype):
     assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL[dtype]
 
 
+@pytest.mark.parametrize("name", ["cfg4", "cfg5b"])
+def test_dense_tensor_core_kernel_vs_oracle(name):
+    """GFT_FLAG_DENSE_TC: dense U^T x as one tcgen05 3xTF32 leaf."""
+    cfg = workloads.config(name)
+    plan = G.Plan.from_config(cfg, dtypes=("f32",), dense_tc=True)
+    assert "dfwdtc" in plan.kernel_name(G.K_DENSE_FWD)
+    lam_o, U_o = oracle_basis(name)
+    X = workloads.signals(cfg, batch=2051, dtype="f32")
+    Y = plan.dense_forward(X.cuda())
+    Xr = plan.dense_inverse(Y)
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
+
+
 @pytest.mark.parametrize("batch", [0, 1, 31, 32, 33, 127, 128, 129, 1000])
 @pytest.mark.parametrize("name", ["cfg3", "cfg5a"])   # bulk (odd n) and TMA layouts
 def test_small_and_ragged_batches(name, batch):
