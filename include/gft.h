@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GFT_ABI_VERSION 1
+#define GFT_ABI_VERSION 2
 #if defined(__GNUC__)
 #define GFT_API __attribute__((visibility("default")))
 #else
@@ -86,6 +86,10 @@ typedef struct {
                                        instead of CUDA-core FMA: the strongest dense baseline */
 #define GFT_FLAG_NO_TENSOR_CORES 4u /* fp32 leaves >= 32 stay on CUDA-core FMA instead of
                                        tcgen05 3xTF32 micro-GEMMs (ablation / comparison) */
+#define GFT_FLAG_NO_RIGHT_HAAR 32u  /* do not factor right Haar stages (PAPER.md:218-269,
+                                       eq:right_gft) out of symmetry-free bipartite leaves
+                                       whose Laplacian diagonal is constant; such leaves then
+                                       stay one dense block */
 
 typedef struct {
   int32_t n;
@@ -106,6 +110,9 @@ typedef struct {
   int32_t kernels_ready;                  /* bitmask of dtypes with compiled kernels */
   double residual;                        /* max |L U_f - U_f Lambda| of the realised basis */
   double orth_error;                      /* max |U_f^T U_f - I| */
+  int32_t n_right_stages;                 /* right Haar stages (bipartite leaves split E | F) */
+  int32_t n_right_pairs;                  /* coefficient butterflies of those stages (2 adds
+                                             each, counted in `adds`) */
 } gft_plan_info;
 
 /* ---- plan lifecycle -------------------------------------------------------------- */

@@ -107,6 +107,7 @@ gft_status gft_plan_create(gft_plan* out, int32_t n, int64_t n_edges, const int3
     po.search_budget = o.search_budget;
     po.sym_rtol = o.sym_rtol;
     po.normalized = (o.flags & GFT_FLAG_NORMALIZED) != 0;
+    po.right_haar = (o.flags & GFT_FLAG_NO_RIGHT_HAAR) == 0;
     gft::SubGraph g = gft::graph_from_edges(n, n_edges, src, dst, w, self_loops);
     std::unique_ptr<gft_plan_s> p(new gft_plan_s);
     p->P = gft::build_plan(g, phi, po);
@@ -181,19 +182,73 @@ gft_status gft_filter_create(gft_filter* out, gft_plan plan, const double* h, ui
     std::unique_ptr<gft_filter_s> f(new gft_filter_s);
     f->P = plan->P;
     f->flags = flags;
-    for (auto& lf : f->P.leaves) {
-      const int k = lf.k;
-      std::vector<double> F((size_t)k * k, 0.0);
-      for (int r = 0; r < k; ++r) {
-        const double hr = h[lf.slot[r]];
-        if (hr == 0.0) continue;
-        for (int c = 0; c < k; ++c) {
-          const double a = lf.M[(size_t)r * k + c] * hr;
-          for (int c2 = 0; c2 < k; ++c2) F[(size_t)c * k + c2] += a * lf.M[(size_t)r * k + c2];
+    // Each block's coefficient rows (row r: y[slot] = row . x[pos]).  A right Haar stage
+    // couples its E and F leaves through the coefficient butterflies, so the pair becomes ONE
+    // block on pos_E ++ pos_F with rows (m_E, m_F) and s (m_E, -m_F);
+    // F = sum_r h_slot(r) row_r row_r^T in every case.
+    const gft::Plan& P0 = plan->P;
+    std::vector<gft::Leaf> blocks;
+    for (size_t l = 0; l < P0.leaves.size(); ++l) {
+      const gft::Leaf& lf = P0.leaves[l];
+      gft::Leaf b;
+      std::vector<std::vector<double>> rows;
+      std::vector<int> slots;
+      if (lf.right < 0) {
+        b.pos = lf.pos;
+        for (int r = 0; r < lf.k; ++r) {
+          rows.emplace_back(lf.M.begin() + (size_t)r * lf.k, lf.M.begin() + (size_t)(r + 1) * lf.k);
+          slots.push_back(lf.slot[r]);
+        }
+      } else {
+        if (lf.side == 1) continue;   // merged into its E leaf's block
+        const gft::RightStage& rs = P0.rights[lf.right];
+        const gft::Leaf& lF = P0.leaves[rs.leafF];
+        const int kE = lf.k, kF = lF.k;
+        b.pos = lf.pos;
+        b.pos.insert(b.pos.end(), lF.pos.begin(), lF.pos.end());
+        auto mrow = [](const gft::Leaf& x, int r) {
+          return std::vector<double>(x.M.begin() + (size_t)r * x.k, x.M.begin() + (size_t)(r + 1) * x.k);
+        };
+        for (size_t j = 0; j < rs.rE.size(); ++j) {
+          const std::vector<double> e = mrow(lf, rs.rE[j]), fr = mrow(lF, rs.rF[j]);
+          std::vector<double> a(kE + kF), q(kE + kF);
+          for (int c = 0; c < kE; ++c) { a[c] = e[c]; q[c] = rs.sign[j] * e[c]; }
+          for (int c = 0; c < kF; ++c) { a[kE + c] = fr[c]; q[kE + c] = -rs.sign[j] * fr[c]; }
+          rows.push_back(a);
+          slots.push_back(lf.slot[rs.rE[j]]);
+          rows.push_back(q);
+          slots.push_back(lF.slot[rs.rF[j]]);
+        }
+        for (int side = 0; side < 2; ++side) {
+          const gft::Leaf& x = side == 0 ? lf : lF;
+          for (int r = 0; r < x.k; ++r) {
+            if (x.pair[r] >= 0) continue;
+            std::vector<double> a(kE + kF, 0.0);
+            const std::vector<double> m = mrow(x, r);
+            for (int c = 0; c < x.k; ++c) a[(side == 0 ? 0 : kE) + c] = m[c];
+            rows.push_back(a);
+            slots.push_back(x.slot[r]);
+          }
         }
       }
-      lf.M.swap(F);
+      const int k = (int)b.pos.size();
+      b.k = k;
+      b.level = lf.level;
+      b.slot = slots;   // unused by the filter kernel (reads and writes positions)
+      b.M.assign((size_t)k * k, 0.0);
+      for (size_t r = 0; r < rows.size(); ++r) {
+        const double hr = h[slots[r]];
+        if (hr == 0.0) continue;
+        for (int c = 0; c < k; ++c) {
+          const double a = rows[r][c] * hr;
+          for (int c2 = 0; c2 < k; ++c2) b.M[(size_t)c * k + c2] += a * rows[r][c2];
+        }
+      }
+      blocks.push_back(std::move(b));
     }
+    f->P.leaves.swap(blocks);
+    f->P.rights.clear();
+    f->P.post.clear();
     for (int dt = 0; dt < 2; ++dt) {
       if (!(dtypes & (1u << dt))) continue;
       f->k[dt].reset(new gft::Kernel);
@@ -288,7 +343,7 @@ gft_status gft_plan_info_get(gft_plan plan, gft_plan_info* info) {
     info->n_scale_fix = P.n_fix;
     info->n_vz_total = P.n_vz_total;
     info->sum_k2 = P.sum_k2;
-    info->adds = 2 * (int64_t)P.n_units + P.sum_kk1;
+    info->adds = 2 * (int64_t)P.n_units + P.sum_kk1 + 2 * (int64_t)P.n_post;
     info->mults = P.sum_k2 + P.n_fix;
     info->paper_mults = P.sum_k2 + P.n_vz_total;
     info->dense_adds = (int64_t)P.n * (P.n - 1);
@@ -304,6 +359,8 @@ gft_status gft_plan_info_get(gft_plan plan, gft_plan_info* info) {
     info->kernels_ready = (int32_t)ready;
     info->residual = P.residual;
     info->orth_error = P.orth_error;
+    info->n_right_stages = (int32_t)P.rights.size();
+    info->n_right_pairs = P.n_post;
   });
 }
 

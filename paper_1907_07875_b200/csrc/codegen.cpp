@@ -151,9 +151,30 @@ void emit_leaf_fma(std::ostringstream& o, const Leaf& lf, size_t l, Dir d, int d
   }
 }
 
+// Right Haar stages on the coefficients, type T of the array:
+//   forward (after the leaves):  y_p <- a + b,  y_q <- s (a - b)
+//   inverse (before the leaves): x_p <- y_p + s y_q,  x_q <- y_p - s y_q   (transpose)
+void emit_post_units(std::ostringstream& o, const Plan& P, const char* arr, bool inverse, const char* T) {
+  if (P.post.empty()) return;
+  o << "  // ---- right Haar stage (" << P.post.size() << " coefficient pairs)\n  { " << T << " a_, b_;\n";
+  for (const PostUnit& u : P.post) {
+    o << "  a_ = " << arr << "[" << u.p << "]; b_ = " << arr << "[" << u.q << "]; ";
+    if (!inverse)
+      o << arr << "[" << u.p << "] = a_ + b_; " << arr << "[" << u.q << "] = "
+        << (u.s > 0 ? "a_ - b_" : "b_ - a_") << ";\n";
+    else
+      o << arr << "[" << u.p << "] = " << (u.s > 0 ? "a_ + b_" : "a_ - b_") << "; " << arr << "[" << u.q
+        << "] = " << (u.s > 0 ? "a_ - b_" : "a_ + b_") << ";\n";
+  }
+  o << "  (void)a_; (void)b_; }\n";
+}
+
 void emit_fast(std::ostringstream& o, const Plan& P, int dtype, Dir d) {
+  if (d == DIR_FILTER && !P.post.empty()) fail(GFT_ERR_COMPILE, "filter plan with right Haar stages");
   if (d != DIR_INV) emit_units_elem(o, P, "x", false, dtype);
+  if (d == DIR_INV) emit_post_units(o, P, "x", true, "elem_t");
   for (size_t l = 0; l < P.leaves.size(); ++l) emit_leaf_fma(o, P.leaves[l], l, d, dtype);
+  if (d == DIR_FWD) emit_post_units(o, P, "y", false, "elem_t");
   if (d != DIR_FWD) emit_units_elem(o, P, "y", true, dtype);
 }
 
@@ -317,6 +338,8 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, bool pair, 
          "    u32 tmem, u32 bsm, u32 mbar, u32 par, int tid) {\n";
   // ---- front: butterflies (forward) ----
   if (d != DIR_INV) emit_units(o, P, "x", false, dtype);
+  if (d == DIR_FILTER && !P.post.empty()) fail(GFT_ERR_COMPILE, "filter plan with right Haar stages");
+  if (d == DIR_INV) emit_post_units(o, P, "x", true, "float");
   std::ostringstream iss;   // body of gft_issue_pair (CTA-pair variant)
   for (size_t ti = 0; ti < T.size(); ++ti) {
     const TcLeaf& t = T[ti];
@@ -386,6 +409,7 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, bool pair, 
       o << "  }\n";
     }
   }
+  if (d == DIR_FWD) emit_post_units(o, P, "y", false, "float");
   // ---- back: reverse butterflies (inverse) ----
   if (d != DIR_FWD) emit_units(o, P, "y", true, dtype);
   o << "}\n";

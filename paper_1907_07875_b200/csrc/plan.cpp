@@ -270,6 +270,148 @@ struct Builder {
     P.leaves.push_back(std::move(lf));
   }
 
+  // Right Haar stage: needs a bipartite component whose Laplacian has a
+  // constant diagonal c; builds E (part S1) and F (part S2) from the component's
+  // eigenvectors paired by sigma = diag(+1 on S1, -1 on S2) (Lemma 1 / Theorem 1
+  // construction).  Returns false (caller emits a dense leaf) if any check fails.
+  bool try_right(const SubGraph& g, const std::vector<int>& pos, int depth) {
+    const int k = g.k;
+    if (k < 2) return false;
+    const std::vector<double> L = g.laplacian();
+    double lmax = 0;
+    for (double v : L) lmax = std::max(lmax, std::fabs(v));
+    const double tol = 1e-9 * std::max(1.0, lmax);
+    const double c = L[0];
+    for (int i = 0; i < k; ++i)
+      if (std::fabs(L[(size_t)i * k + i] - c) > tol) return false;
+    // 2-colouring over the edges (the component is connected)
+    std::vector<int> col(k, -1);
+    col[0] = 0;
+    std::vector<int> q{0};
+    for (size_t h = 0; h < q.size(); ++h) {
+      const int u = q[h];
+      for (int v = 0; v < k; ++v) {
+        if (v == u || g.w(u, v) == 0.0) continue;
+        if (col[v] < 0) { col[v] = 1 - col[u]; q.push_back(v); }
+        else if (col[v] == col[u]) return false;   // odd cycle: not bipartite
+      }
+    }
+    std::vector<int> S1, S2;
+    for (int i = 0; i < k; ++i) (col[i] == 0 ? S1 : S2).push_back(i);
+    if (S2.empty()) return false;
+    std::vector<double> lam, V;
+    jacobi_eigh(k, L, lam, V);
+    auto comp = [&](int j, const std::vector<int>& S, double scale) {
+      std::vector<double> e(S.size());
+      for (size_t a = 0; a < S.size(); ++a) e[a] = scale * V[(size_t)S[a] * k + j];
+      return e;
+    };
+    std::vector<std::vector<double>> Ecol, Fcol;
+    std::vector<double> lamE, lamF;
+    std::vector<int> pairE, pairF;
+    // clusters of (nearly) equal eigenvalues
+    std::vector<std::pair<int, int>> cl;   // [begin, end)
+    for (int j = 0; j < k;) {
+      int e = j + 1;
+      while (e < k && lam[e] - lam[e - 1] <= tol) ++e;
+      cl.push_back({j, e});
+      j = e;
+    }
+    const double s2 = std::sqrt(2.0);
+    std::vector<char> used(cl.size(), 0);
+    for (size_t a = 0; a < cl.size(); ++a) {
+      const int b0 = cl[a].first, b1 = cl[a].second;
+      const double la = lam[b0];
+      if (la < c - tol) {
+        // partner cluster at 2c - lambda with the same multiplicity
+        size_t bpart = cl.size();
+        for (size_t b = 0; b < cl.size(); ++b)
+          if (!used[b] && std::fabs(lam[cl[b].first] - (2 * c - la)) <= 10 * tol &&
+              cl[b].second - cl[b].first == b1 - b0)
+            bpart = b;
+        if (bpart == cl.size()) return false;
+        used[a] = used[bpart] = 1;
+        for (int j = b0; j < b1; ++j) {
+          pairE.push_back((int)Ecol.size());
+          pairF.push_back((int)Fcol.size());
+          Ecol.push_back(comp(j, S1, s2));
+          Fcol.push_back(comp(j, S2, s2));
+          lamE.push_back(lam[j]);
+          lamF.push_back(lam[cl[bpart].first + (j - b0)]);
+        }
+      } else if (std::fabs(la - c) <= tol) {
+        // sigma-invariant eigenspace: split into S1-supported and S2-supported halves
+        used[a] = 1;
+        for (int part = 0; part < 2; ++part) {
+          const std::vector<int>& S = part == 0 ? S1 : S2;
+          std::vector<std::vector<double>> basis;
+          for (int j = b0; j < b1; ++j) {
+            std::vector<double> v = comp(j, S, 1.0);
+            for (const auto& u : basis) {   // Gram-Schmidt (twice for stability)
+              for (int rep = 0; rep < 2; ++rep) {
+                double d = 0;
+                for (size_t t = 0; t < v.size(); ++t) d += v[t] * u[t];
+                for (size_t t = 0; t < v.size(); ++t) v[t] -= d * u[t];
+              }
+            }
+            double nv = 0;
+            for (double x : v) nv += x * x;
+            nv = std::sqrt(nv);
+            if (nv > 1e-6) {
+              for (double& x : v) x /= nv;
+              basis.push_back(v);
+            }
+          }
+          for (auto& v : basis) {
+            if (part == 0) { Ecol.push_back(v); lamE.push_back(la); }
+            else { Fcol.push_back(v); lamF.push_back(la); }
+          }
+        }
+      }
+    }
+    for (size_t a = 0; a < cl.size(); ++a)
+      if (!used[a]) return false;
+    if (Ecol.size() != S1.size() || Fcol.size() != S2.size()) return false;
+    auto orth_ok = [](const std::vector<std::vector<double>>& C) {
+      for (size_t a = 0; a < C.size(); ++a)
+        for (size_t b = a; b < C.size(); ++b) {
+          double d = 0;
+          for (size_t t = 0; t < C[a].size(); ++t) d += C[a][t] * C[b][t];
+          if (std::fabs(d - (a == b ? 1.0 : 0.0)) > 1e-9) return false;
+        }
+      return true;
+    };
+    if (!orth_ok(Ecol) || !orth_ok(Fcol)) return false;
+    // emit the two leaves and the stage
+    const int ri = (int)P.rights.size();
+    RightStage rs;
+    for (int side = 0; side < 2; ++side) {
+      const std::vector<int>& S = side == 0 ? S1 : S2;
+      const auto& C = side == 0 ? Ecol : Fcol;
+      Leaf lf;
+      lf.k = (int)S.size();
+      for (int i : S) lf.pos.push_back(pos[i]);
+      lf.level = depth;
+      lf.lam = side == 0 ? lamE : lamF;
+      lf.V.assign((size_t)lf.k * lf.k, 0.0);
+      for (int r = 0; r < lf.k; ++r)
+        for (int cc = 0; cc < lf.k; ++cc) lf.V[(size_t)cc * lf.k + r] = C[r][cc];
+      lf.right = ri;
+      lf.side = side;
+      lf.pair.assign(lf.k, -1);
+      const auto& pl = side == 0 ? pairE : pairF;
+      for (size_t j = 0; j < pl.size(); ++j) lf.pair[pl[j]] = (int)j;
+      (side == 0 ? rs.leafE : rs.leafF) = (int)P.leaves.size();
+      P.leaves.push_back(std::move(lf));
+    }
+    rs.rE = pairE;
+    rs.rF = pairF;
+    rs.sign.assign(pairE.size(), 1);
+    P.rights.push_back(rs);
+    P.n_post += (int)pairE.size();
+    return true;
+  }
+
   void emit_stage(const SubGraph& g, const std::vector<int>& pos, int depth,
                   const std::vector<int>& phi) {
     int p = 0, nz = 0;
@@ -331,7 +473,7 @@ struct Builder {
     }
     SearchResult r = find_involution(g, internal_rtol(), opt.search_budget);
     if (r.p == 0) {
-      emit_leaf(g, pos, depth);
+      if (!(opt.right_haar && try_right(g, pos, depth))) emit_leaf(g, pos, depth);
       return;
     }
     emit_stage(g, pos, depth, r.phi);
@@ -397,29 +539,69 @@ Plan build_plan(const SubGraph& g0, const int32_t* user_phi, const PlanOptions& 
   std::vector<Col> cols;
   std::vector<std::vector<double>> realised;   // per (leaf, r) in cols order
   const double r2 = 1.0 / kSqrt2;
+  auto apply_units_T = [&](std::vector<double>& u) {
+    for (auto it = P.ops.rbegin(); it != P.ops.rend(); ++it) {
+      if (it->kind != Op::UNIT) continue;
+      const double a = u[it->a], b = u[it->b];
+      u[it->a] = (a + b) * r2;
+      u[it->b] = (a - b) * r2;
+    }
+  };
+  // sign rule: first entry with |u_i| > 1e-8 positive (reading A-3)
+  auto first_sign = [&](const std::vector<double>& u) {
+    for (int i = 0; i < n; ++i)
+      if (std::fabs(u[i]) > 1e-8) return u[i] < 0 ? -1 : 1;
+    return 1;
+  };
+  auto negate_col = [](Leaf& lf, int r) {
+    for (int c = 0; c < lf.k; ++c) lf.V[(size_t)c * lf.k + r] = -lf.V[(size_t)c * lf.k + r];
+  };
   for (int l = 0; l < (int)P.leaves.size(); ++l) {
     Leaf& lf = P.leaves[l];
     P.max_leaf = std::max(P.max_leaf, lf.k);
     P.sum_k2 += (int64_t)lf.k * lf.k;
     P.sum_kk1 += (int64_t)lf.k * (lf.k - 1);
     for (int r = 0; r < lf.k; ++r) {
+      if (lf.right >= 0 && lf.pair[r] >= 0) {
+        // right Haar pair: u_A = (e; f)/sqrt2 (lambda), u_B = s (e; -f)/sqrt2
+        // (2c - lambda); realised together when the E leaf is visited
+        if (lf.side == 1) continue;
+        RightStage& rs = P.rights[lf.right];
+        const int j = lf.pair[r];
+        Leaf& lF = P.leaves[rs.leafF];
+        const int rf = rs.rF[j];
+        std::vector<double> uA(n, 0.0), uB(n, 0.0);
+        for (int c = 0; c < lf.k; ++c) uA[lf.pos[c]] = uB[lf.pos[c]] = lf.V[(size_t)c * lf.k + r] * r2;
+        for (int c = 0; c < lF.k; ++c) {
+          const double v = lF.V[(size_t)c * lF.k + rf] * r2;
+          uA[lF.pos[c]] = v;
+          uB[lF.pos[c]] = -v;
+        }
+        apply_units_T(uA);
+        apply_units_T(uB);
+        if (first_sign(uA) < 0) {   // flip (e, f) jointly: u_A -> -u_A, u_B -> -u_B
+          for (double& v : uA) v = -v;
+          for (double& v : uB) v = -v;
+          negate_col(lf, r);
+          negate_col(lF, rf);
+        }
+        rs.sign[j] = 1;
+        if (first_sign(uB) < 0) {
+          for (double& v : uB) v = -v;
+          rs.sign[j] = -1;
+        }
+        cols.push_back(Col{lf.lam[r], l, r});
+        realised.push_back(std::move(uA));
+        cols.push_back(Col{lF.lam[rf], rs.leafF, rf});
+        realised.push_back(std::move(uB));
+        continue;
+      }
       std::vector<double> u(n, 0.0);
       for (int c = 0; c < lf.k; ++c) u[lf.pos[c]] = lf.V[(size_t)c * lf.k + r];
-      for (auto it = P.ops.rbegin(); it != P.ops.rend(); ++it) {
-        if (it->kind != Op::UNIT) continue;
-        const double a = u[it->a], b = u[it->b];
-        u[it->a] = (a + b) * r2;
-        u[it->b] = (a - b) * r2;
-      }
-      // sign rule: first entry with |u_i| > 1e-8 positive (reading A-3)
-      for (int i = 0; i < n; ++i) {
-        if (std::fabs(u[i]) > 1e-8) {
-          if (u[i] < 0) {
-            for (double& v : u) v = -v;
-            for (int c = 0; c < lf.k; ++c) lf.V[(size_t)c * lf.k + r] = -lf.V[(size_t)c * lf.k + r];
-          }
-          break;
-        }
+      apply_units_T(u);
+      if (first_sign(u) < 0) {
+        for (double& v : u) v = -v;
+        negate_col(lf, r);
       }
       cols.push_back(Col{lf.lam[r], l, r});
       realised.push_back(std::move(u));
@@ -439,13 +621,21 @@ Plan build_plan(const SubGraph& g0, const int32_t* user_phi, const PlanOptions& 
     const auto& u = realised[order[rank]];
     for (int i = 0; i < n; ++i) P.U[(size_t)i * n + rank] = u[i];
   }
-  // ---- P7: fold 2^(-d/2) into the leaves: M[r][c] = v_r(c) * 2^(-d_pos(c)/2) ----
+  // right Haar post-units on the coefficient slots (forward order = stage order)
+  for (const RightStage& rs : P.rights)
+    for (size_t j = 0; j < rs.rE.size(); ++j)
+      P.post.push_back(PostUnit{P.leaves[rs.leafE].slot[rs.rE[j]], P.leaves[rs.leafF].slot[rs.rF[j]],
+                                rs.sign[j]});
+  // ---- P7: fold 2^(-d/2) into the leaves: M[r][c] = v_r(c) * 2^(-d_pos(c)/2), and the
+  // 1/sqrt2 of a right Haar pair into its rows (post-units are unnormalised (a+b, a-b)) ----
   for (auto& lf : P.leaves) {
     lf.M.assign((size_t)lf.k * lf.k, 0.0);
-    for (int r = 0; r < lf.k; ++r)
+    for (int r = 0; r < lf.k; ++r) {
+      const double pr = (lf.right >= 0 && lf.pair[r] >= 0) ? r2 : 1.0;
       for (int c = 0; c < lf.k; ++c)
         lf.M[(size_t)r * lf.k + c] =
-            lf.V[(size_t)c * lf.k + r] * std::pow(2.0, -0.5 * P.dexp[lf.pos[c]]);
+            lf.V[(size_t)c * lf.k + r] * std::pow(2.0, -0.5 * P.dexp[lf.pos[c]]) * pr;
+    }
   }
   // ---- self-check of the realised basis ----
   double lmax = 0;

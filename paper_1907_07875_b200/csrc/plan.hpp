@@ -60,6 +60,10 @@ struct Leaf {
   std::vector<double> V;       // eigenvectors, row-major V[c*k + r] = v_r(c), canonical sign
   std::vector<double> M;       // folded matrix, row-major M[r*k + c]
   int level = 0;               // depth at which the leaf was emitted
+  // right Haar stage membership: index into Plan::rights, side 0 = E (part S1), 1 = F (S2),
+  // pair[r] = pair index of output r or -1 (unpaired, passes through)
+  int right = -1, side = 0;
+  std::vector<int> pair;
 };
 
 struct PlanOptions {
@@ -68,12 +72,33 @@ struct PlanOptions {
   int64_t search_budget = 1000000;
   double sym_rtol = 1e-12;
   bool normalized = false;   // GFT of D^{-1/2} L D^{-1/2}
+  bool right_haar = true;    // right Haar stages on constant-diagonal bipartite components
+};
+
+// A right Haar stage (eq:right_gft / eq:right_pm, Theorems 1-2): on a
+// bipartite component whose Laplacian has a constant diagonal c (a k-regular bipartite
+// graph, or the normalised Laplacian of any bipartite graph), eigenvectors pair as
+// (mu1; mu2) <-> (mu1; -mu2) with eigenvalues lambda <-> 2c - lambda (Lemma 1), so
+//   U^T x = B diag(E^T, F^T) x:  a = E^T x_S1, b = F^T x_S2 (two dense leaves), then a
+// butterfly on coefficient pairs.  Unpaired eigenvectors (lambda = c) are supported on one
+// part only and pass through.
+struct PostUnit {
+  int p, q;   // coefficient slots: y_p <- a + b (eigenvalue lambda), y_q <- s (a - b) (2c - lambda)
+  int s;      // +1 / -1, chosen so that both realised columns have the canonical sign
+};
+
+struct RightStage {
+  int leafE = -1, leafF = -1;        // indices in Plan::leaves (E on part S1, F on part S2)
+  std::vector<int> rE, rF;           // paired local outputs
+  std::vector<int> sign;             // s per pair
 };
 
 struct Plan {
   int n = 0;
   std::vector<Op> ops;               // forward order
   std::vector<Leaf> leaves;          // emission order
+  std::vector<RightStage> rights;    // right Haar stages (pairs of leaves)
+  std::vector<PostUnit> post;        // forward: applied to the coefficients after the leaves
   std::vector<int> dexp;             // final Haar scale exponent per position
   std::vector<double> lambda;        // ascending, size n
   std::vector<double> U;             // realised basis row-major U[i*n+k]
@@ -81,7 +106,7 @@ struct Plan {
   // statistics
   int depth = 0;
   std::vector<int> units_per_level;
-  int n_units = 0, n_fix = 0, n_vz_total = 0, max_leaf = 0, n_clusters = 0;
+  int n_units = 0, n_fix = 0, n_vz_total = 0, max_leaf = 0, n_clusters = 0, n_post = 0;
   int64_t sum_k2 = 0, sum_kk1 = 0;
   double residual = 0, orth_error = 0;
 };

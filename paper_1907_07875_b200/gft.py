@@ -23,6 +23,7 @@ LIB_PATH = os.environ.get("GFT_LIB", os.path.join(_HERE, "_lib", "libgft.so"))
 GFT_F32, GFT_F64 = 0, 1
 GFT_FLAG_HOST_ONLY, GFT_FLAG_NO_CUBIN_CACHE, GFT_FLAG_NO_TENSOR_CORES, GFT_FLAG_NORMALIZED = 1, 2, 4, 8
 GFT_FLAG_DENSE_TC = 16
+GFT_FLAG_NO_RIGHT_HAAR = 32
 K_FAST_FWD, K_FAST_INV, K_DENSE_FWD, K_DENSE_INV = 0, 1, 2, 3
 GFT_MAX_LEVELS = 64
 
@@ -59,7 +60,8 @@ class gft_plan_info(ctypes.Structure):
                 ("max_leaf", c_int32), ("n_scale_fix", c_int32), ("n_vz_total", c_int32),
                 ("sum_k2", c_int64), ("adds", c_int64), ("mults", c_int64), ("paper_mults", c_int64),
                 ("dense_adds", c_int64), ("dense_mults", c_int64), ("n_clusters", c_int32),
-                ("kernels_ready", c_int32), ("residual", c_double), ("orth_error", c_double)]
+                ("kernels_ready", c_int32), ("residual", c_double), ("orth_error", c_double),
+                ("n_right_stages", c_int32), ("n_right_pairs", c_int32)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "units_per_level"}
@@ -388,7 +390,8 @@ class Plan:
 
     def __init__(self, n, src, dst, w, self_loops=None, phi=None, *, max_depth=-1, min_leaf=1,
                  search_budget=1000000, sym_rtol=1e-12, dtypes=("f32", "f64"), host_only=False,
-                 no_cubin_cache=False, no_tensor_cores=False, normalized=False, dense_tc=False):
+                 no_cubin_cache=False, no_tensor_cores=False, normalized=False, dense_tc=False,
+                 right_haar=True):
         o = gft_plan_opts_default()
         o.max_depth = max_depth
         o.min_leaf = min_leaf
@@ -399,7 +402,8 @@ class Plan:
             o.dtypes |= 1 << _dtype_code(d)
         o.flags = ((GFT_FLAG_HOST_ONLY if host_only else 0) | (GFT_FLAG_NO_CUBIN_CACHE if no_cubin_cache else 0)
                    | (GFT_FLAG_NO_TENSOR_CORES if no_tensor_cores else 0)
-                   | (GFT_FLAG_NORMALIZED if normalized else 0) | (GFT_FLAG_DENSE_TC if dense_tc else 0))
+                   | (GFT_FLAG_NORMALIZED if normalized else 0) | (GFT_FLAG_DENSE_TC if dense_tc else 0)
+                   | (0 if right_haar else GFT_FLAG_NO_RIGHT_HAAR))
         self.n = int(n)
         self._h = gft_plan_create(n, src, dst, w, self_loops, phi, o)
 

@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert sorted(G.EXPORTS) == syms
-    assert G.gft_abi_version() == 1
+    assert G.gft_abi_version() == 2
 
 
 def test_library_has_no_hard_cuda_dependency():

@@ -254,3 +254,57 @@ def random_symmetric_graph(rng: np.random.Generator, n: int, density: float = 0.
                 s[i] = v; s[phi[i]] = v
     src, dst, w = _edges(pairs, weights)
     return src, dst, w, s, phi
+
+
+def random_bipartite_graph(rng: np.random.Generator, n1: int, n2: int, density: float = 0.5,
+                           shuffle: bool = True):
+    """Random connected weighted bipartite graph on parts S1 (n1 nodes) and S2 (n2 nodes),
+    weights U(0.2, 2) (the input of the normalised-Laplacian right Haar stage).
+    A spanning tree across the parts keeps it connected for any n1, n2 >= 1.  Node labels are shuffled unless shuffle=False (S1 = 0..n1-1).
+    Returns (src, dst, w, self_loops, part) with part[i] in {0, 1}."""
+    n = n1 + n2
+    lab = rng.permutation(n) if shuffle else np.arange(n)
+    A, B = [int(v) for v in lab[:n1]], [int(v) for v in lab[n1:]]
+    edges = {}
+    # spanning tree: every node of B attaches to a node of A and vice versa
+    for j, b in enumerate(B):
+        edges[tuple(sorted((A[j % n1], b)))] = rng.uniform(0.2, 2.0)
+    for i, a in enumerate(A):
+        if i >= n2:
+            edges[tuple(sorted((a, B[int(rng.integers(n2))])))] = rng.uniform(0.2, 2.0)
+    for i in range(n1 - 1):   # link consecutive A nodes through a shared B node (connectivity)
+        b = B[int(rng.integers(n2))]
+        edges.setdefault(tuple(sorted((A[i], b))), rng.uniform(0.2, 2.0))
+        edges.setdefault(tuple(sorted((A[i + 1], b))), rng.uniform(0.2, 2.0))
+    for a in A:
+        for b in B:
+            if rng.random() < density:
+                edges.setdefault(tuple(sorted((a, b))), rng.uniform(0.2, 2.0))
+    pairs = sorted(edges)
+    src, dst, w = _edges(pairs, [edges[p] for p in pairs])
+    part = np.zeros(n, dtype=np.int32)
+    part[B] = 1
+    return src, dst, w, np.zeros(n), part
+
+
+def regular_bipartite_graph(rng: np.random.Generator, m: int, n_matchings: int = 3,
+                            loop: float = 0.0, shuffle: bool = True):
+    """Weighted k-regular bipartite graph (k-RBG) on 2m nodes: the union of
+    `n_matchings` random perfect matchings S1 -> S2, matching t with weight U(0.5, 1.5)
+    (coinciding edges add up), plus the same self-loop `loop` on every node, so every
+    weighted degree is the same.  Returns (src, dst, w, self_loops, part)."""
+    n = 2 * m
+    lab = rng.permutation(n) if shuffle else np.arange(n)
+    A, B = [int(v) for v in lab[:m]], [int(v) for v in lab[m:]]
+    edges = {}
+    for t in range(n_matchings):
+        wt = rng.uniform(0.5, 1.5)
+        perm = rng.permutation(m)
+        for i in range(m):
+            key = tuple(sorted((A[i], B[int(perm[i])])))
+            edges[key] = edges.get(key, 0.0) + wt
+    pairs = sorted(edges)
+    src, dst, w = _edges(pairs, [edges[p] for p in pairs])
+    part = np.zeros(n, dtype=np.int32)
+    part[B] = 1
+    return src, dst, w, np.full(n, float(loop)), part
