@@ -214,6 +214,40 @@ def config_table(args, stream, hbm, device):
     return rows
 
 
+def right_haar_table(args, stream, hbm, device):
+    """Right Haar stages: plans with / without them on bipartite graphs
+    whose Laplacian diagonal is constant, device-resident N(0,1), 2^20 signals."""
+    import torch
+    import workloads
+    from paper_1907_07875_b200 import gft
+    rows = []
+    for case in workloads.RIGHT_HAAR_BENCH_CASES:
+        label, dtype = case[0], case[4]
+        n, s, d, w, loops, norm = workloads.right_haar_bench_graph(case)
+        tdt = torch.float64 if dtype == "f64" else torch.float32
+        batch = 1 << 20
+        X = torch.randn(batch, n, generator=torch.Generator(device=device).manual_seed(5), device=device,
+                        dtype=tdt)
+        Y = torch.empty_like(X)
+        nbytes = 2 * batch * n * X.element_size()
+        row = {"graph": label, "dtype": dtype, "n": n, "batch": batch}
+        for tag, rh in (("right_haar", True), ("one_block", False)):
+            plan = gft.Plan(n, s, d, w, loops, dtypes=(dtype,), normalized=norm, right_haar=rh)
+            info = plan.info()
+            r = {"leaves": plan.leaf_sizes(), "pairs": info["n_right_pairs"], "mults": info["mults"],
+                 "adds": info["adds"], "kernel": plan.kernel_name(0, dtype)}
+            for k, f in ((0, plan.forward), (1, plan.inverse)):
+                ms = time_kernel(lambda: f(X, Y, stream), stream, 3, args.table_iters)
+                r[KIND_NAMES[k]] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
+                                    "frac": round(nbytes / ms / 1e6 / hbm, 4)}
+            row[tag] = r
+            plan.close()
+        row["right_vs_one_block_fwd"] = round(row["one_block"]["fast_fwd"]["ms"] / row["right_haar"]["fast_fwd"]["ms"], 3)
+        rows.append(row)
+        del X, Y
+    return rows
+
+
 def cpu_oracle_step_time(cfg, X_cpu, budget_s):
     """The oracle (as it stands) on the host: dense fp64 forward + inverse."""
     import oracle
@@ -397,8 +431,10 @@ def main():
     roundtrip_err = float(((Zh.double() - X_cpu.double()).norm(dim=1) / X_cpu.double().norm(dim=1)).max())
 
     table = None
+    rh_table = None
     if rank == 0 and not args.no_table:
         table = config_table(args, stream, hbm, device)
+        rh_table = right_haar_table(args, stream, hbm, device)
 
     cpu = None
     if rank == 0:
@@ -433,6 +469,7 @@ def main():
                         "fast_vs_dense": round((dense_fwd + dense_inv) / (fwd_ms + inv_ms), 3)},
             "clocks": clocks,
             "configs_table": table,
+            "right_haar_table": rh_table,
         }
         print(json.dumps(out))
     if dist:

@@ -108,6 +108,7 @@ def build_aot_cubins(jobs=8, verbose=True):
     """Generate the BASELINE configs' kernels via the library and nvcc-compile them."""
     sys.path.insert(0, ROOT)
     from paper_1907_07875_b200 import gft as G
+    import workloads
     os.makedirs(KDIR, exist_ok=True)
     import numpy as np
     todo = {}
@@ -129,6 +130,13 @@ def build_aot_cubins(jobs=8, verbose=True):
                                    dtypes=(dt,), dense_tc=True)
                     for kind in (2, 3):
                         todo.setdefault(dplan.kernel_name(kind, dt), dplan.kernel_source(kind, dt))
+    for case in workloads.RIGHT_HAAR_BENCH_CASES:
+        # right Haar plans (and their one-block ablation) timed by bench.py
+        n, s, d, w, loops, norm = workloads.right_haar_bench_graph(case)
+        for rh in (True, False):
+            plan = G.Plan(n, s, d, w, loops, dtypes=(case[4],), normalized=norm, right_haar=rh)
+            for kind in (0, 1):
+                todo.setdefault(plan.kernel_name(kind, case[4]), plan.kernel_source(kind, case[4]))
     nvcc = os.path.join(CUDA_HOME, "bin", "nvcc")
     pending = [(n, s) for n, s in todo.items() if not os.path.exists(os.path.join(KDIR, n + ".cubin"))]
     with tempfile.TemporaryDirectory() as td:

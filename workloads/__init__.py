@@ -20,6 +20,9 @@ Config readings:
   cfg5a cycle N=64, phi i<->63-i, 2^20 x N(0,1), seed 4
   cfg5b bipartite 64+64, orbit-drawn edges p=0.1, w~U[0.5,2],
         phi i<->127-i, 2^20 x N(0,1), seed 4                              (A-13)
+Beyond the configs (right Haar stages): random connected bipartite graphs
+(weights U(0.2, 2), used with the normalised Laplacian) and weighted k-regular bipartite
+graphs (unions of random perfect matchings), seeded by the caller.
 """
 from __future__ import annotations
 
@@ -29,7 +32,9 @@ from typing import Optional
 import numpy as np
 
 __all__ = ["Config", "CONFIGS", "config", "signals", "path_graph", "cycle_graph",
-           "grid_graph", "skeleton25_graph", "random_symmetric_graph", "precision_matrix"]
+           "grid_graph", "skeleton25_graph", "random_symmetric_graph", "precision_matrix",
+           "random_bipartite_graph", "regular_bipartite_graph", "RIGHT_HAAR_BENCH_CASES",
+           "right_haar_bench_graph"]
 
 
 @dataclasses.dataclass
@@ -308,3 +313,23 @@ def regular_bipartite_graph(rng: np.random.Generator, m: int, n_matchings: int =
     part = np.zeros(n, dtype=np.int32)
     part[B] = 1
     return src, dst, w, np.full(n, float(loop)), part
+
+
+# Bipartite graphs timed by bench.py's right-Haar table (and AOT-compiled by build.py):
+# (label, kind, |S1|, |S2|, dtype); kind "norm" = normalised Laplacian of a random bipartite
+# graph (Theorem 2), "reg" = unnormalised Laplacian of a weighted 3-RBG (Theorem 1).
+RIGHT_HAAR_BENCH_CASES = [("norm-bipartite 32|32", "norm", 32, 32, "f32"),
+                          ("norm-bipartite 64|64", "norm", 64, 64, "f32"),
+                          ("3-RBG 64|64", "reg", 64, 64, "f32"),
+                          ("norm-bipartite 12|20", "norm", 12, 20, "f64")]
+
+
+def right_haar_bench_graph(case):
+    """(n, src, dst, w, self_loops, normalized) of a RIGHT_HAAR_BENCH_CASES entry."""
+    _, kind, a, b, _ = case
+    rng = np.random.default_rng(a * 1000 + b)
+    if kind == "norm":
+        s, d, w, loops, _ = random_bipartite_graph(rng, a, b, density=0.3)
+    else:
+        s, d, w, loops, _ = regular_bipartite_graph(rng, a, 3, loop=0.0)
+    return a + b, s, d, w, loops, kind == "norm"
