@@ -290,3 +290,57 @@ def test_leaf_closed_forms_cycle64():
     lam = plan.eigenvalues()
     ref = np.sort(2 - 2 * np.cos(2 * np.pi * np.arange(64) / 64))
     assert np.abs(lam - ref).max() < 1e-12
+
+
+# --- graphs with 2-sparse eigenvectors (Lemma 4; NEXT-3) ---------------
+def _star(n):
+    return workloads._edges([(0, i) for i in range(1, n)])
+
+
+def _complete(n):
+    return workloads._edges([(i, j) for i in range(n) for j in range(i + 1, n)])
+
+
+def _clique_with_tail(m, tail):
+    """K_m on 0..m-1; nodes m-2, m-1 also chain to a path of `tail` nodes (so nodes 0..m-3
+    keep no outside neighbours: Lemma 4's clique example)."""
+    pairs = [(i, j) for i in range(m) for j in range(i + 1, m)]
+    pairs += [(m - 2, m), (m - 1, m)] + [(m + t, m + t + 1) for t in range(tail - 1)]
+    return workloads._edges(pairs)
+
+
+@pytest.mark.parametrize("kind,n", [("star", 9), ("star", 16), ("complete", 8), ("complete", 13),
+                                    ("clique", 7)])
+def test_two_sparse_eigenvector_graphs(kind, n):
+    """Closed forms pin the oracle (star: 0, 1^(n-2), n; complete: 0, n^(n-1)); Lemma 4's
+    2-sparse vectors e_i - e_j are eigenvectors; the plan finds Haar units and matches."""
+    if kind == "star":
+        s, d, w = _star(n)
+        nn = n
+        ref = np.array([0.0] + [1.0] * (n - 2) + [float(n)])
+    elif kind == "complete":
+        s, d, w = _complete(n)
+        nn = n
+        ref = np.array([0.0] + [float(n)] * (n - 1))
+    else:
+        s, d, w = _clique_with_tail(n, 4)
+        nn = n + 4
+        ref = None
+    L = oracle.laplacian(nn, s, d, w)
+    lam_o, U_o = oracle.gft_basis(L)
+    if ref is not None:
+        assert np.abs(lam_o - ref).max() < 1e-12
+    # Lemma 4: w_vi = w_vj for all other v  <=>  (e_i - e_j)/sqrt2 is an eigenvector
+    i, j = (1, 2) if kind != "clique" else (0, 1)
+    u = np.zeros(nn); u[i], u[j] = 2 ** -0.5, -2 ** -0.5
+    Lu = L @ u
+    mu = float(u @ Lu)
+    assert np.abs(Lu - mu * u).max() < 1e-12
+    plan = G.Plan(nn, s, d, w, host_only=True)
+    info = plan.info()
+    assert info["n_units"] >= 1 and info["units_per_level"][0] >= 1
+    check_basis_against_oracle(nn, s, d, w, None, plan)
+    # the 2-sparse eigenvector lies in the plan's eigenspace of mu
+    lam_f, U_f = plan.eigenvalues(), plan.basis()
+    C = np.where(np.abs(lam_f - mu) < 1e-9 * max(1, mu))[0]
+    assert np.linalg.norm(U_f[:, C] @ (U_f[:, C].T @ u) - u) < 1e-10
