@@ -309,3 +309,29 @@ def test_execute_host_end_to_end():
     ref = plan.forward(X.cuda())
     torch.cuda.synchronize()
     assert torch.equal(Y, ref.cpu())
+
+
+@pytest.mark.parametrize("kind,n,dtype", [("complete", 64, "f32"), ("complete", 64, "f64"),
+                                          ("star", 33, "f32"), ("star", 100, "f64")])
+def test_two_sparse_eigenvector_graphs_on_gpu(kind, n, dtype):
+    """Lemma 4 graphs: K_64 plans to a pure Haar network (63 units, all
+    leaves 1x1); the star keeps one small leaf.  Parity vs the oracle (degenerate spectra:
+    aligned per cluster)."""
+    if kind == "complete":
+        pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+    else:
+        pairs = [(0, i) for i in range(1, n)]
+    s = np.array([p[0] for p in pairs], np.int32)
+    d = np.array([p[1] for p in pairs], np.int32)
+    w = np.ones(len(pairs))
+    plan = G.Plan(n, s, d, w, dtypes=(dtype,))
+    if kind == "complete":
+        assert plan.info()["n_units"] == n - 1 and max(plan.leaf_sizes()) == 1
+    L = oracle.laplacian(n, s, d, w)
+    lam_o, U_o = oracle.gft_basis(L)
+    X = torch.randn(2053, n, generator=torch.Generator().manual_seed(n), dtype=TDT[dtype])
+    Y = plan.forward(X.cuda())
+    Xr = plan.inverse(Y)
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), TOL[dtype])
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL[dtype]
