@@ -333,3 +333,35 @@ def right_haar_bench_graph(case):
     else:
         s, d, w, loops, _ = regular_bipartite_graph(rng, a, 3, loop=0.0)
     return a + b, s, d, w, loops, kind == "norm"
+
+
+def bidiag_grid(N=8, a=0.5):
+    """Bi-diagonally symmetric 6-connected N x N grid G_b of Sec. VI (PAPER.md:679, 757, 763;
+    reading R-5): the 4-connected uniform grid (node = N r + c, w = 1) plus the diagonal edges
+    (r, c)-(r+1, c+1) with weight a.  Symmetric about both diagonals."""
+    pairs, wts = [], []
+    for r in range(N):
+        for c in range(N):
+            v = N * r + c
+            if c + 1 < N:
+                pairs.append((v, v + 1)); wts.append(1.0)
+            if r + 1 < N:
+                pairs.append((v, v + N)); wts.append(1.0)
+            if r + 1 < N and c + 1 < N:
+                pairs.append((v, v + N + 1)); wts.append(a)
+    return _edges(pairs, wts)
+
+
+def z_grid(N=8, w=2.0):
+    """z-shaped N x N grid G_z (reading R-5): horizontal edges
+    (r, c)-(r, c+1) with weight 1 and anti-diagonal edges (r, c)-(r+1, c-1) with weight w;
+    centrosymmetric under phi(i) = N^2 - 1 - i."""
+    pairs, wts = [], []
+    for r in range(N):
+        for c in range(N):
+            v = N * r + c
+            if c + 1 < N:
+                pairs.append((v, v + 1)); wts.append(1.0)
+            if r + 1 < N and c >= 1:
+                pairs.append((v, v + N - 1)); wts.append(w)
+    return _edges(pairs, wts)
