@@ -74,6 +74,16 @@ typedef struct {
                              weights carry rounding */
   uint32_t dtypes;        /* bitmask (1u<<GFT_F32)|(1u<<GFT_F64) of kernels to generate [both] */
   uint32_t flags;         /* GFT_FLAG_* below [0] */
+  int32_t approx_layers;  /* "Haar + approximate GFT": >= 0 replaces every
+                             leaf with >= approx_min_leaf nodes by at most this many layers of
+                             parallel Givens rotations from the truncated Jacobi algorithm
+                             (layer rule = DESIGN.md reading R-4) followed by a
+                             sorting permutation.  The plan is then an orthogonal APPROXIMATE
+                             GFT: gft_plan_basis() returns U_hat, gft_plan_eigenvalues() the
+                             sorted diag(U_hat^T L U_hat), columns keep the rotations' signs.
+                             With max_depth = 0 the whole graph is one approximate leaf (the
+                             "approximate GFT" of the comparison).  -1 = exact leaves [-1] */
+  int32_t approx_min_leaf;/* smallest leaf approximated [2] */
 } gft_plan_opts;
 
 #define GFT_FLAG_HOST_ONLY 1u      /* build the factorisation only; no kernel codegen (CPU use) */
@@ -101,8 +111,10 @@ typedef struct {
   int32_t n_scale_fix;                    /* explicit sqrt(2)^m multiplies (unequal partner scales) */
   int32_t n_vz_total;                     /* V_Z pass-through nodes summed over all decompositions */
   int64_t sum_k2;                         /* sum over leaves of k^2 (leaf multiplies) */
-  int64_t adds;                           /* 2*n_units + sum k(k-1) (adds incl. subtractions) */
-  int64_t mults;                          /* sum k^2 + n_scale_fix (sqrt2 folded into leaves) */
+  int64_t adds;                           /* 2*n_units + sum k(k-1) (adds incl. subtractions)
+                                             over exact leaves (+ right Haar / Givens terms) */
+  int64_t mults;                          /* sum k^2 + n_scale_fix (sqrt2 folded into leaves)
+                                             over exact leaves (+ Givens terms) */
   int64_t paper_mults;                    /* sum k^2 + n_vz_total: tab:runtime convention (A-23) */
   int64_t dense_adds;                     /* n(n-1) */
   int64_t dense_mults;                    /* n^2 */
@@ -113,6 +125,9 @@ typedef struct {
   int32_t n_right_stages;                 /* right Haar stages (bipartite leaves split E | F) */
   int32_t n_right_pairs;                  /* coefficient butterflies of those stages (2 adds
                                              each, counted in `adds`) */
+  int32_t n_approx_leaves;                /* leaves realised as Givens layers (approx_layers) */
+  int32_t n_givens;                       /* their rotations: 2 adds + 4 mults each, counted in
+                                             adds / mults (plus 1 mult per 2^(-d/2) pre-scale) */
 } gft_plan_info;
 
 /* ---- plan lifecycle -------------------------------------------------------------- */

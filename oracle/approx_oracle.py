@@ -13,7 +13,8 @@ What it computes (Sec. VI-B):
       each layer: repeatedly take the not-yet-used index pair (p, q) with the largest
       |a_pq| (ties within relative TIE_RTOL -> lexicographically smallest (p, q)), rotate
       with the classical Jacobi angle that annihilates a_pq, until no disjoint pair with
-      |a_pq| > ZERO_RTOL * max(1, max|L|) remains; an empty layer ends the iteration;
+      |a_pq| > ZERO_RTOL * max(1, max|L|) remains (a_pp, a_qq equal within TIE_RTOL take
+      the 45 degree rotation); an empty layer ends the iteration;
       Pi_{J+1} sorts the final diagonal ascending (stable).
     The approximate basis is U_hat = G_1 G_2 ... G_J Pi, approximate eigenvalues =
     diag(U_hat^T L U_hat).  Column signs are those the rotations produce (no sign rule: the
@@ -41,8 +42,13 @@ TIE_RTOL = 1e-12     # reading R-4: near-equal |a_pq| are ties
 ZERO_RTOL = 1e-14    # reading R-4: entries below this (relative) are not rotated
 
 
-def _rotation(app, aqq, apq):
-    """(c, s) of the classical Jacobi rotation annihilating a_pq (stable tan formula)."""
+def _rotation(app, aqq, apq, tie_rtol=TIE_RTOL):
+    """(c, s) of the classical Jacobi rotation annihilating a_pq (stable tan formula).
+    Diagonal entries equal within tie_rtol count as equal (tau = 0 -> the 45 degree
+    rotation, t = 1): the sign of a rounding-level tau would otherwise flip the rotation
+    direction (reading R-4)."""
+    if abs(aqq - app) <= tie_rtol * max(abs(app), abs(aqq), abs(apq)):
+        return 1.0 / math.sqrt(2.0), 1.0 / math.sqrt(2.0)
     tau = (aqq - app) / (2.0 * apq)
     if abs(tau) > 1e150:
         t = 1.0 / (2.0 * tau)

@@ -87,6 +87,8 @@ void gft_plan_opts_default(gft_plan_opts* o) {
   o->sym_rtol = 1e-12;
   o->dtypes = (1u << GFT_F32) | (1u << GFT_F64);
   o->flags = 0;
+  o->approx_layers = -1;
+  o->approx_min_leaf = 2;
 }
 
 gft_status gft_plan_create(gft_plan* out, int32_t n, int64_t n_edges, const int32_t* src,
@@ -108,6 +110,9 @@ gft_status gft_plan_create(gft_plan* out, int32_t n, int64_t n_edges, const int3
     po.sym_rtol = o.sym_rtol;
     po.normalized = (o.flags & GFT_FLAG_NORMALIZED) != 0;
     po.right_haar = (o.flags & GFT_FLAG_NO_RIGHT_HAAR) == 0;
+    if (o.approx_layers < -1) gft::fail(GFT_ERR_INVALID_ARG, "approx_layers must be >= -1");
+    po.approx_layers = o.approx_layers;
+    po.approx_min_leaf = o.approx_min_leaf;
     gft::SubGraph g = gft::graph_from_edges(n, n_edges, src, dst, w, self_loops);
     std::unique_ptr<gft_plan_s> p(new gft_plan_s);
     p->P = gft::build_plan(g, phi, po);
@@ -343,9 +348,9 @@ gft_status gft_plan_info_get(gft_plan plan, gft_plan_info* info) {
     info->n_scale_fix = P.n_fix;
     info->n_vz_total = P.n_vz_total;
     info->sum_k2 = P.sum_k2;
-    info->adds = 2 * (int64_t)P.n_units + P.sum_kk1 + 2 * (int64_t)P.n_post;
-    info->mults = P.sum_k2 + P.n_fix;
-    info->paper_mults = P.sum_k2 + P.n_vz_total;
+    info->adds = 2 * (int64_t)P.n_units + P.sum_kk1 + 2 * (int64_t)P.n_post + 2 * (int64_t)P.n_givens;
+    info->mults = P.sum_k2 + P.n_fix + 4 * (int64_t)P.n_givens + P.n_approx_scale;
+    info->paper_mults = P.sum_k2 + P.n_vz_total + 4 * (int64_t)P.n_givens + P.n_approx_scale;
     info->dense_adds = (int64_t)P.n * (P.n - 1);
     info->dense_mults = (int64_t)P.n * P.n;
     info->n_clusters = P.n_clusters;
@@ -361,6 +366,8 @@ gft_status gft_plan_info_get(gft_plan plan, gft_plan_info* info) {
     info->orth_error = P.orth_error;
     info->n_right_stages = (int32_t)P.rights.size();
     info->n_right_pairs = P.n_post;
+    info->n_approx_leaves = P.n_approx_leaves;
+    info->n_givens = P.n_givens;
   });
 }
 

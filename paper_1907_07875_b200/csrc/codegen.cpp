@@ -140,7 +140,48 @@ void emit_units_elem(std::ostringstream& o, const Plan& P, const char* arr, bool
   o << "  (void)a_; (void)b_; }\n";
 }
 
+// Approximate leaf (NEXT-4): U_hat_l = G_1...G_J Pi applied as register
+// rotations.  Forward: scale by 2^(-d/2), G_1^T ... G_J^T in place on x[pos], then
+// y[slot[r]] = x[pos[perm[r]]].  Inverse: the transpose in reverse order.
+void emit_leaf_givens(std::ostringstream& o, const Leaf& lf, size_t l, Dir d, int dtype) {
+  const std::string fma = dtype == GFT_F64 ? "__fma_rn" : "__fmaf_rn";
+  const std::string mul = dtype == GFT_F64 ? "__dmul_rn" : "__fmul_rn";
+  size_t nrot = 0;
+  for (const auto& layer : lf.layers) nrot += layer.size();
+  o << "  // ---- leaf " << l << " (k=" << lf.k << ", approximate: " << lf.layers.size() << " Givens layers, "
+    << nrot << " rotations)\n  { elem_t a_, b_;\n";
+  const char* arr = d == DIR_FWD ? "x" : "y";
+  auto X = [&](int c) { return std::string(arr) + "[" + std::to_string(lf.pos[c]) + "]"; };
+  auto scale = [&]() {
+    for (int c = 0; c < lf.k; ++c)
+      if (lf.scale[c] != 1.0) o << "  " << X(c) << " = " << mul << "(" << X(c) << ", " << lit(lf.scale[c], dtype) << ");\n";
+  };
+  auto rot = [&](const Givens& g, bool transpose) {
+    // G^T: (p, q) <- (c a - s b, s a + c b);  G: (p, q) <- (c a + s b, -s a + c b)
+    const double sg = transpose ? g.s : -g.s;
+    o << "  a_ = " << X(g.p) << "; b_ = " << X(g.q) << "; " << X(g.p) << " = " << fma << "(" << lit(g.c, dtype)
+      << ", a_, " << mul << "(" << lit(-sg, dtype) << ", b_)); " << X(g.q) << " = " << fma << "(" << lit(sg, dtype)
+      << ", a_, " << mul << "(" << lit(g.c, dtype) << ", b_));\n";
+  };
+  if (d == DIR_FWD) {
+    scale();
+    for (const auto& layer : lf.layers)
+      for (const Givens& g : layer) rot(g, true);
+    for (int r = 0; r < lf.k; ++r) o << "  y[" << lf.slot[r] << "] = " << X(lf.perm[r]) << ";\n";
+  } else {
+    for (int r = 0; r < lf.k; ++r) o << "  " << X(lf.perm[r]) << " = x[" << lf.slot[r] << "];\n";
+    for (auto it = lf.layers.rbegin(); it != lf.layers.rend(); ++it)
+      for (const Givens& g : *it) rot(g, false);
+    scale();
+  }
+  o << "  (void)a_; (void)b_; }\n";
+}
+
 void emit_leaf_fma(std::ostringstream& o, const Leaf& lf, size_t l, Dir d, int dtype) {
+  if (lf.approx && d != DIR_FILTER) {   // the fused filter keeps F = M^T diag(h) M dense
+    emit_leaf_givens(o, lf, l, d, dtype);
+    return;
+  }
   o << "  // ---- leaf " << l << " (k=" << lf.k << ")\n";
   std::vector<std::string> in(lf.k);
   for (int i = 0; i < lf.k; ++i) in[i] = xs("x", in_idx(lf, d, i));
@@ -219,7 +260,7 @@ bool plan_tc(const Plan& P, int dtype, int stages, bool pair, std::vector<TcLeaf
   if (dtype != GFT_F32 || P.n % 32 != 0 || P.n > 256) return false;
   std::vector<int> order;
   for (int l = 0; l < (int)P.leaves.size(); ++l)
-    if (P.leaves[l].k >= 32) order.push_back(l);
+    if (P.leaves[l].k >= 32 && !P.leaves[l].approx) order.push_back(l);
   std::stable_sort(order.begin(), order.end(),
                    [&](int a, int b) { return P.leaves[a].k > P.leaves[b].k; });
   const int tile = 128 * P.n * 4;
@@ -456,7 +497,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
     // CTA pair first (3 tile buffers if they fit, else 2), then the single-CTA variant;
     // every big leaf must land on the tensor core for the pair variant to be chosen
     int nbig = 0;
-    for (const auto& lf : P.leaves) nbig += lf.k >= 32;
+    for (const auto& lf : P.leaves) nbig += lf.k >= 32 && !lf.approx;
     for (int st = 3; st >= 2 && !ok; --st)
       if (plan_tc(P, dtype, st, true, T, tmem_cols, b_bytes) && (int)T.size() == nbig &&
           getenv("GFT_NO_CTA_PAIR") == nullptr) {

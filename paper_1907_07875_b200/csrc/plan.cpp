@@ -266,7 +266,13 @@ struct Builder {
     lf.k = g.k;
     lf.pos = pos;
     lf.level = depth;
-    jacobi_eigh(g.k, g.laplacian(), lf.lam, lf.V);
+    if (opt.approx_layers >= 0 && g.k >= std::max(2, opt.approx_min_leaf)) {
+      // Haar + approximate GFT: the sub-GFT becomes J Givens layers
+      lf.approx = true;
+      truncated_jacobi(g.k, g.laplacian(), opt.approx_layers, lf.layers, lf.perm, lf.lam, lf.V);
+    } else {
+      jacobi_eigh(g.k, g.laplacian(), lf.lam, lf.V);
+    }
     P.leaves.push_back(std::move(lf));
   }
 
@@ -559,8 +565,14 @@ Plan build_plan(const SubGraph& g0, const int32_t* user_phi, const PlanOptions& 
   for (int l = 0; l < (int)P.leaves.size(); ++l) {
     Leaf& lf = P.leaves[l];
     P.max_leaf = std::max(P.max_leaf, lf.k);
-    P.sum_k2 += (int64_t)lf.k * lf.k;
-    P.sum_kk1 += (int64_t)lf.k * (lf.k - 1);
+    if (lf.approx) {
+      ++P.n_approx_leaves;
+      for (const auto& layer : lf.layers) P.n_givens += (int)layer.size();
+      for (int c = 0; c < lf.k; ++c) P.n_approx_scale += P.dexp[lf.pos[c]] != 0;
+    } else {
+      P.sum_k2 += (int64_t)lf.k * lf.k;
+      P.sum_kk1 += (int64_t)lf.k * (lf.k - 1);
+    }
     for (int r = 0; r < lf.k; ++r) {
       if (lf.right >= 0 && lf.pair[r] >= 0) {
         // right Haar pair: u_A = (e; f)/sqrt2 (lambda), u_B = s (e; -f)/sqrt2
@@ -599,7 +611,9 @@ Plan build_plan(const SubGraph& g0, const int32_t* user_phi, const PlanOptions& 
       std::vector<double> u(n, 0.0);
       for (int c = 0; c < lf.k; ++c) u[lf.pos[c]] = lf.V[(size_t)c * lf.k + r];
       apply_units_T(u);
-      if (first_sign(u) < 0) {
+      // approximate columns keep the signs the rotations give (the paper's delta / epsilon
+      // take absolute values); the rotations themselves are the code
+      if (!lf.approx && first_sign(u) < 0) {
         for (double& v : u) v = -v;
         negate_col(lf, r);
       }
@@ -629,6 +643,10 @@ Plan build_plan(const SubGraph& g0, const int32_t* user_phi, const PlanOptions& 
   // ---- P7: fold 2^(-d/2) into the leaves: M[r][c] = v_r(c) * 2^(-d_pos(c)/2), and the
   // 1/sqrt2 of a right Haar pair into its rows (post-units are unnormalised (a+b, a-b)) ----
   for (auto& lf : P.leaves) {
+    if (lf.approx) {
+      lf.scale.resize(lf.k);
+      for (int c = 0; c < lf.k; ++c) lf.scale[c] = std::pow(2.0, -0.5 * P.dexp[lf.pos[c]]);
+    }
     lf.M.assign((size_t)lf.k * lf.k, 0.0);
     for (int r = 0; r < lf.k; ++r) {
       const double pr = (lf.right >= 0 && lf.pair[r] >= 0) ? r2 : 1.0;
@@ -655,7 +673,8 @@ Plan build_plan(const SubGraph& g0, const int32_t* user_phi, const PlanOptions& 
     }
   P.residual = res;
   P.orth_error = orth;
-  if (!(res <= 1e-8 * std::max(1.0, lmax)) || !(orth <= 1e-10))
+  // an approximate plan is orthogonal but not an eigenbasis: only orthogonality is checked
+  if ((P.n_approx_leaves == 0 && !(res <= 1e-8 * std::max(1.0, lmax))) || !(orth <= 1e-10))
     fail(GFT_ERR_EIG_NOCONVERGE, "realised basis failed self-check (residual " +
                                      std::to_string(res) + ", orthogonality " +
                                      std::to_string(orth) + ")");
@@ -742,6 +761,80 @@ void jacobi_eigh(int k, const std::vector<double>& A0, std::vector<double>& lam,
     for (int c = 0; c < k; ++c) Vs[(size_t)c * k + r] = V[(size_t)c * k + idx[r]];
   }
   V.swap(Vs);
+}
+
+// ---------------------------------------------------------------------------------
+// Parallel truncated Jacobi (approximate sub-GFTs; reading R-4)
+// ---------------------------------------------------------------------------------
+void truncated_jacobi(int k, const std::vector<double>& A0, int J, std::vector<std::vector<Givens>>& layers,
+                      std::vector<int>& perm, std::vector<double>& lam, std::vector<double>& V) {
+  std::vector<double> a(A0);
+  auto A = [&](int i, int j) -> double& { return a[(size_t)i * k + j]; };
+  std::vector<double> W((size_t)k * k, 0.0);   // accumulated G_1 G_2 ... (row-major)
+  for (int i = 0; i < k; ++i) W[(size_t)i * k + i] = 1.0;
+  double amax = 0;
+  for (double v : a) amax = std::max(amax, std::fabs(v));
+  const double zt = 1e-14 * std::max(1.0, amax);
+  layers.clear();
+  for (int layer = 0; layer < J; ++layer) {
+    std::vector<char> used(k, 0);
+    std::vector<Givens> rots;
+    for (;;) {
+      double m = -1;
+      for (int p = 0; p < k; ++p) {
+        if (used[p]) continue;
+        for (int q = p + 1; q < k; ++q)
+          if (!used[q]) m = std::max(m, std::fabs(A(p, q)));
+      }
+      if (!(m > zt)) break;
+      // lexicographically first pair within the relative tie band of the maximum
+      const double thr = m * (1.0 - 1e-12);
+      int bp = -1, bq = -1;
+      for (int p = 0; p < k && bp < 0; ++p) {
+        if (used[p]) continue;
+        for (int q = p + 1; q < k; ++q)
+          if (!used[q] && std::fabs(A(p, q)) >= thr) { bp = p; bq = q; break; }
+      }
+      const int p = bp, q = bq;
+      const double apq = A(p, q), app = A(p, p), aqq = A(q, q), tau = (aqq - app) / (2.0 * apq);
+      double t;
+      // numerically equal diagonals -> the 45 degree rotation (a rounding-level tau must
+      // not decide the rotation direction)
+      if (std::fabs(aqq - app) <= 1e-12 * std::max(std::fabs(app), std::max(std::fabs(aqq), std::fabs(apq)))) t = 1.0;
+      else if (std::fabs(tau) > 1e150) t = 1.0 / (2.0 * tau);
+      else t = (tau >= 0 ? 1.0 : -1.0) / (std::fabs(tau) + std::sqrt(1.0 + tau * tau));
+      const double c = 1.0 / std::sqrt(1.0 + t * t), s = t * c;
+      for (int r = 0; r < k; ++r) {              // columns p, q
+        const double xp = A(r, p), xq = A(r, q);
+        A(r, p) = c * xp - s * xq;
+        A(r, q) = s * xp + c * xq;
+      }
+      for (int r = 0; r < k; ++r) {              // rows p, q
+        const double xp = A(p, r), xq = A(q, r);
+        A(p, r) = c * xp - s * xq;
+        A(q, r) = s * xp + c * xq;
+      }
+      A(p, q) = A(q, p) = 0.0;
+      for (int r = 0; r < k; ++r) {
+        const double wp = W[(size_t)r * k + p], wq = W[(size_t)r * k + q];
+        W[(size_t)r * k + p] = c * wp - s * wq;
+        W[(size_t)r * k + q] = s * wp + c * wq;
+      }
+      used[p] = used[q] = 1;
+      rots.push_back(Givens{p, q, c, s});
+    }
+    if (rots.empty()) break;
+    layers.push_back(std::move(rots));
+  }
+  perm.resize(k);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return A(x, x) < A(y, y); });
+  lam.resize(k);
+  V.assign((size_t)k * k, 0.0);
+  for (int r = 0; r < k; ++r) {
+    lam[r] = A(perm[r], perm[r]);
+    for (int c = 0; c < k; ++c) V[(size_t)c * k + r] = W[(size_t)c * k + perm[r]];
+  }
 }
 
 }  // namespace gft

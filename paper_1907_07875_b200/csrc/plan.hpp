@@ -50,6 +50,13 @@ struct Op {
   int level;    // butterfly level (depth of the decomposition node)
 };
 
+// One Givens rotation of an approximate leaf (local indices p < q): G = I except
+// G[p][p] = G[q][q] = c, G[p][q] = s, G[q][p] = -s; the leaf's A <- G^T A G.
+struct Givens {
+  int p, q;
+  double c, s;
+};
+
 // A dense sub-GFT block.  Forward: y[slot[r]] = sum_c M[r*k + c] * x[pos[c]],
 // inverse: x[pos[c]] = sum_r M[r*k + c] * y[slot[r]]  (M = V^T diag(2^(-d/2))).
 struct Leaf {
@@ -64,6 +71,13 @@ struct Leaf {
   // pair[r] = pair index of output r or -1 (unpaired, passes through)
   int right = -1, side = 0;
   std::vector<int> pair;
+  // approximate leaf (NEXT-4): J layers of parallel Givens rotations from
+  // the truncated Jacobi algorithm, then output r = rotated local index perm[r]; V holds the
+  // realised U_hat_l = G_1...G_J Pi, lam the final (sorted) diagonal; scale[c] = 2^(-d/2)
+  bool approx = false;
+  std::vector<std::vector<Givens>> layers;
+  std::vector<int> perm;
+  std::vector<double> scale;
 };
 
 struct PlanOptions {
@@ -73,6 +87,8 @@ struct PlanOptions {
   double sym_rtol = 1e-12;
   bool normalized = false;   // GFT of D^{-1/2} L D^{-1/2}
   bool right_haar = true;    // right Haar stages on constant-diagonal bipartite components
+  int approx_layers = -1;    // >= 0: leaves with k >= approx_min_leaf become J Givens layers
+  int approx_min_leaf = 2;
 };
 
 // A right Haar stage (eq:right_gft / eq:right_pm, Theorems 1-2): on a
@@ -107,6 +123,7 @@ struct Plan {
   int depth = 0;
   std::vector<int> units_per_level;
   int n_units = 0, n_fix = 0, n_vz_total = 0, max_leaf = 0, n_clusters = 0, n_post = 0;
+  int n_givens = 0, n_approx_scale = 0, n_approx_leaves = 0;
   int64_t sum_k2 = 0, sum_kk1 = 0;
   double residual = 0, orth_error = 0;
 };
@@ -148,6 +165,14 @@ std::vector<std::vector<int>> components(const SubGraph& g);
 // Returns eigenvalues ascending and eigenvectors V[c*k + r] (column r).
 void jacobi_eigh(int k, const std::vector<double>& A, std::vector<double>& lam,
                  std::vector<double>& V);
+
+// Parallel truncated Jacobi (reading R-4 of DESIGN.md): up to J layers, each
+// greedily rotating disjoint pairs by decreasing |a_pq| (relative ties 1e-12 -> lexicographic
+// (p, q)) while |a_pq| > 1e-14 max(1, max|A|); an empty layer stops.  Returns the layers,
+// perm (ascending final diagonal, stable), lam = sorted diagonal and V[c*k + r] = column r of
+// U_hat = G_1...G_J Pi.
+void truncated_jacobi(int k, const std::vector<double>& A, int J, std::vector<std::vector<Givens>>& layers,
+                      std::vector<int>& perm, std::vector<double>& lam, std::vector<double>& V);
 
 Plan build_plan(const SubGraph& g, const int32_t* user_phi, const PlanOptions& opt);
 

@@ -51,7 +51,8 @@ class GFTError(RuntimeError):
 
 class gft_plan_opts(ctypes.Structure):
     _fields_ = [("max_depth", c_int32), ("min_leaf", c_int32), ("search_budget", c_int64),
-                ("sym_rtol", c_double), ("dtypes", c_uint32), ("flags", c_uint32)]
+                ("sym_rtol", c_double), ("dtypes", c_uint32), ("flags", c_uint32),
+                ("approx_layers", c_int32), ("approx_min_leaf", c_int32)]
 
 
 class gft_plan_info(ctypes.Structure):
@@ -61,7 +62,8 @@ class gft_plan_info(ctypes.Structure):
                 ("sum_k2", c_int64), ("adds", c_int64), ("mults", c_int64), ("paper_mults", c_int64),
                 ("dense_adds", c_int64), ("dense_mults", c_int64), ("n_clusters", c_int32),
                 ("kernels_ready", c_int32), ("residual", c_double), ("orth_error", c_double),
-                ("n_right_stages", c_int32), ("n_right_pairs", c_int32)]
+                ("n_right_stages", c_int32), ("n_right_pairs", c_int32),
+                ("n_approx_leaves", c_int32), ("n_givens", c_int32)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "units_per_level"}
@@ -391,8 +393,10 @@ class Plan:
     def __init__(self, n, src, dst, w, self_loops=None, phi=None, *, max_depth=-1, min_leaf=1,
                  search_budget=1000000, sym_rtol=1e-12, dtypes=("f32", "f64"), host_only=False,
                  no_cubin_cache=False, no_tensor_cores=False, normalized=False, dense_tc=False,
-                 right_haar=True):
+                 right_haar=True, approx_layers=-1, approx_min_leaf=2):
         o = gft_plan_opts_default()
+        o.approx_layers = approx_layers
+        o.approx_min_leaf = approx_min_leaf
         o.max_depth = max_depth
         o.min_leaf = min_leaf
         o.search_budget = search_budget
