@@ -248,6 +248,54 @@ def right_haar_table(args, stream, hbm, device):
     return rows
 
 
+def approx_table(args, stream, hbm, device):
+    """Sec. VI-B comparison on B200: matrix GFT, Haar + matrix (exact fast
+    GFT), approximate GFT (J Givens layers) and Haar + approximate, each with its kernel time
+    and the paper's error metrics delta / epsilon against the exact plan basis (M = 20000
+    U[0,1] signals).  fp32, 2^21 device-resident signals (> L2)."""
+    import torch
+    import workloads
+    from paper_1907_07875_b200 import gft
+    batch = 1 << 21
+    Xs = np.random.default_rng(0).uniform(0.0, 1.0, (20000, 64))
+    X = torch.rand(batch, 64, generator=torch.Generator(device=device).manual_seed(6), device=device)
+    Y = torch.empty_like(X)
+    nbytes = 2 * batch * 64 * 4
+    rows, exact = [], {}
+
+    def delta(Uh, U):
+        return float(np.linalg.norm(np.abs(Uh.T @ U) - np.eye(64)) / 8.0)
+
+    def eps(Uh, U):
+        dd = np.abs(Xs @ U) - np.abs(Xs @ Uh)
+        return float(np.sum(dd * dd) / Xs.shape[0])
+
+    for label, variant, kw in workloads.approx_bench_plans():
+        s, d, w = workloads.APPROX_BENCH_GRAPHS[label][0]()
+        kw = dict(kw)
+        phi = kw.pop("phi")
+        plan = gft.Plan(64, s, d, w, None, phi, dtypes=("f32",), **kw)
+        info = plan.info()
+        ms = time_kernel(lambda: plan.forward(X, Y, stream), stream, 3, args.table_iters)
+        row = {"graph": label, "variant": variant, "adds": info["adds"], "mults": info["mults"],
+               "givens": info["n_givens"], "fast_fwd": {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
+                                                        "frac": round(nbytes / ms / 1e6 / hbm, 4)}}
+        if variant == "haar":
+            exact[label] = plan.basis()
+            msd = time_kernel(lambda: plan.dense_forward(X, Y, stream), stream, 3, args.table_iters)
+            rows.append({"graph": label, "variant": "matrix", "adds": info["dense_adds"],
+                         "mults": info["dense_mults"], "delta": 0.0, "epsilon": 0.0,
+                         "fast_fwd": {"ms": round(msd, 5), "gbs": round(nbytes / msd / 1e6, 1),
+                                      "frac": round(nbytes / msd / 1e6 / hbm, 4)}})
+            row.update(delta=0.0, epsilon=0.0)
+        else:
+            Uh = plan.basis()
+            row.update(delta=round(delta(Uh, exact[label]), 5), epsilon=round(eps(Uh, exact[label]), 5))
+        rows.append(row)
+        plan.close()
+    return rows
+
+
 def cpu_oracle_step_time(cfg, X_cpu, budget_s):
     """The oracle (as it stands) on the host: dense fp64 forward + inverse."""
     import oracle
@@ -431,10 +479,11 @@ def main():
     roundtrip_err = float(((Zh.double() - X_cpu.double()).norm(dim=1) / X_cpu.double().norm(dim=1)).max())
 
     table = None
-    rh_table = None
+    rh_table = ap_table = None
     if rank == 0 and not args.no_table:
         table = config_table(args, stream, hbm, device)
         rh_table = right_haar_table(args, stream, hbm, device)
+        ap_table = approx_table(args, stream, hbm, device)
 
     cpu = None
     if rank == 0:
@@ -470,6 +519,7 @@ def main():
             "clocks": clocks,
             "configs_table": table,
             "right_haar_table": rh_table,
+            "approx_table": ap_table,
         }
         print(json.dumps(out))
     if dist:

@@ -137,6 +137,14 @@ def build_aot_cubins(jobs=8, verbose=True):
             plan = G.Plan(n, s, d, w, loops, dtypes=(case[4],), normalized=norm, right_haar=rh)
             for kind in (0, 1):
                 todo.setdefault(plan.kernel_name(kind, case[4]), plan.kernel_source(kind, case[4]))
+    for label, variant, kw in workloads.approx_bench_plans():
+        # Sec. VI-B comparison (exact / approximate / Haar + approximate) timed by bench.py
+        s, d, w = workloads.APPROX_BENCH_GRAPHS[label][0]()
+        kw = dict(kw)
+        phi = kw.pop("phi")
+        plan = G.Plan(64, s, d, w, None, phi, dtypes=("f32",), **kw)
+        for kind in ((0, 1, 2) if variant == "haar" else (0, 1)):
+            todo.setdefault(plan.kernel_name(kind, "f32"), plan.kernel_source(kind, "f32"))
     nvcc = os.path.join(CUDA_HOME, "bin", "nvcc")
     pending = [(n, s) for n, s in todo.items() if not os.path.exists(os.path.join(KDIR, n + ".cubin"))]
     with tempfile.TemporaryDirectory() as td:

@@ -365,3 +365,25 @@ def z_grid(N=8, w=2.0):
             if r + 1 < N and c >= 1:
                 pairs.append((v, v + N - 1)); wts.append(w)
     return _edges(pairs, wts)
+
+
+# Approximate-GFT comparison of Sec. VI-B (PAPER.md:780-809), timed by bench.py and
+# AOT-compiled by build.py: graph -> (builder, involution used for the Haar stages).
+APPROX_BENCH_GRAPHS = {
+    "G_b 8x8 bidiag 6-conn a=0.5": (bidiag_grid, np.array([8 * (i % 8) + i // 8 for i in range(64)], np.int32)),
+    "G_z 8x8 z-shaped w=2": (z_grid, np.array([63 - i for i in range(64)], np.int32)),
+}
+APPROX_BENCH_LAYERS = (5, 10, 20, 40)
+
+
+def approx_bench_plans():
+    """[(graph label, variant, plan kwargs)] of the Sec. VI-B comparison: "matrix" is the dense
+    kernel of the exact plan, "haar" the exact fast GFT, "approx J" max_depth 0 with J
+    layers, "haar+approx J" Haar stages with J-layer leaves."""
+    out = []
+    for label, (_, phi) in APPROX_BENCH_GRAPHS.items():
+        out.append((label, "haar", {"phi": phi}))
+        for J in APPROX_BENCH_LAYERS:
+            out.append((label, "approx %d" % J, {"phi": None, "max_depth": 0, "approx_layers": J}))
+            out.append((label, "haar+approx %d" % J, {"phi": phi, "approx_layers": J}))
+    return out
