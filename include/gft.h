@@ -126,8 +126,10 @@ typedef struct {
   int32_t n_right_pairs;                  /* coefficient butterflies of those stages (2 adds
                                              each, counted in `adds`) */
   int32_t n_approx_leaves;                /* leaves realised as Givens layers (approx_layers) */
-  int32_t n_givens;                       /* their rotations: 2 adds + 4 mults each, counted in
-                                             adds / mults (plus 1 mult per 2^(-d/2) pre-scale) */
+  int32_t n_givens;                       /* their rotations.  Counted as executed: 2 FFMA each
+                                             (scaled "fast Givens" form) = 2 adds + 2 mults, plus
+                                             one multiply per approximate-leaf output; the
+                                             paper convention (paper_mults) counts 4 mults */
 } gft_plan_info;
 
 /* ---- plan lifecycle -------------------------------------------------------------- */

@@ -349,8 +349,8 @@ gft_status gft_plan_info_get(gft_plan plan, gft_plan_info* info) {
     info->n_vz_total = P.n_vz_total;
     info->sum_k2 = P.sum_k2;
     info->adds = 2 * (int64_t)P.n_units + P.sum_kk1 + 2 * (int64_t)P.n_post + 2 * (int64_t)P.n_givens;
-    info->mults = P.sum_k2 + P.n_fix + 4 * (int64_t)P.n_givens + P.n_approx_scale;
-    info->paper_mults = P.sum_k2 + P.n_vz_total + 4 * (int64_t)P.n_givens + P.n_approx_scale;
+    info->mults = P.sum_k2 + P.n_fix + 2 * (int64_t)P.n_givens + P.n_approx_scale;
+    info->paper_mults = P.sum_k2 + P.n_vz_total + 4 * (int64_t)P.n_givens;
     info->dense_adds = (int64_t)P.n * (P.n - 1);
     info->dense_mults = (int64_t)P.n * P.n;
     info->n_clusters = P.n_clusters;

@@ -141,40 +141,54 @@ void emit_units_elem(std::ostringstream& o, const Plan& P, const char* arr, bool
 }
 
 // Approximate leaf (NEXT-4): U_hat_l = G_1...G_J Pi applied as register
-// rotations.  Forward: scale by 2^(-d/2), G_1^T ... G_J^T in place on x[pos], then
-// y[slot[r]] = x[pos[perm[r]]].  Inverse: the transpose in reverse order.
+// rotations in "scaled" (fast-Givens) form: each position carries a plan-time scale d_c with
+// value = d_c * register, so a rotation (c, s) on (p, q) is two FFMAs
+//   r_p <- r_p - (s d_q / (c d_p)) r_q,   r_q <- r_q + (s d_p / (c d_q)) r_p(old),
+//   d_p <- c d_p,  d_q <- c d_q
+// (|s/c| <= 1 for Jacobi angles).  The 2^(-d/2) Haar scale starts d (forward) or ends it
+// (inverse); one multiply per output applies d.  Forward: G_1^T ... G_J^T then
+// y[slot[r]] = x[pos[perm[r]]]; inverse: the transpose in reverse order.
 void emit_leaf_givens(std::ostringstream& o, const Leaf& lf, size_t l, Dir d, int dtype) {
   const std::string fma = dtype == GFT_F64 ? "__fma_rn" : "__fmaf_rn";
   const std::string mul = dtype == GFT_F64 ? "__dmul_rn" : "__fmul_rn";
   size_t nrot = 0;
   for (const auto& layer : lf.layers) nrot += layer.size();
   o << "  // ---- leaf " << l << " (k=" << lf.k << ", approximate: " << lf.layers.size() << " Givens layers, "
-    << nrot << " rotations)\n  { elem_t a_, b_;\n";
+    << nrot << " rotations, scaled form)\n  { elem_t a_;\n";
   const char* arr = d == DIR_FWD ? "x" : "y";
   auto X = [&](int c) { return std::string(arr) + "[" + std::to_string(lf.pos[c]) + "]"; };
-  auto scale = [&]() {
-    for (int c = 0; c < lf.k; ++c)
-      if (lf.scale[c] != 1.0) o << "  " << X(c) << " = " << mul << "(" << X(c) << ", " << lit(lf.scale[c], dtype) << ");\n";
-  };
+  std::vector<double> ds(lf.k, 1.0);
+  if (d == DIR_FWD) ds = lf.scale;
   auto rot = [&](const Givens& g, bool transpose) {
     // G^T: (p, q) <- (c a - s b, s a + c b);  G: (p, q) <- (c a + s b, -s a + c b)
     const double sg = transpose ? g.s : -g.s;
-    o << "  a_ = " << X(g.p) << "; b_ = " << X(g.q) << "; " << X(g.p) << " = " << fma << "(" << lit(g.c, dtype)
-      << ", a_, " << mul << "(" << lit(-sg, dtype) << ", b_)); " << X(g.q) << " = " << fma << "(" << lit(sg, dtype)
-      << ", a_, " << mul << "(" << lit(g.c, dtype) << ", b_));\n";
+    const double t1 = sg * ds[g.q] / (g.c * ds[g.p]), t2 = sg * ds[g.p] / (g.c * ds[g.q]);
+    o << "  a_ = " << X(g.p) << "; " << X(g.p) << " = " << fma << "(" << lit(-t1, dtype) << ", " << X(g.q) << ", a_); "
+      << X(g.q) << " = " << fma << "(" << lit(t2, dtype) << ", a_, " << X(g.q) << ");\n";
+    ds[g.p] *= g.c;
+    ds[g.q] *= g.c;
+    for (int c : {g.p, g.q})
+      if (ds[c] < 0x1p-30) {   // keep registers far from overflow (after ~60 layers)
+        o << "  " << X(c) << " = " << mul << "(" << X(c) << ", " << lit(ds[c], dtype) << ");\n";
+        ds[c] = 1.0;
+      }
+  };
+  auto apply = [&](int c, double f, const std::string& dst, const std::string& src) {
+    if (f == 1.0) o << "  " << dst << " = " << src << ";\n";
+    else o << "  " << dst << " = " << mul << "(" << src << ", " << lit(f, dtype) << ");\n";
   };
   if (d == DIR_FWD) {
-    scale();
     for (const auto& layer : lf.layers)
       for (const Givens& g : layer) rot(g, true);
-    for (int r = 0; r < lf.k; ++r) o << "  y[" << lf.slot[r] << "] = " << X(lf.perm[r]) << ";\n";
+    for (int r = 0; r < lf.k; ++r)
+      apply(lf.perm[r], ds[lf.perm[r]], "y[" + std::to_string(lf.slot[r]) + "]", X(lf.perm[r]));
   } else {
     for (int r = 0; r < lf.k; ++r) o << "  " << X(lf.perm[r]) << " = x[" << lf.slot[r] << "];\n";
     for (auto it = lf.layers.rbegin(); it != lf.layers.rend(); ++it)
       for (const Givens& g : *it) rot(g, false);
-    scale();
+    for (int c = 0; c < lf.k; ++c) apply(c, ds[c] * lf.scale[c], X(c), X(c));
   }
-  o << "  (void)a_; (void)b_; }\n";
+  o << "  (void)a_; }\n";
 }
 
 void emit_leaf_fma(std::ostringstream& o, const Leaf& lf, size_t l, Dir d, int dtype) {

@@ -568,7 +568,7 @@ Plan build_plan(const SubGraph& g0, const int32_t* user_phi, const PlanOptions& 
     if (lf.approx) {
       ++P.n_approx_leaves;
       for (const auto& layer : lf.layers) P.n_givens += (int)layer.size();
-      for (int c = 0; c < lf.k; ++c) P.n_approx_scale += P.dexp[lf.pos[c]] != 0;
+      P.n_approx_scale += lf.k;   // one output multiply per position (scaled rotations)
     } else {
       P.sum_k2 += (int64_t)lf.k * lf.k;
       P.sum_kk1 += (int64_t)lf.k * (lf.k - 1);

@@ -41,7 +41,8 @@ def test_pure_approximate_matches_oracle(name, J):
     assert info["n_approx_leaves"] == 1 and info["depth"] == 0
     nrot = sum(len(l) for l in layers)
     assert info["n_givens"] == nrot
-    assert info["adds"] == 2 * nrot and info["mults"] == 4 * nrot
+    assert info["adds"] == 2 * nrot and info["mults"] == 2 * nrot + 64
+    assert info["paper_mults"] == 4 * nrot
     assert np.abs(plan.eigenvalues() - lam_o).max() < 1e-12
     assert np.abs(plan.basis() - U_o).max() < 1e-12          # same signs: no sign rule
     assert info["orth_error"] < 1e-13
