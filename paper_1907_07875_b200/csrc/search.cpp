@@ -12,8 +12,20 @@
 // complete assignments the one with max p_phi wins (motivated by the p^2 + (n-p)^2
 // complexity), ties broken by the lexicographically smallest phi
 // (reading A-8).  A budget bounds the enumeration.
+//
+// Trees ("searching of identical tree branches"): when the budget runs
+// out on a component that is a tree, an O(n log n) canonical-label search takes over (the
+// report [lu2019search] with the paper's algorithm is not available; this is the standard
+// AHU rooted-tree labelling, weights and self-loops included).  Every involutive
+// automorphism fixes the tree's centre (or swaps a bicentre), so rooted at the centre a
+// max-p_phi involution swaps floor(m/2) pairs among each class of m identical child
+// branches and recurses only into the unpaired one -- swapping two identical branches of
+// size s pairs s nodes, more than any involution inside them.
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
+#include <functional>
+#include <map>
 #include <numeric>
 
 #include "plan.hpp"
@@ -96,6 +108,90 @@ struct Ctx {
   }
 };
 
+// Max-p involution of a tree component (see the header).  nodes = the component,
+// nbr = neighbour lists over |w| > tol.  Returns p and writes phi on the component.
+int tree_involution(const SubGraph& g, const std::vector<int>& nodes, const std::vector<std::vector<int>>& nbr,
+                    double tol, std::vector<int>& phi) {
+  const int k = g.k;
+  const double quantum = tol > 0 ? tol : 1e-300;
+  auto q = [quantum](double v) { return (int64_t)std::llround(v / quantum); };
+  // centre(s) by peeling leaves
+  std::vector<int> deg(k, 0), layer;
+  for (int v : nodes) {
+    deg[v] = (int)nbr[v].size();
+    if (deg[v] <= 1) layer.push_back(v);
+  }
+  int remaining = (int)nodes.size();
+  std::vector<char> gone(k, 0);
+  while (remaining > 2) {
+    std::vector<int> next;
+    for (int v : layer) {
+      gone[v] = 1;
+      --remaining;
+      for (int u : nbr[v])
+        if (!gone[u] && --deg[u] == 1) next.push_back(u);
+    }
+    layer.swap(next);
+  }
+  std::vector<int> centres;
+  for (int v : nodes) if (!gone[v]) centres.push_back(v);
+  // canonical labels of rooted subtrees (parent excluded)
+  std::map<std::vector<int64_t>, int> ids;
+  std::vector<int> label(k, -1);
+  std::function<int(int, int)> lab = [&](int v, int parent) -> int {
+    std::vector<std::pair<int64_t, int>> ch;
+    for (int c : nbr[v])
+      if (c != parent) ch.push_back({q(g.w(v, c)), lab(c, v)});
+    std::sort(ch.begin(), ch.end());
+    std::vector<int64_t> key{q(g.s[v])};
+    for (auto& e : ch) { key.push_back(e.first); key.push_back(e.second); }
+    auto it = ids.emplace(key, (int)ids.size()).first;
+    return label[v] = it->second;
+  };
+  auto children = [&](int v, int parent) {
+    std::vector<int> ch;
+    for (int c : nbr[v]) if (c != parent) ch.push_back(c);
+    std::sort(ch.begin(), ch.end(), [&](int a, int b) {
+      const auto ka = std::make_pair(q(g.w(v, a)), label[a]), kb = std::make_pair(q(g.w(v, b)), label[b]);
+      return ka != kb ? ka < kb : a < b;
+    });
+    return ch;
+  };
+  int p = 0;
+  // map the isomorphic subtrees rooted at a (parent pa) and b (parent pb) onto each other
+  std::function<void(int, int, int, int)> iso = [&](int a, int pa, int b, int pb) {
+    phi[a] = b;
+    phi[b] = a;
+    ++p;
+    const auto ca = children(a, pa), cb = children(b, pb);
+    for (size_t t = 0; t < ca.size(); ++t) iso(ca[t], a, cb[t], b);
+  };
+  std::function<void(int, int)> build = [&](int v, int parent) {
+    phi[v] = v;
+    const auto ch = children(v, parent);
+    for (size_t a = 0; a < ch.size();) {
+      size_t b = a;
+      const auto key = std::make_pair(q(g.w(v, ch[a])), label[ch[a]]);
+      while (b < ch.size() && std::make_pair(q(g.w(v, ch[b])), label[ch[b]]) == key) ++b;
+      // class ch[a..b): the smallest-index branch stays (when m is odd), the rest pair up
+      size_t t = a;
+      if ((b - a) % 2 == 1) build(ch[t++], v);
+      for (; t + 1 < b; t += 2) iso(ch[t], v, ch[t + 1], v);
+      a = b;
+    }
+  };
+  if (centres.size() == 2) {
+    const int c1 = centres[0], c2 = centres[1];
+    if (lab(c1, c2) == lab(c2, c1)) {
+      iso(c1, c2, c2, c1);
+      return p;
+    }
+  }
+  lab(centres[0], -1);
+  build(centres[0], -1);
+  return p;
+}
+
 }  // namespace
 
 SearchResult find_involution(const SubGraph& g, double rtol, int64_t budget) {
@@ -162,6 +258,31 @@ SearchResult find_involution(const SubGraph& g, double rtol, int64_t budget) {
     ctx.best.resize(k);
     for (int v : ctx.nodes) ctx.best[v] = v;   // identity is always valid (p = 0)
     ctx.dfs(0, 0, (int)ctx.nodes.size());
+    if (!ctx.complete) {
+      // budget exhausted: on a tree, the identical-branch search gives a
+      // max-p involution in O(n log n); used if it beats the partial enumeration and passes
+      // Definition 2 on the component
+      size_t twice_edges = 0;
+      for (int v : ctx.nodes) twice_edges += nbr[v].size();
+      if (twice_edges == 2 * (ctx.nodes.size() - 1)) {
+        std::vector<int> tphi(k);
+        std::iota(tphi.begin(), tphi.end(), 0);
+        const int tp = tree_involution(g, ctx.nodes, nbr, tol, tphi);
+        bool ok = tp > ctx.best_p;
+        for (size_t a = 0; ok && a < ctx.nodes.size(); ++a) {
+          const int i = ctx.nodes[a];
+          ok = std::fabs(g.s[i] - g.s[tphi[i]]) <= tol && tphi[tphi[i]] == i;
+          for (size_t b = a + 1; ok && b < ctx.nodes.size(); ++b) {
+            const int j = ctx.nodes[b];
+            ok = std::fabs(g.w(i, j) - g.w(tphi[i], tphi[j])) <= tol;
+          }
+        }
+        if (ok) {
+          ctx.best_p = tp;
+          for (int v : ctx.nodes) ctx.best[v] = tphi[v];
+        }
+      }
+    }
     for (int v : ctx.nodes) res.phi[v] = ctx.best[v];
     res.p += ctx.best_p;
     res.steps += ctx.steps;

@@ -344,3 +344,51 @@ def test_two_sparse_eigenvector_graphs(kind, n):
     lam_f, U_f = plan.eigenvalues(), plan.basis()
     C = np.where(np.abs(lam_f - mu) < 1e-9 * max(1, mu))[0]
     assert np.linalg.norm(U_f[:, C] @ (U_f[:, C].T @ u) - u) < 1e-10
+
+
+# --- identical-branch tree search (NEXT-3) --------------------------------
+def _random_tree(rng, n, weights=False):
+    parent = [-1] + [int(rng.integers(0, i)) for i in range(1, n)]
+    pairs = [(p, i) for i, p in enumerate(parent) if p >= 0]
+    w = rng.choice([1.0, 2.0], len(pairs)) if weights else None
+    return workloads._edges(pairs, w)
+
+
+def test_tree_search_matches_brute_force_max_p():
+    """With the backtracking budget exhausted (budget = 1), trees fall back to the
+    identical-branch search; its p_phi must be the brute-force maximum and phi valid."""
+    rng = np.random.default_rng(12)
+    checked = 0
+    for trial in range(150):
+        n = int(rng.integers(3, 9))
+        s, d, w = _random_tree(rng, n, weights=bool(trial % 2))
+        loops = np.where(rng.random(n) < 0.2, 0.5, 0.0) if trial % 3 == 0 else None
+        L = oracle.laplacian(n, s, d, w, loops)
+        best_p = 0
+        for phi in _involutions(n):
+            P = np.zeros((n, n)); P[np.arange(n), phi] = 1
+            if np.abs(P @ L @ P.T - L).max() <= 1e-12:
+                best_p = max(best_p, int(np.sum(phi > np.arange(n))))
+        phi, p, complete = G.gft_find_involution(L, 1e-10, 1)
+        if best_p > 0:
+            assert not complete
+        assert p == best_p, (n, p, best_p)
+        assert np.all(phi[phi] == np.arange(n))
+        assert np.abs(L[np.ix_(phi, phi)] - L).max() <= 1e-12
+        checked += best_p > 0
+    assert checked > 50
+
+
+def test_tree_search_rescues_large_random_tree():
+    """A 300-node random tree: the budgeted backtracking finds nothing, the tree search
+    pairs every set of identical sibling branches; the plan is still the oracle's GFT."""
+    rng = np.random.default_rng(0)
+    s, d, w = _random_tree(rng, 300)
+    L = oracle.laplacian(300, s, d, w)
+    phi, p, complete = G.gft_find_involution(L, 1e-10, 10 ** 5)
+    assert p >= 40 and not complete
+    assert np.abs(L[np.ix_(phi, phi)] - L).max() <= 1e-12
+    s, d, w = _random_tree(rng, 90)
+    plan = G.Plan(90, s, d, w, host_only=True, search_budget=1000)
+    assert plan.info()["n_units"] > 0
+    check_basis_against_oracle(90, s, d, w, None, plan)
