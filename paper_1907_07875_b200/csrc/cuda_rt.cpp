@@ -5,6 +5,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -378,9 +379,10 @@ void unload_kernel(Kernel& k) {
 }
 
 namespace {
+constexpr int kMaxHostSlots = 4;
 struct HostStreams {
-  CUstream s[2];
-  CUevent start, done[2];
+  CUstream s[kMaxHostSlots];
+  CUevent start, done[kMaxHostSlots];
 };
 std::mutex g_hs_mu;
 std::map<CUcontext, HostStreams> g_hs;
@@ -390,9 +392,9 @@ HostStreams& host_streams(CUcontext ctx) {
   if (it != g_hs.end()) return it->second;
   Driver& d = need_driver();
   HostStreams h;
-  for (int i = 0; i < 2; ++i) ck(d.cuStreamCreate(&h.s[i], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+  for (int i = 0; i < kMaxHostSlots; ++i) ck(d.cuStreamCreate(&h.s[i], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
   ck(d.cuEventCreate(&h.start, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
-  for (int i = 0; i < 2; ++i) ck(d.cuEventCreate(&h.done[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+  for (int i = 0; i < kMaxHostSlots; ++i) ck(d.cuEventCreate(&h.done[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
   return g_hs.emplace(ctx, h).first->second;
 }
 }  // namespace
@@ -410,11 +412,12 @@ void execute_host(Kernel& k, const void* in_host, void* out_host, int64_t batch,
   Driver& d = need_driver();
   CUcontext ctx = current_ctx(stream);
   HostStreams& hs = host_streams(ctx);
+  const int slots = (int)std::min<size_t>(kMaxHostSlots, workspace_bytes / chunk_bytes);
   ck(d.cuEventRecord(hs.start, (CUstream)stream), "cuEventRecord");
-  for (int i = 0; i < 2; ++i) ck(d.cuStreamWaitEvent(hs.s[i], hs.start, 0), "cuStreamWaitEvent");
+  for (int i = 0; i < slots; ++i) ck(d.cuStreamWaitEvent(hs.s[i], hs.start, 0), "cuStreamWaitEvent");
   int64_t c = 0;
   for (int64_t off = 0; off < batch; off += chunk_rows, ++c) {
-    const int slot = (int)(c & 1);
+    const int slot = (int)(c % slots);
     const int64_t rows = std::min<int64_t>(chunk_rows, batch - off);
     CUstream s = hs.s[slot];
     unsigned char* buf = static_cast<unsigned char*>(workspace) + slot * chunk_bytes;
@@ -426,7 +429,7 @@ void execute_host(Kernel& k, const void* in_host, void* out_host, int64_t batch,
                            rows * row_bytes, s),
        "cuMemcpyDtoHAsync");
   }
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < slots; ++i) {
     ck(d.cuEventRecord(hs.done[i], hs.s[i]), "cuEventRecord");
     ck(d.cuStreamWaitEvent((CUstream)stream, hs.done[i], 0), "cuStreamWaitEvent");
   }
