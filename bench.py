@@ -296,6 +296,45 @@ def approx_table(args, stream, hbm, device):
     return rows
 
 
+def pcie_roof(device):
+    """Pinned-host copy bandwidth of this box (256 MiB): H2D, D2H, and each direction while
+    both run concurrently -- the roof of the e2e path (one H2D + one D2H per transform)."""
+    import torch
+    nb = 256 << 20
+    hs = torch.empty(nb, dtype=torch.uint8).pin_memory()
+    hd = torch.empty(nb, dtype=torch.uint8).pin_memory()
+    da = torch.empty(nb, dtype=torch.uint8, device=device)
+    db = torch.empty(nb, dtype=torch.uint8, device=device)
+    s1, s2 = torch.cuda.Stream(device), torch.cuda.Stream(device)
+
+    def timed(fn, iters=4):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(iters):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / iters
+
+    def both():
+        cur = torch.cuda.current_stream()
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            da.copy_(hs, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hd.copy_(db, non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+    out = {"h2d_gbs": round(nb / timed(lambda: da.copy_(hs, non_blocking=True)) / 1e6, 1),
+           "d2h_gbs": round(nb / timed(lambda: hd.copy_(db, non_blocking=True)) / 1e6, 1),
+           "bidir_each_gbs": round(nb / timed(both) / 1e6, 1)}
+    del hs, hd, da, db
+    return out
+
+
 def cpu_oracle_step_time(cfg, X_cpu, budget_s):
     """The oracle (as it stands) on the host: dense fp64 forward + inverse."""
     import oracle
@@ -477,6 +516,9 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(s_e.elapsed_time(e_e) / args.e2e_steps, device)
     roundtrip_err = float(((Zh.double() - X_cpu.double()).norm(dim=1) / X_cpu.double().norm(dim=1)).max())
+    pcie = pcie_roof(device)
+    pcie["achieved_each_dir_gbs"] = round(2 * B * n * esz / (e2e_ms * 1e6), 1)
+    pcie["frac_of_bidir"] = round(pcie["achieved_each_dir_gbs"] / pcie["bidir_each_gbs"], 4)
 
     table = None
     rh_table = ap_table = None
@@ -511,7 +553,8 @@ def main():
             "e2e": {"value": B * ws / (e2e_ms * 1e-3), "unit": "signals/s",
                     "h2d_bytes_per_step": 2 * B * n * esz, "d2h_bytes_per_step": 2 * B * n * esz,
                     "ms_per_step": e2e_ms, "roundtrip_max_rel_err": roundtrip_err,
-                    "path": "gft_execute_host (pinned host, 2 streams, 2^18-row chunks)"},
+                    "path": "gft_execute_host (pinned host, 2 streams, 2^18-row chunks)",
+                    "pcie": pcie},
             "gpu_launches": 2 * args.steps,
             "kernels": {"fast_fwd_ms": round(fwd_ms, 5), "fast_inv_ms": round(inv_ms, 5),
                         "dense_fwd_ms": round(dense_fwd, 5), "dense_inv_ms": round(dense_inv, 5),

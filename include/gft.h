@@ -92,7 +92,8 @@ typedef struct {
                                        (Theorem 3 holds for it);
                                        every degree d_i = l_ii must be > 0 */
 #define GFT_FLAG_DENSE_TC 16u       /* the dense comparison kernels (gft_dense_*) run the whole
-                                       basis as one tcgen05 3xTF32 leaf (fp32, n % 32 == 0)
+                                       basis as one tcgen05 3xTF32 leaf (fp32, n % 4 == 0,
+                                       n >= 32)
                                        instead of CUDA-core FMA: the strongest dense baseline */
 #define GFT_FLAG_NO_TENSOR_CORES 4u /* fp32 leaves >= 32 stay on CUDA-core FMA instead of
                                        tcgen05 3xTF32 micro-GEMMs (ablation / comparison) */

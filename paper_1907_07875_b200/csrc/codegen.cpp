@@ -271,13 +271,13 @@ float tf32_rna_host(float v) {
 bool plan_tc(const Plan& P, int dtype, int stages, bool pair, std::vector<TcLeaf>& out, int& tmem_cols,
              int& b_bytes) {
   out.clear();
-  if (dtype != GFT_F32 || P.n % 32 != 0 || P.n > 256) return false;
+  if (dtype != GFT_F32 || P.n % 4 != 0 || P.n > 256) return false;   // 16-byte rows for TMA
   std::vector<int> order;
   for (int l = 0; l < (int)P.leaves.size(); ++l)
     if (P.leaves[l].k >= 32 && !P.leaves[l].approx) order.push_back(l);
   std::stable_sort(order.begin(), order.end(),
                    [&](int a, int b) { return P.leaves[a].k > P.leaves[b].k; });
-  const int tile = 128 * P.n * 4;
+  const int tile = 128 * ((P.n + 31) / 32 * 32) * 4;   // padded to whole TMA boxes
   int cols = 0, bytes = 0;
   for (int l : order) {
     TcLeaf t;

@@ -25,11 +25,14 @@ typedef float elem_t;
 struct __align__(64) TmaDesc { u64 d[16]; };
 
 #define GFT_TILE_ROWS 128
-#define GFT_ROW_BYTES (GFT_N * 4)
+// tile rows are padded to whole 32-float (128 B) TMA boxes; TMA zero-fills the columns
+// beyond n on load and clips them on store, so any n % 4 == 0 works
+#define GFT_NP ((GFT_N + 31) / 32 * 32)
+#define GFT_ROW_BYTES (GFT_NP * 4)
 #define GFT_TILE_BYTES (GFT_TILE_ROWS * GFT_ROW_BYTES)
 #define GFT_BOXC 32
 #define GFT_BOX_BYTES (GFT_TILE_ROWS * 128)
-#define GFT_NBOX (GFT_N / GFT_BOXC)
+#define GFT_NBOX (GFT_NP / GFT_BOXC)
 
 static __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 static __device__ __forceinline__ void mbar_init(u32 bar, u32 count) {

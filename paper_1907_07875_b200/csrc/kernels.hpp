@@ -29,7 +29,8 @@ struct KernelCfg {
   int tc_b_bytes = 0;           // SMEM bytes of the B operands
   int tc_tmem_cols = 0;         // TMEM columns allocated
   int tile_rows() const { return tc ? 128 : 32 * R; }
-  int tile_bytes() const { return tile_rows() * n * elem; }
+  // tensor-core tiles pad each row to whole 32-float TMA boxes (kernel_tc*_skeleton.cuh)
+  int tile_bytes() const { return tile_rows() * (tc ? (n + 31) / 32 * 32 : n) * elem; }
   int threads() const { return tc ? (tc_pair ? 192 : 160) : warps * 32; }
   int tiles_per_cta() const { return tc ? 1 : warps; }   // tiles processed concurrently per CTA
   int smem_bytes() const {

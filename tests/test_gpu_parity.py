@@ -245,7 +245,8 @@ def _random_big_leaf_graph(rng, n, sym):
     return s, d, w, rng.uniform(0, 0.5, n), None
 
 
-@pytest.mark.parametrize("n,sym", [(32, False), (64, False), (96, True), (128, True), (160, True)])
+@pytest.mark.parametrize("n,sym", [(32, False), (64, False), (80, False), (96, True), (100, True),
+                                   (128, True), (160, True)])
 def test_tensor_core_leaves_general(n, sym):
     """tcgen05 3xTF32 leaves on random graphs (leaf sizes 32..80 incl. padded K/N), against
     the oracle and against the same plan forced onto CUDA-core FMA."""

@@ -51,7 +51,8 @@ def _check(Y_hat, X, lam_o, U_o, U_f, tol):
 
 CASES = [("norm", 16, 16, "f32"), ("norm", 16, 16, "f64"), ("norm", 13, 20, "f32"),
          ("norm", 5, 9, "f64"), ("reg", 24, 0, "f32"), ("reg", 24, 0, "f64"),
-         ("norm", 32, 32, "f32"), ("norm", 40, 56, "f32"), ("reg", 64, 0, "f32")]
+         ("norm", 32, 32, "f32"), ("norm", 40, 56, "f32"), ("reg", 64, 0, "f32"),
+         ("norm", 40, 40, "f32"), ("norm", 36, 48, "f32")]
 
 
 @pytest.mark.parametrize("kind,a,b,dtype", CASES)
