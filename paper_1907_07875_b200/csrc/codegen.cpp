@@ -30,7 +30,7 @@ static const char* kSkeletonTC2 =
 #include "skeleton_tc2_inc.h"
     ;
 
-KernelCfg choose_cfg(int n, int dtype) {
+KernelCfg choose_cfg(int n, int dtype, int64_t work) {
   KernelCfg c;
   c.n = n;
   c.elem = dtype == GFT_F64 ? 8 : 4;
@@ -57,7 +57,7 @@ KernelCfg choose_cfg(int n, int dtype) {
   c.warps = std::max(2, std::min(8, (128 * 1024) / (c.stages * c.tile_bytes())));
   // measured geometry for this (n, dtype) if the tuning table has one (tools/gpu_autotune.py)
   int tR, tS, tW;
-  if (tuned_geometry(n, dtype, tR, tS, tW)) {
+  if (tuned_geometry(n, dtype, work, tR, tS, tW)) {
     c.R = tR;
     c.stages = tS;
     c.warps = tW;
@@ -501,7 +501,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
   }
   k.kind = kind;
   k.dtype = dtype;
-  k.cfg = choose_cfg(P.n, dtype);
+  k.cfg = choose_cfg(P.n, dtype, (kind == K_DENSE_FWD || kind == K_DENSE_INV) ? (int64_t)P.n * P.n : P.sum_k2);
   static const char* kKindNameTC[] = {"fwdtc", "invtc", "", "", "filttc"};
   const Dir dir = kind == K_FAST_INV ? DIR_INV : kind == K_FILTER ? DIR_FILTER : DIR_FWD;
   if (allow_tc && (kind == K_FAST_FWD || kind == K_FAST_INV || kind == K_FILTER)) {

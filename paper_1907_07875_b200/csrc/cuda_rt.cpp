@@ -245,8 +245,10 @@ constexpr int64_t kMaxRowsPerLaunch = (int64_t)1 << 30;
 
 }  // namespace
 
-bool tuned_geometry(int n, int dtype, int& R, int& S, int& W) {
-  struct Entry { int n, dt, R, S, W; };
+bool tuned_geometry(int n, int dtype, int64_t work, int& R, int& S, int& W) {
+  // lines: "fma <n> <f32|f64> <R> <S> <W> [work=<FMAs per signal>]"; an entry with a work key
+  // applies only to kernels with exactly that much leaf work (plan-specific measurement)
+  struct Entry { int n, dt, R, S, W; int64_t work; };
   static const std::vector<Entry> table = [] {
     std::vector<Entry> t;
     const char* e = getenv("GFT_TUNING_FILE");
@@ -256,20 +258,25 @@ bool tuned_geometry(int n, int dtype, int& R, int& S, int& W) {
     std::string line;
     while (std::getline(f, line)) {
       std::istringstream ss(line);
-      std::string mode, dt;
+      std::string mode, dt, extra;
       Entry x;
       if (!(ss >> mode >> x.n >> dt >> x.R >> x.S >> x.W) || mode != "fma") continue;
       x.dt = dt == "f64" ? GFT_F64 : GFT_F32;
+      x.work = -1;
+      if ((ss >> extra) && extra.rfind("work=", 0) == 0) x.work = std::atoll(extra.c_str() + 5);
       t.push_back(x);
     }
     return t;
   }();
+  const Entry* hit = nullptr;
   for (const Entry& x : table)
-    if (x.n == n && x.dt == dtype) {
-      R = x.R; S = x.S; W = x.W;
-      return true;
+    if (x.n == n && x.dt == dtype && (x.work == work || (x.work < 0 && !hit))) {
+      hit = &x;
+      if (x.work == work) break;
     }
-  return false;
+  if (!hit) return false;
+  R = hit->R; S = hit->S; W = hit->W;
+  return true;
 }
 
 std::string cubin_cache_dir() {

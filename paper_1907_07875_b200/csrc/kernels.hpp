@@ -40,7 +40,8 @@ struct KernelCfg {
   int swizzle_bytes() const { return swz_mask == 7 ? 128 : swz_mask == 3 ? 64 : swz_mask == 1 ? 32 : 0; }
 };
 
-KernelCfg choose_cfg(int n, int dtype);
+// work = FMAs per signal of the kernel body (selects plan-specific tuning entries)
+KernelCfg choose_cfg(int n, int dtype, int64_t work = -1);
 
 struct LoadedFn {
   void* module = nullptr;   // CUmodule
@@ -83,6 +84,6 @@ std::string cubin_cache_dir();
 // Measured geometry table (paper_1907_07875_b200/tuning.tsv, written by
 // tools/gpu_autotune.py on a B200): lines "fma <n> <f32|f64> <R> <S> <W>".  Returns false
 // if (n, dtype) has no entry.  GFT_TUNING_FILE overrides the path ("none" disables).
-bool tuned_geometry(int n, int dtype, int& R, int& S, int& W);
+bool tuned_geometry(int n, int dtype, int64_t work, int& R, int& S, int& W);
 
 }  // namespace gft
