@@ -12,6 +12,10 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CASES = [("cfg2", "f32"), ("cfg3", "f32"), ("cfg4", "f32"), ("cfg5a", "f32"), ("cfg4", "f64"), ("cfg1", "f32")]
+# per-plan sweep (--per-plan): (config, dtype, kind); entries keyed by the kernel's leaf work
+PLAN_CASES = [("cfg2", "f32", 0), ("cfg2b", "f32", 0), ("cfg3", "f32", 0), ("cfg4", "f64", 0),
+              ("cfg2", "f32", 2), ("cfg3", "f32", 2), ("cfg4", "f32", 2), ("cfg4", "f64", 2),
+              ("cfg5a", "f32", 2)]
 
 
 def measure(cfg, dt, R, S, W, kind=0):
@@ -23,6 +27,41 @@ def measure(cfg, dt, R, S, W, kind=0):
         if l.startswith("{"):
             return json.loads(l)
     return None
+
+
+def per_plan():
+    """Sweep per (config, kind, dtype); writes gpurun_out/tuning_plans.tsv with work= keys
+    (work = sum k^2 of the plan for fast kernels, n^2 for the dense kernels)."""
+    import workloads
+    from paper_1907_07875_b200 import gft
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    log = open(os.path.join(ROOT, "gpurun_out", "autotune_plans.log"), "w")
+    best = {}
+    for cfg, dt, kind in PLAN_CASES:
+        c = workloads.config(cfg)
+        plan = gft.Plan.from_config(c, dtypes=(dt,), host_only=True)
+        work = c.n * c.n if kind >= 2 else plan.info()["sum_k2"]
+        esz = 8 if dt == "f64" else 4
+        row = c.n * esz
+        for R, S, W in itertools.product((1, 2, 4, 8), (2, 3), (4, 8, 12, 16)):
+            tile = 32 * R * row
+            if tile < 2048 or tile > 32768 or W * S * tile > 220 * 1024:
+                continue
+            d = measure(cfg, dt, R, S, W, kind)
+            if d is None:
+                continue
+            rec = {"cfg": cfg, "dtype": dt, "kind": kind, "n": c.n, "work": work, "R": R, "S": S, "W": W,
+                   "b2b_ms": d["b2b_ms"], "gbs": d["b2b_gbs"]}
+            log.write(json.dumps(rec) + "\n")
+            log.flush()
+            key = (c.n, dt, work)
+            if key not in best or rec["gbs"] > best[key]["gbs"]:
+                best[key] = rec
+    with open(os.path.join(ROOT, "gpurun_out", "tuning_plans.tsv"), "w") as f:
+        for (n, dt, work), r in sorted(best.items()):
+            f.write("fma %d %s %d %d %d work=%d   # %.0f GB/s %s kind %d\n"
+                    % (n, dt, r["R"], r["S"], r["W"], work, r["gbs"], r["cfg"], r["kind"]))
+    print(open(os.path.join(ROOT, "gpurun_out", "tuning_plans.tsv")).read())
 
 
 def main():
@@ -67,4 +106,4 @@ def main():
 
 if __name__ == "__main__":
     sys.path.insert(0, ROOT)
-    main()
+    per_plan() if "--per-plan" in sys.argv else main()
