@@ -145,6 +145,10 @@ def build_aot_cubins(jobs=8, verbose=True):
         plan = G.Plan(64, s, d, w, None, phi, dtypes=("f32",), **kw)
         for kind in ((0, 1, 2) if variant == "haar" else (0, 1)):
             todo.setdefault(plan.kernel_name(kind, "f32"), plan.kernel_source(kind, "f32"))
+    s, d, w, loops, _ = workloads.smoke_bipartite32()   # __graft_entry__.smoke()'s tcgen05 case
+    plan = G.Plan(64, s, d, w, loops, dtypes=("f32",), normalized=True)
+    for kind in (0, 1):
+        todo.setdefault(plan.kernel_name(kind, "f32"), plan.kernel_source(kind, "f32"))
     nvcc = os.path.join(CUDA_HOME, "bin", "nvcc")
     pending = [(n, s) for n, s in todo.items() if not os.path.exists(os.path.join(KDIR, n + ".cubin"))]
     with tempfile.TemporaryDirectory() as td:

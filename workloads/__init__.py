@@ -387,3 +387,9 @@ def approx_bench_plans():
             out.append((label, "approx %d" % J, {"phi": None, "max_depth": 0, "approx_layers": J}))
             out.append((label, "haar+approx %d" % J, {"phi": phi, "approx_layers": J}))
     return out
+
+
+def smoke_bipartite32():
+    """The 32|32 bipartite graph of __graft_entry__.smoke() (normalised Laplacian -> a right
+    Haar stage with two 32-node tcgen05 leaves); AOT-compiled by build.py."""
+    return random_bipartite_graph(np.random.default_rng(7), 32, 32, density=0.3)
