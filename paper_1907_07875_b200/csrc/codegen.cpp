@@ -522,10 +522,32 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
       stages = 2;
       ok = plan_tc(P, dtype, stages, false, T, tmem_cols, b_bytes);
     }
+    // two compute warpgroups on the CTA pair for small n: the per-tile MMA chain of one
+    // warpgroup hides behind the other's staging.  320 threads leave 168 registers per
+    // thread, so only plans whose every leaf is on the tensor core (no FMA leaf registers)
+    // and n <= 80 qualify (measured: +4-5% at n = 64 with two 32-leaves, -6% with an FMA
+    // leaf beside them; tools/tc_vs_fma.py)
+    int wgs = 1, wg_cols = 0;
+    if (ok && pair && P.n <= 80 && T.size() == P.leaves.size() && getenv("GFT_NO_TC_2WG") == nullptr) {
+      for (const auto& t : T) wg_cols = std::max(wg_cols, t.d_col + ru(t.np, 32));
+      if (2 * wg_cols <= 512) {
+        std::vector<TcLeaf> T2;
+        int tc2 = 0, bb2 = 0;
+        for (int st = 6; st >= 4; --st)
+          if (plan_tc(P, dtype, st, true, T2, tc2, bb2) && T2.size() == T.size()) {
+            wgs = 2;
+            stages = st;
+            tmem_cols = 32;
+            while (tmem_cols < 2 * wg_cols) tmem_cols *= 2;
+            break;
+          }
+      }
+    }
     if (ok) {
       KernelCfg& c = k.cfg;
       c.tc = 1;
       c.tc_pair = pair ? 1 : 0;
+      c.tc_wgs = wgs;
       c.stages = stages;
       c.mode = 0;
       c.boxc = 32;
@@ -540,6 +562,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
       std::ostringstream pre;
       pre << "#define GFT_N " << c.n << "\n#define GFT_STAGES " << c.stages << "\n#define GFT_TMEM_COLS "
           << tmem_cols << "\n";
+      if (wgs == 2) pre << "#define GFT_WGS 2\n#define GFT_WG_COLS " << wg_cols << "\n";
       const std::string skel(pair ? kSkeletonTC2 : kSkeletonTC);
       const std::string marker = "// @@GFT_GENERATED@@";
       const size_t at = skel.find(marker);
@@ -547,7 +570,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
       const std::string key = pre.str() + gen.str() + skel;
       char hbuf[32];
       std::snprintf(hbuf, sizeof hbuf, "%016llx", (unsigned long long)fnv1a(key));
-      k.name = std::string("gft_") + kKindNameTC[kind] + (pair ? "2" : "") + "_f32_n" + std::to_string(c.n) + "_" + hbuf;
+      k.name = std::string("gft_") + kKindNameTC[kind] + (pair ? (wgs == 2 ? "2w" : "2") : "") + "_f32_n" + std::to_string(c.n) + "_" + hbuf;
       std::ostringstream src;
       src << "// generated by paper_1907_07875_b200 codegen.cpp — plan-specialised GFT kernel with\n"
           << "// tcgen05 3xTF32 leaves (" << T.size() << " tensor-core leaves)\n"

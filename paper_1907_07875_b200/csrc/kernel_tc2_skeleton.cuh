@@ -151,7 +151,17 @@ static __device__ __forceinline__ void signal_staged(u32 staged_cluster_addr) {
 
 // @@GFT_GENERATED@@  (codegen.cpp inserts gft_tcB[][] and gft_tile() here)
 
-extern "C" __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+// GFT_WGS compute warpgroups (1 or 2): with 2, consecutive pair tiles alternate between
+// warpgroups 0 and 1, each with its own TMEM columns (GFT_WG_COLS apart) and its own
+// mma / staged barriers, so one warpgroup stages and drains a tile while the tensor core
+// works on the other's -- the per-tile chain is hidden for small n (registers permitting).
+#ifndef GFT_WGS
+#define GFT_WGS 1
+#define GFT_WG_COLS 0
+#endif
+#define GFT_THREADS (32 * (4 * GFT_WGS + 2))
+
+extern "C" __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GFT_THREADS, 1)
 GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc tout,
           const float* X, float* Y, long long batch) {
   extern __shared__ unsigned char smem_raw[];
@@ -160,8 +170,8 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   unsigned char* stages = smem;
   unsigned char* bsm = smem + GFT_STAGES * GFT_TILE_BYTES;            // this CTA's half of B
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(bsm + GFT_B_FLOATS * 4);
-  // bars: full[S], done[S], mma, staged[GFT_NTC] (staged used in the leader only)
-  u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * GFT_STAGES + 1 + GFT_NTC);
+  // bars: full[S], done[S], mma[GFT_WGS], staged[GFT_WGS] (staged used in the leader only)
+  u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * GFT_STAGES + 2 * GFT_WGS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const u32 rank = cluster_rank();
   const long long npairs = (batch + 2 * GFT_TILE_ROWS - 1) / (2 * GFT_TILE_ROWS);
@@ -175,13 +185,15 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
                  :: "r"(smem_u32(tmem_slot)), "n"(GFT_TMEM_COLS) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
-  if (tid == 128) {
+  if (tid == 128 * GFT_WGS) {
     for (int s = 0; s < GFT_STAGES; ++s) {
       mbar_init(smem_u32(&bars[s]), 1);
       mbar_init(smem_u32(&bars[GFT_STAGES + s]), 4);
     }
-    mbar_init(smem_u32(&bars[2 * GFT_STAGES]), 1);
-    for (int i = 0; i < GFT_NTC; ++i) mbar_init(smem_u32(&bars[2 * GFT_STAGES + 1 + i]), 8);
+    for (int g = 0; g < GFT_WGS; ++g) {
+      mbar_init(smem_u32(&bars[2 * GFT_STAGES + g]), 1);
+      mbar_init(smem_u32(&bars[2 * GFT_STAGES + GFT_WGS + g]), 8);
+    }
     fence_mbar_init();
   }
   // this CTA's half of every B operand -> SMEM, K-major 128B-swizzled atoms
@@ -197,7 +209,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   tc_fence_after();
   const u32 tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 4 * GFT_WGS) {
     // ---------------- producer / storer of this CTA's 128 rows per pair tile ----------------
     if (lane == 0) {
       long long it = 0;
@@ -233,35 +245,37 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       }
       bulk_wait_all();
     }
-  } else if (warp == 5) {
-    // ---------------- MMA issuer (leader CTA only) ----------------
+  } else if (warp == 4 * GFT_WGS + 1) {
+    // ---------------- MMA issuer (leader CTA only); tile it belongs to warpgroup it % WGS ----
     if (rank == 0 && lane == 0) {
-      const u32 mbar = smem_u32(&bars[2 * GFT_STAGES]);
-      const u32 staged_local = smem_u32(&bars[2 * GFT_STAGES + 1]);
       const u32 bsm_s = smem_u32(bsm);
       for (long long it = 0;; ++it) {
         if (pid0 + it * npid >= npairs) break;
-        gft_issue_pair(tmem, bsm_s, mbar, staged_local, (u32)(it & 1));
+        const int g = (int)(it % GFT_WGS);
+        gft_issue_pair(tmem + (u32)(g * GFT_WG_COLS), bsm_s, smem_u32(&bars[2 * GFT_STAGES + g]),
+                       smem_u32(&bars[2 * GFT_STAGES + GFT_WGS + g]), (u32)((it / GFT_WGS) & 1));
       }
     }
   } else {
-    // ---------------- compute (thread tid = tile row tid = TMEM lane tid) ----------------
-    const u32 tm_lane = tmem + ((u32)(warp * 32) << 16);
+    // ---------------- compute (row r = TMEM lane r of this warpgroup's columns) ----------------
+    const int g = warp >> 2, row = tid & 127;
+    const u32 tmem_g = tmem + (u32)(g * GFT_WG_COLS);
+    const u32 tm_lane = tmem_g + ((u32)((warp & 3) * 32) << 16);
     const u32 bsm_s = smem_u32(bsm);
-    const u32 mbar = smem_u32(&bars[2 * GFT_STAGES]);
+    const u32 mbar = smem_u32(&bars[2 * GFT_STAGES + g]);
     // `staged` barriers live in the leader CTA (rank 0)
-    const u32 staged0 = map_to_cta(smem_u32(&bars[2 * GFT_STAGES + 1]), 0);
-    const u32 staged_local = smem_u32(&bars[2 * GFT_STAGES + 1]);
-    for (long long it = 0;; ++it) {
+    const u32 staged0 = map_to_cta(smem_u32(&bars[2 * GFT_STAGES + GFT_WGS + g]), 0);
+    const u32 staged_local = smem_u32(&bars[2 * GFT_STAGES + GFT_WGS + g]);
+    for (long long it = g;; it += GFT_WGS) {
       const long long p = pid0 + it * npid;
       if (p >= npairs) break;
       const int s = (int)(it % GFT_STAGES);
       mbar_wait(smem_u32(&bars[s]), (u32)((it / GFT_STAGES) & 1));
       unsigned char* buf = stages + s * GFT_TILE_BYTES;
       float x[GFT_N], y[GFT_N];
-      load_row(buf, tid, x);
-      gft_tile(x, y, tm_lane, tmem, bsm_s, mbar, staged0, staged_local, (u32)(it & 1), tid, rank);
-      store_row(buf, tid, y);
+      load_row(buf, row, x);
+      gft_tile(x, y, tm_lane, tmem_g, bsm_s, mbar, staged0, staged_local, (u32)((it / GFT_WGS) & 1), row, rank);
+      store_row(buf, row, y);
       fence_proxy_async();
       tc_fence_before();
       __syncwarp();

@@ -28,10 +28,11 @@ struct KernelCfg {
   int tc_pair = 0;              // CTA-pair (cta_group::2, cluster of 2) variant, grid must be even
   int tc_b_bytes = 0;           // SMEM bytes of the B operands
   int tc_tmem_cols = 0;         // TMEM columns allocated
+  int tc_wgs = 1;               // compute warpgroups of the CTA-pair kernel (1 or 2)
   int tile_rows() const { return tc ? 128 : 32 * R; }
   // tensor-core tiles pad each row to whole 32-float TMA boxes (kernel_tc*_skeleton.cuh)
   int tile_bytes() const { return tile_rows() * (tc ? (n + 31) / 32 * 32 : n) * elem; }
-  int threads() const { return tc ? (tc_pair ? 192 : 160) : warps * 32; }
+  int threads() const { return tc ? (tc_pair ? 32 * (4 * tc_wgs + 2) : 160) : warps * 32; }
   int tiles_per_cta() const { return tc ? 1 : warps; }   // tiles processed concurrently per CTA
   int smem_bytes() const {
     if (tc) return stages * tile_bytes() + tc_b_bytes + (2 * stages + 8) * 8 + 16 + 1024;
