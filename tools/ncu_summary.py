@@ -107,6 +107,13 @@ def main():
             f.write("| kernel | total ns | share |\n|---|---|---|\n")
             for k, v in sorted(shares.items(), key=lambda kv: -kv[1]):
                 f.write("| %s | %.0f | %.3f |\n" % (k, v, v / tot))
+            # the bench step is the fast forward + fast inverse; the dense (gft_d*) comparison
+            # kernels run after the timed region
+            step = {k: v for k, v in shares.items() if re.match(r"gft_(fwd|inv)", k)}
+            st = sum(step.values()) or 1.0
+            f.write("\nShare of the bench step (fast forward + fast inverse only; the dense `gft_d*` "
+                    "kernels are the comparison timed after the step): " +
+                    ", ".join("%s %.3f" % (k, v / st) for k, v in sorted(step.items())) + ".\n")
     with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
         json.dump({"round": a.round, "kernels": rows, "launch_shares": {k: v / tot for k, v in shares.items()}},
                   f, indent=1)
