@@ -169,8 +169,16 @@ def test_config_basis_invariants(name):
     assert np.abs(L @ U - U * lam).max() < 1e-10            # north-star residual bound
     assert np.abs(U.T @ U - np.eye(cfg.n)).max() < 1e-12
     assert np.all(np.diff(lam) >= -1e-12)
-    ref = np.linalg.eigh(L)[0]
+    ref, V_ref = np.linalg.eigh(L)
     assert np.abs(lam - ref).max() < 1e-11 * max(1, ref.max())
+    # eigenspaces vs LAPACK (a routine independent of the oracle's Jacobi), per cluster
+    for C in oracle.clusters(lam):
+        assert np.abs(_proj(U, C) - _proj(V_ref, C)).max() < 1e-10
+    # Theorem 3: spec(L) = spec(L+) u spec(L-) for the config's involution, by LAPACK
+    if cfg.phi is not None:
+        Lp, Lm, _, _ = oracle.decompose_blocks(L, cfg.phi)
+        spec = np.sort(np.concatenate([np.linalg.eigvalsh(Lp), np.linalg.eigvalsh(Lm)]))
+        assert np.abs(spec - ref).max() < 1e-11 * max(1, ref.max())
     # Parseval ||U^T x|| = ||x||
     x = workloads.signals(cfg, batch=64, dtype="f64").numpy()
     y = oracle.forward(x, U)
