@@ -120,6 +120,13 @@ class ClockSampler:
 from paper_1907_07875_b200.dist import barrier, dist_env, max_over_ranks  # noqa: E402
 
 
+def fma_peak_per_s(dtype, sm_mhz=1965.0, sms=148):
+    """Lane-FMA issue peak: FFMA with an immediate operand (the form the generated kernels use)
+    issues 1 warp instruction / clk / SMSP (B300_MICROARCH.md "FFMA imm-form rt_SMSP=1"), i.e.
+    128 lane-FMAs / clk / SM; DFMA runs at half that on B200.  sm_mhz = the max SM clock."""
+    return sms * (128 if dtype == "f32" else 64) * sm_mhz * 1e6
+
+
 def time_kernel(fn, stream, warmup, iters):
     import torch
     for _ in range(warmup):
@@ -180,6 +187,9 @@ def config_table(args, stream, hbm, device):
                                      "signals_per_s": cfg.batch / ms * 1e3}
         if cfg.batch * cfg.n * esz <= (64 << 20):   # small workloads: launch-bound, replay a graph
             row["fast_fwd"]["graph_ms"] = round(time_graph(lambda: plan.forward(X, Y), 50), 5)
+        # the dense kernel is FMA-issue-bound for n >= 64: its fraction of the lane-FMA peak
+        row["dense_fwd"]["fma_frac"] = round(cfg.n * cfg.n * cfg.batch / (row["dense_fwd"]["ms"] * 1e-3)
+                                             / fma_peak_per_s(dtype), 4)
         row["fast_vs_dense_fwd"] = round(row["dense_fwd"]["ms"] / row["fast_fwd"]["ms"], 3)
         row["fast_vs_dense_inv"] = round(row["dense_inv"]["ms"] / row["fast_inv"]["ms"], 3)
         # fused graph filter U diag(exp(-lambda)) U^T (one pass) vs forward + inverse (two)
@@ -277,14 +287,19 @@ def approx_table(args, stream, hbm, device):
         plan = gft.Plan(64, s, d, w, None, phi, dtypes=("f32",), **kw)
         info = plan.info()
         ms = time_kernel(lambda: plan.forward(X, Y, stream), stream, 3, args.table_iters)
+        # lane-FMA instructions per signal as generated: dense = n^2, Givens = 2 per rotation +
+        # one output multiply per position, exact leaves = sum k^2 (units are adds)
+        fmas = 2 * info["n_givens"] + 64 if info["n_givens"] else info["sum_k2"]
         row = {"graph": label, "variant": variant, "adds": info["adds"], "mults": info["mults"],
-               "givens": info["n_givens"], "fast_fwd": {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
+               "givens": info["n_givens"], "fma_frac": round(fmas * batch / (ms * 1e-3) / fma_peak_per_s("f32"), 4),
+               "fast_fwd": {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
                                                         "frac": round(nbytes / ms / 1e6 / hbm, 4)}}
         if variant == "haar":
             exact[label] = plan.basis()
             msd = time_kernel(lambda: plan.dense_forward(X, Y, stream), stream, 3, args.table_iters)
             rows.append({"graph": label, "variant": "matrix", "adds": info["dense_adds"],
                          "mults": info["dense_mults"], "delta": 0.0, "epsilon": 0.0,
+                         "fma_frac": round(4096 * batch / (msd * 1e-3) / fma_peak_per_s("f32"), 4),
                          "fast_fwd": {"ms": round(msd, 5), "gbs": round(nbytes / msd / 1e6, 1),
                                       "frac": round(nbytes / msd / 1e6 / hbm, 4)}})
             row.update(delta=0.0, epsilon=0.0)
