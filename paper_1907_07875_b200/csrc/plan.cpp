@@ -280,17 +280,17 @@ struct Builder {
   // constant diagonal c; builds E (part S1) and F (part S2) from the component's
   // eigenvectors paired by sigma = diag(+1 on S1, -1 on S2) (Lemma 1 / Theorem 1
   // construction).  Returns false (caller emits a dense leaf) if any check fails.
-  bool try_right(const SubGraph& g, const std::vector<int>& pos, int depth) {
+  // The preconditions of a right Haar stage on a connected (sub)graph: constant Laplacian
+  // diagonal and a 2-colouring; returns the parts S1 (colour of node 0) and S2.
+  static bool right_parts(const SubGraph& g, std::vector<int>& S1, std::vector<int>& S2) {
     const int k = g.k;
     if (k < 2) return false;
     const std::vector<double> L = g.laplacian();
     double lmax = 0;
     for (double v : L) lmax = std::max(lmax, std::fabs(v));
     const double tol = 1e-9 * std::max(1.0, lmax);
-    const double c = L[0];
     for (int i = 0; i < k; ++i)
-      if (std::fabs(L[(size_t)i * k + i] - c) > tol) return false;
-    // 2-colouring over the edges (the component is connected)
+      if (std::fabs(L[(size_t)i * k + i] - L[0]) > tol) return false;
     std::vector<int> col(k, -1);
     col[0] = 0;
     std::vector<int> q{0};
@@ -302,9 +302,21 @@ struct Builder {
         else if (col[v] == col[u]) return false;   // odd cycle: not bipartite
       }
     }
-    std::vector<int> S1, S2;
+    S1.clear();
+    S2.clear();
     for (int i = 0; i < k; ++i) (col[i] == 0 ? S1 : S2).push_back(i);
-    if (S2.empty()) return false;
+    return !S2.empty() && (int)q.size() == k;
+  }
+
+  bool try_right(const SubGraph& g, const std::vector<int>& pos, int depth) {
+    const int k = g.k;
+    std::vector<int> S1, S2;
+    if (!right_parts(g, S1, S2)) return false;
+    const std::vector<double> L = g.laplacian();
+    double lmax = 0;
+    for (double v : L) lmax = std::max(lmax, std::fabs(v));
+    const double tol = 1e-9 * std::max(1.0, lmax);
+    const double c = L[0];
     std::vector<double> lam, V;
     jacobi_eigh(k, L, lam, V);
     auto comp = [&](int j, const std::vector<int>& S, double scale) {
@@ -481,6 +493,15 @@ struct Builder {
     if (r.p == 0) {
       if (!(opt.right_haar && try_right(g, pos, depth))) emit_leaf(g, pos, depth);
       return;
+    }
+    // both stage types available (a symmetric k-RBG / normalised bipartite graph): take the
+    // one with fewer leaf multiplications at this level -- p^2 + (n-p)^2 for the left stage
+    // (PAPER.md:721), |S1|^2 + |S2|^2 for the right stage (reading R-7)
+    std::vector<int> S1, S2;
+    if (opt.right_haar && right_parts(g, S1, S2)) {
+      const int64_t kr = (int64_t)S1.size() * S1.size() + (int64_t)S2.size() * S2.size();
+      const int64_t kl = (int64_t)r.p * r.p + (int64_t)(g.k - r.p) * (g.k - r.p);
+      if (kr < kl && try_right(g, pos, depth)) return;
     }
     emit_stage(g, pos, depth, r.phi);
   }
