@@ -143,41 +143,39 @@ def test_canonical_signs_of_right_pairs():
             assert first > 0
 
 
-def _rbg_with_twins(seed):
-    """Unweighted 3-regular bipartite graph on 8|8 in which S1 nodes 0 and 1 are twins (same
-    three neighbours 8, 9, 10): the transposition (0 1) is a symmetry with p = 1 (Lemma 4)."""
+def _bipartite_with_twins(seed):
+    """Random weighted bipartite graph on 8|8 where S1 nodes 0 and 1 are twins (identical
+    neighbours and weights): the transposition (0 1) is its only symmetry (p = 1, Lemma 4);
+    with the normalised Laplacian (diagonal 1) a right stage also applies."""
     rng = np.random.default_rng(seed)
-    base = [(0, 8), (0, 9), (0, 10), (1, 8), (1, 9), (1, 10), (2, 8), (3, 9), (4, 10)]
-    s1 = [2, 2, 3, 3, 4, 4, 5, 5, 5, 6, 6, 6, 7, 7, 7]
-    for _ in range(1000):
-        s2 = list(rng.permutation([v for v in range(11, 16) for _ in range(3)]))
-        edges = set(base)
-        ok = True
-        for a, b in zip(s1, s2):
-            if (a, int(b)) in edges:
-                ok = False
-                break
-            edges.add((a, int(b)))
-        if ok:
-            return workloads._edges(sorted(edges))
-    raise RuntimeError("no simple completion")
+    pairs, wts = [], []
+    nb0 = [8, 9, 10]
+    w0 = rng.uniform(0.5, 2.0, 3)
+    for v, x in zip(nb0, w0):
+        pairs += [(0, v), (1, v)]
+        wts += [x, x]
+    for a in range(2, 8):
+        for b in range(8, 16):
+            if rng.random() < 0.45 or b == 8 + (a % 8):
+                pairs.append((a, b))
+                wts.append(rng.uniform(0.5, 2.0))
+    return workloads._edges(pairs, wts)
 
 
 def test_right_stage_preferred_over_a_small_left_stage():
     """Reading R-7: with a symmetry of p = 1 the left stage leaves 1 + 15^2 = 226 leaf
     multiplications, the right stage 8^2 + 8^2 = 128 -- the planner takes the right stage,
     and the basis is still the oracle's GFT."""
-    s, d, w = _rbg_with_twins(0)
-    L = oracle.laplacian(16, s, d, w)
-    assert np.allclose(np.diag(L), 3)
+    s, d, w = _bipartite_with_twins(0)
+    L = oracle.normalized_laplacian(oracle.laplacian(16, s, d, w))
     phi, p, _ = G.gft_find_involution(L)
-    assert p >= 1
-    plan = G.Plan(16, s, d, w, host_only=True)
+    assert p == 1 and phi[0] == 1
+    plan = G.Plan(16, s, d, w, host_only=True, normalized=True)
     info = plan.info()
-    if p * p + (16 - p) ** 2 > 128:
-        assert info["depth"] == 0 and info["n_right_stages"] == 1
-        assert info["sum_k2"] == 128
+    assert info["depth"] == 0 and info["n_right_stages"] == 1 and info["sum_k2"] == 128
     _check_basis(L, plan)
+    off = G.Plan(16, s, d, w, host_only=True, normalized=True, right_haar=False).info()
+    assert off["units_per_level"][0] == 1 and off["sum_k2"] > 128
     # the cycle C64 (2-RBG with p = 32: 2048 = 2048) keeps the left recursion
     cfg = workloads.config("cfg5a")
     assert G.Plan.from_config(cfg, host_only=True).info()["n_right_stages"] == 0
