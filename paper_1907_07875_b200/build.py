@@ -33,7 +33,7 @@ ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
 SKELETONS = {"kernel_skeleton.cuh": "skeleton_inc.h", "kernel_tc_skeleton.cuh": "skeleton_tc_inc.h",
-             "kernel_tc2_skeleton.cuh": "skeleton_tc2_inc.h"}
+             "kernel_tc2_skeleton.cuh": "skeleton_tc2_inc.h", "kernel_tc3_skeleton.cuh": "skeleton_tc3_inc.h"}
 
 
 def _write_skeleton_inc():

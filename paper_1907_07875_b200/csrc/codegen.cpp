@@ -29,6 +29,9 @@ static const char* kSkeletonTC =
 static const char* kSkeletonTC2 =
 #include "skeleton_tc2_inc.h"
     ;
+static const char* kSkeletonTC3 =
+#include "skeleton_tc3_inc.h"
+    ;
 
 KernelCfg choose_cfg(int n, int dtype, int64_t work) {
   KernelCfg c;
@@ -474,6 +477,145 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, bool pair, 
   }
 }
 
+// Warp-specialised CTA-pair variant (kernel_tc3_skeleton.cuh): the tile chain split into a
+// stager (front butterflies, hi/lo -> TMEM A, small leaves -> SMEM row) and a drainer
+// (TMEM D -> registers, back / coefficient butterflies); D double-buffered in TMEM.
+// Returns false if the TMEM layout (A + 2 D) does not fit in 512 columns.
+bool ws_layout(std::vector<TcLeaf>& T, int& a_cols, int& d_cols, int& tmem_cols) {
+  a_cols = d_cols = 0;
+  for (auto& t : T) {
+    t.hi_col = a_cols;
+    t.lo_col = a_cols + ru(t.kp8, 32);
+    a_cols += 2 * ru(t.kp8, 32);
+  }
+  for (auto& t : T) {
+    t.d_col = d_cols;            // relative to the D buffer base
+    d_cols += ru(t.np, 32);
+  }
+  if (a_cols + 2 * d_cols > 512) return false;
+  tmem_cols = 32;
+  while (tmem_cols < a_cols + 2 * d_cols) tmem_cols *= 2;
+  return true;
+}
+
+void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_cols, int d_cols,
+                    std::ostringstream& o) {
+  const int dtype = GFT_F32;
+  std::vector<char> is_tc(P.leaves.size(), 0);
+  for (const auto& t : T) is_tc[t.leaf] = 1;
+  // ---- B operands: identical layout to the CTA-pair kernel (N/2 rows per CTA) ----
+  std::vector<float> B;
+  for (int r = 0; r < 2; ++r)
+    for (const auto& t : T) {
+      const Leaf& lf = P.leaves[t.leaf];
+      const int rows = t.np / 2;
+      for (int part = 0; part < 2; ++part)
+        for (int a = 0; a < t.kp32 / 32; ++a)
+          for (int n = r * rows; n < (r + 1) * rows; ++n)
+            for (int kk = 32 * a; kk < 32 * a + 32; ++kk) {
+              float v = 0.f;
+              if (n < t.k && kk < t.k) v = (float)leaf_coef(lf, d, n, kk);
+              const float hi = tf32_rna_host(v);
+              B.push_back(part == 0 ? hi : v - hi);
+            }
+    }
+  const size_t per_cta = B.size() / 2;
+  o << "#define GFT_B_FLOATS " << per_cta << "\n#define GFT_A_COLS " << a_cols << "\n#define GFT_D_COLS "
+    << d_cols << "\n#define GFT_SMALL " << (T.size() < P.leaves.size() ? 1 : 0) << "\n";
+  o << "__device__ __align__(16) const float gft_tcB[2][" << per_cta << "] = {\n";
+  for (size_t i = 0; i < B.size(); ++i) {
+    char buf[48];
+    std::snprintf(buf, sizeof buf, "%af,", (double)B[i]);
+    o << buf << ((i % 8 == 7) ? "\n" : "");
+  }
+  o << "};\n";
+  o << "static __device__ __forceinline__ void st_elem(unsigned char* buf, int row, int col, float v) {\n"
+       "  *reinterpret_cast<float*>(buf + tile_off(row, col)) = v;\n}\n"
+       "static __device__ __forceinline__ float ld_elem(const unsigned char* buf, int row, int col) {\n"
+       "  return *reinterpret_cast<const float*>(buf + tile_off(row, col));\n}\n";
+  // ---- stager ----
+  o << "static __device__ __forceinline__ void gft_stage(float (&x)[GFT_N], u32 tm, u32 staged0,\n"
+       "    unsigned char* buf, int row, u32 abar, u32 apar, bool await_a) {\n";
+  if (d != DIR_INV) emit_units(o, P, "x", false, dtype);
+  if (d == DIR_FILTER && !P.post.empty()) fail(GFT_ERR_COMPILE, "filter plan with right Haar stages");
+  if (d == DIR_INV) emit_post_units(o, P, "x", true, "float");
+  o << "  if (await_a) { mbar_wait(abar, apar); tc_fence_after(); }   // MMA(t-1) has read A\n";
+  for (const TcLeaf& t : T) {
+    const Leaf& lf = P.leaves[t.leaf];
+    for (int c0 = 0; c0 < t.kp8; c0 += 32) {
+      const int w = std::min(32, t.kp8 - c0);
+      o << "  { u32 h[" << w << "], l[" << w << "];\n";
+      for (int c = c0; c < c0 + w; ++c) {
+        if (c < t.k) {
+          const int src = in_idx(lf, d, c);
+          o << "  h[" << c - c0 << "] = tf32_rna(x[" << src << "]); l[" << c - c0 << "] = __float_as_uint(x["
+            << src << "] - __uint_as_float(h[" << c - c0 << "]));\n";
+        } else {
+          o << "  h[" << c - c0 << "] = 0u; l[" << c - c0 << "] = 0u;\n";
+        }
+      }
+      emit_tmem_st(o, "h", t.hi_col + c0, w);
+      emit_tmem_st(o, "l", t.lo_col + c0, w);
+      o << "  }\n";
+    }
+  }
+  o << "  signal_staged(staged0);\n";
+  if (T.size() < P.leaves.size()) {
+    o << "  { float y[GFT_N];\n";
+    for (size_t l = 0; l < P.leaves.size(); ++l)
+      if (!is_tc[l]) emit_leaf_fma(o, P.leaves[l], l, d, dtype);
+    for (size_t l = 0; l < P.leaves.size(); ++l)
+      if (!is_tc[l])
+        for (int r = 0; r < P.leaves[l].k; ++r) {
+          const int oi = out_idx(P.leaves[l], d, r);
+          o << "  st_elem(buf, row, " << oi << ", y[" << oi << "]);\n";
+        }
+    o << "  }\n";
+  }
+  o << "}\n";
+  // ---- drainer: small-leaf outputs from SMEM, TC outputs from TMEM ----
+  o << "static __device__ __forceinline__ void gft_drain(float (&y)[GFT_N], u32 tm, const unsigned char* buf, int row) {\n";
+  for (size_t l = 0; l < P.leaves.size(); ++l)
+    if (!is_tc[l])
+      for (int r = 0; r < P.leaves[l].k; ++r) {
+        const int oi = out_idx(P.leaves[l], d, r);
+        o << "  y[" << oi << "] = ld_elem(buf, row, " << oi << ");\n";
+      }
+  for (const TcLeaf& t : T) {
+    const Leaf& lf = P.leaves[t.leaf];
+    for (int r0 = 0; r0 < t.k; r0 += 32) {
+      const int w = std::min(32, t.np - r0);
+      o << "  { u32 d[" << w << "];\n";
+      emit_tmem_ld(o, "d", t.d_col + r0, w);
+      for (int r = r0; r < std::min(t.k, r0 + w); ++r)
+        o << "  y[" << out_idx(lf, d, r) << "] = __uint_as_float(d[" << r - r0 << "]);\n";
+      o << "  }\n";
+    }
+  }
+  o << "}\n";
+  o << "static __device__ __forceinline__ void gft_finish(float (&y)[GFT_N]) {\n";
+  if (d == DIR_FWD) emit_post_units(o, P, "y", false, "float");
+  if (d != DIR_FWD) emit_units(o, P, "y", true, dtype);
+  o << "}\n";
+  // ---- issuer ----
+  o << "static __device__ __forceinline__ void gft_issue_ws(u32 tA, u32 tD, u32 bsm) {\n";
+  for (const TcLeaf& t : T) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(t.np >> 3) << 17) | (16u << 24);
+    const int ksteps = t.kp8 / 8;
+    const int atom_bytes = (t.np / 2) * 128;
+    for (int pass = 0; pass < 3; ++pass) {
+      const int acol = pass == 2 ? t.lo_col : t.hi_col;
+      const int boff = pass == 1 ? t.blo_off : t.bhi_off;
+      for (int j = 0; j < ksteps; ++j) {
+        const int bo = boff + (j / 4) * atom_bytes + (j % 4) * 32;
+        o << "  mma_ts2(tD + " << t.d_col << "u, tA + " << (acol + 8 * j) << "u, smem_desc_sw128(bsm + " << bo
+          << "u), " << idesc << "u, " << ((pass == 0 && j == 0) ? 0 : 1) << "u);\n";
+      }
+    }
+  }
+  o << "}\n";
+}
+
 }  // namespace
 
 void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc, bool dense_tc) {
@@ -543,11 +685,34 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
           }
       }
     }
+    // warp-specialised pair kernel (stager / drainer, D double-buffered) when its TMEM layout
+    // and FOUR tile buffers fit: a buffer is held from TMA load through staging to the drain,
+    // so with 3 buffers only one tile of prefetch remains and the stager waits on HBM
+    // (measured: n = 64 +9% over the two-warpgroup kernel; n = 128 with 3 buffers -7% vs the
+    // plain pair kernel).  GFT_NO_TC_WS=1 keeps the plain pair kernel (ablation).
+    bool ws = false;
+    int ws_a = 0, ws_d = 0, ws_tmem = 0;
+    std::vector<TcLeaf> Tws;
+    if (ok && pair && getenv("GFT_NO_TC_WS") == nullptr) {
+      Tws = T;
+      if (ws_layout(Tws, ws_a, ws_d, ws_tmem)) {
+        const int tile = 128 * ((P.n + 31) / 32 * 32) * 4;
+        int st = 6;
+        while (st >= 4 && st * tile + b_bytes + 2048 > 227 * 1024) --st;
+        if (st >= 4) {
+          ws = true;
+          stages = st;
+          wgs = 1;
+          tmem_cols = ws_tmem;
+        }
+      }
+    }
     if (ok) {
       KernelCfg& c = k.cfg;
       c.tc = 1;
       c.tc_pair = pair ? 1 : 0;
       c.tc_wgs = wgs;
+      c.tc_ws = ws ? 1 : 0;
       c.stages = stages;
       c.mode = 0;
       c.boxc = 32;
@@ -558,19 +723,20 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
       c.tc_b_bytes = b_bytes;
       c.tc_tmem_cols = tmem_cols;
       std::ostringstream gen;
-      generate_tc(P, dir, T, pair, gen);
+      if (ws) generate_tc_ws(P, dir, Tws, ws_a, ws_d, gen);
+      else generate_tc(P, dir, T, pair, gen);
       std::ostringstream pre;
       pre << "#define GFT_N " << c.n << "\n#define GFT_STAGES " << c.stages << "\n#define GFT_TMEM_COLS "
           << tmem_cols << "\n";
       if (wgs == 2) pre << "#define GFT_WGS 2\n#define GFT_WG_COLS " << wg_cols << "\n";
-      const std::string skel(pair ? kSkeletonTC2 : kSkeletonTC);
+      const std::string skel(ws ? kSkeletonTC3 : pair ? kSkeletonTC2 : kSkeletonTC);
       const std::string marker = "// @@GFT_GENERATED@@";
       const size_t at = skel.find(marker);
       if (at == std::string::npos) fail(GFT_ERR_COMPILE, "TC skeleton marker missing");
       const std::string key = pre.str() + gen.str() + skel;
       char hbuf[32];
       std::snprintf(hbuf, sizeof hbuf, "%016llx", (unsigned long long)fnv1a(key));
-      k.name = std::string("gft_") + kKindNameTC[kind] + (pair ? (wgs == 2 ? "2w" : "2") : "") + "_f32_n" + std::to_string(c.n) + "_" + hbuf;
+      k.name = std::string("gft_") + kKindNameTC[kind] + (ws ? "3" : pair ? (wgs == 2 ? "2w" : "2") : "") + "_f32_n" + std::to_string(c.n) + "_" + hbuf;
       std::ostringstream src;
       src << "// generated by paper_1907_07875_b200 codegen.cpp — plan-specialised GFT kernel with\n"
           << "// tcgen05 3xTF32 leaves (" << T.size() << " tensor-core leaves)\n"

@@ -1,0 +1,327 @@
+// kernel_tc3_skeleton.cuh — warp-specialised CTA-pair tensor-core GFT kernel.
+//
+// Same math and operand layout as kernel_tc2_skeleton.cuh (cta_group::2, M = 256, 3xTF32,
+// A in TMEM, half of every B operand per CTA), but the per-tile chain
+//   rows -> butterflies -> hi/lo -> TMEM -> MMA -> tcgen05.ld -> rows
+// is split between two warpgroups so that consecutive tiles overlap:
+//   WG0 (warps 0-3)  stager : rows -> registers -> front butterflies -> hi/lo -> TMEM A
+//                             columns -> arrive on the leader's `staged`; small (CUDA-core)
+//                             leaves -> their outputs written back into the SMEM row;
+//   WG1 (warps 4-7)  drainer: wait for the tile's MMAs -> tcgen05.ld the D columns (double
+//                             buffered in TMEM) -> free them (`d_free` on the leader) ->
+//                             back butterflies / coefficient butterflies -> SMEM row;
+//   warp 8           TMA producer / storer of this CTA's rows;
+//   warp 9           MMA issuer (leader CTA): staged(t) and d_free(t-2) -> MMAs into
+//                             D[t % 2] -> one multicast commit on mma_done[t % 2];
+//   warps 10-11      idle (a full third warpgroup so that setmaxnreg can move registers:
+//                             WG2 drops to 56, the stager rises to 248, the drainer to 200).
+// The stager of tile t+1 only waits for MMA(t) to have READ the A columns (mma_done(t)),
+// so staging t+1, the MMAs of t and the drain of t-1 run concurrently.
+// TMEM: A = all leaves' hi/lo columns (single buffer), D = all leaves' D columns x 2.
+// Generated part: GFT_N, GFT_STAGES, GFT_TMEM_COLS, GFT_B_FLOATS, GFT_KNAME, gft_tcB[2][],
+// GFT_A_COLS (D buffer 0 base), GFT_D_COLS (per buffer), GFT_SMALL (1 if CUDA-core leaves
+// exist), gft_stage(), gft_drain(), gft_issue_ws().
+typedef unsigned int u32;
+typedef unsigned long long u64;
+typedef float elem_t;
+
+struct __align__(64) TmaDesc { u64 d[16]; };
+
+#define GFT_TILE_ROWS 128
+// tile rows are padded to whole 32-float (128 B) TMA boxes; TMA zero-fills the columns
+// beyond n on load and clips them on store, so any n % 4 == 0 works
+#define GFT_NP ((GFT_N + 31) / 32 * 32)
+#define GFT_ROW_BYTES (GFT_NP * 4)
+#define GFT_TILE_BYTES (GFT_TILE_ROWS * GFT_ROW_BYTES)
+#define GFT_BOXC 32
+#define GFT_BOX_BYTES (GFT_TILE_ROWS * 128)
+#define GFT_NBOX (GFT_NP / GFT_BOXC)
+
+static __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+static __device__ __forceinline__ void mbar_init(u32 bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+static __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+static __device__ __forceinline__ void mbar_expect_tx(u32 bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+static __device__ __forceinline__ void mbar_arrive(u32 bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
+// arrive on the mbarrier at shared::cluster address `cbar` (may live in the peer CTA)
+static __device__ __forceinline__ void mbar_arrive_cluster(u32 cbar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" :: "r"(cbar) : "memory");
+}
+static __device__ __forceinline__ u32 map_to_cta(u32 saddr, u32 rank) {
+  u32 r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+static __device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
+  u32 done = 0;
+  do {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  } while (!done);
+}
+static __device__ __forceinline__ void mbar_wait_acq_cluster(u32 bar, u32 parity) {
+  u32 done = 0;
+  do {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  } while (!done);
+}
+static __device__ __forceinline__ u32 cluster_rank() {
+  u32 r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+static __device__ __forceinline__ u32 cluster_id_x() {
+  u32 r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+static __device__ __forceinline__ u32 nclusters_x() {
+  u32 r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+static __device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+static __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+static __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+static __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+static __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+static __device__ __forceinline__ void tma_load_2d(u32 dst, const TmaDesc* desc, int c0, int c1, u32 bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      :: "r"(dst), "l"((u64)desc), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+static __device__ __forceinline__ void tma_store_2d(const TmaDesc* desc, int c0, int c1, u32 src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+               :: "l"((u64)desc), "r"(c0), "r"(c1), "r"(src) : "memory");
+}
+// ---- tcgen05 ----
+static __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+static __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+static __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// commit all prior MMAs of this thread; arrive on the mbarrier at the same offset in both CTAs
+static __device__ __forceinline__ void tc_commit_pair(u32 bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               :: "r"(bar), "h"((unsigned short)3) : "memory");
+}
+// D[tmem, both CTAs] (+)= A[tmem, both CTAs] . B[smem desc, N/2 rows per CTA]^T  (M=256, K=8)
+static __device__ __forceinline__ void mma_ts2(u32 d, u32 a, u64 bdesc, u32 idesc, u32 acc) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+               "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p; }"
+               :: "r"(d), "r"(a), "l"(bdesc), "r"(idesc), "r"(acc) : "memory");
+}
+// K-major, 128B-swizzled operand: 8-row core-matrix groups 1024 B apart (SBO)
+static __device__ __forceinline__ u64 smem_desc_sw128(u32 saddr) {
+  return (u64)((saddr >> 4) & 0x3FFFu) | ((u64)(16u >> 4) << 16) | ((u64)(1024u >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+static __device__ __forceinline__ u32 tf32_rna(float v) {
+  u32 r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return r;
+}
+static __device__ __forceinline__ u32 tile_off(int row, int col) {
+  const u32 lin = (u32)((col >> 5) * GFT_BOX_BYTES + row * 128 + (col & 31) * 4);
+  return lin ^ (((lin >> 7) & 7u) << 4);
+}
+static __device__ __forceinline__ void load_row(const unsigned char* buf, int row, float (&x)[GFT_N]) {
+#pragma unroll
+  for (int c = 0; c < GFT_N; c += 4) {
+    float4 v = *reinterpret_cast<const float4*>(buf + tile_off(row, c));
+    x[c] = v.x; x[c + 1] = v.y; x[c + 2] = v.z; x[c + 3] = v.w;
+  }
+}
+static __device__ __forceinline__ void store_row(unsigned char* buf, int row, const float (&y)[GFT_N]) {
+#pragma unroll
+  for (int c = 0; c < GFT_N; c += 4)
+    *reinterpret_cast<float4*>(buf + tile_off(row, c)) = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
+}
+// one elected lane per warp signals "my 32 lanes are staged" to the leader CTA
+static __device__ __forceinline__ void signal_staged(u32 staged_cluster_addr) {
+  tc_wait_st();
+  tc_fence_before();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(staged_cluster_addr);
+}
+
+
+// @@GFT_GENERATED@@  (codegen.cpp inserts gft_tcB[][], gft_stage(), gft_drain(), gft_issue_ws())
+
+// register split of the 12 warps (65536 = 32 x 4 x (248 + 200 + 56)): the stager holds a row
+// plus hi/lo chunks, the drainer a row plus one D chunk, producer / issuer almost nothing
+static __device__ __forceinline__ void reg_stager() { asm volatile("setmaxnreg.inc.sync.aligned.u32 248;" ::: "memory"); }
+static __device__ __forceinline__ void reg_drainer() { asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory"); }
+static __device__ __forceinline__ void reg_control() { asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory"); }
+
+extern "C" __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc tout,
+          const float* X, float* Y, long long batch) {
+  extern __shared__ unsigned char smem_raw[];
+  const u32 raw_s = smem_u32(smem_raw);
+  unsigned char* smem = smem_raw + ((1024u - (raw_s & 1023u)) & 1023u);
+  unsigned char* stages = smem;
+  unsigned char* bsm = smem + GFT_STAGES * GFT_TILE_BYTES;            // this CTA's half of B
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(bsm + GFT_B_FLOATS * 4);
+  // bars: full[S], done[S], rows[S], staged, mma_done[2], d_free[2]
+  unsigned long long* b_full = bars;
+  unsigned long long* b_done = bars + GFT_STAGES;
+  unsigned long long* b_rows = bars + 2 * GFT_STAGES;
+  unsigned long long* b_staged = bars + 3 * GFT_STAGES;
+  unsigned long long* b_mma = bars + 3 * GFT_STAGES + 1;
+  unsigned long long* b_dfree = bars + 3 * GFT_STAGES + 3;
+  u32* tmem_slot = reinterpret_cast<u32*>(bars + 3 * GFT_STAGES + 5);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const u32 rank = cluster_rank();
+  const long long npairs = (batch + 2 * GFT_TILE_ROWS - 1) / (2 * GFT_TILE_ROWS);
+  const long long pid0 = cluster_id_x(), npid = nclusters_x();
+
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp == 0) {   // paired TMEM allocation: same warp id and smem slot in both CTAs
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(tmem_slot)), "n"(GFT_TMEM_COLS) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  if (tid == 256) {
+    for (int s = 0; s < GFT_STAGES; ++s) {
+      mbar_init(smem_u32(&b_full[s]), 1);
+      mbar_init(smem_u32(&b_done[s]), 4);
+      mbar_init(smem_u32(&b_rows[s]), 4);
+    }
+    mbar_init(smem_u32(b_staged), 8);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&b_mma[b]), 1);
+      mbar_init(smem_u32(&b_dfree[b]), 8);
+    }
+    fence_mbar_init();
+  }
+  const float4* bsrc = reinterpret_cast<const float4*>(gft_tcB[rank]);
+  for (int i = tid; i < GFT_B_FLOATS / 4; i += blockDim.x) {
+    const float4 v = bsrc[i];
+    const u32 lin = (u32)i * 16u;
+    *reinterpret_cast<float4*>(bsm + (lin ^ (((lin >> 7) & 7u) << 4))) = v;
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  cluster_sync();   // barriers initialised and B resident in both CTAs before any remote access
+  tc_fence_after();
+  const u32 tmem = *tmem_slot;
+
+  if (warp >= 8) {
+    reg_control();
+    if (warp == 8 && lane == 0) {
+      // ---------------- producer / storer of this CTA's 128 rows per pair tile ----------------
+      long long it = 0;
+      for (;; ++it) {
+        const long long p = pid0 + it * npid;
+        if (p >= npairs) break;
+        const long long row0 = p * 2 * GFT_TILE_ROWS + rank * GFT_TILE_ROWS;
+        const int s = (int)(it % GFT_STAGES);
+        if (it >= GFT_STAGES) {
+          const long long prow = row0 - GFT_STAGES * npid * 2 * GFT_TILE_ROWS;
+          mbar_wait(smem_u32(&b_done[s]), (u32)(((it / GFT_STAGES) - 1) & 1));
+          const u32 src = smem_u32(stages + s * GFT_TILE_BYTES);
+          for (int b = 0; b < GFT_NBOX; ++b)
+            tma_store_2d(&tout, b * GFT_BOXC, (int)prow, src + b * GFT_BOX_BYTES);
+          bulk_commit();
+          bulk_wait_read0();
+        }
+        const u32 bar = smem_u32(&b_full[s]);
+        const u32 dst = smem_u32(stages + s * GFT_TILE_BYTES);
+        mbar_expect_tx(bar, GFT_TILE_BYTES);
+        for (int b = 0; b < GFT_NBOX; ++b)
+          tma_load_2d(dst + b * GFT_BOX_BYTES, &tin, b * GFT_BOXC, (int)row0, bar);
+      }
+      const long long first = it > GFT_STAGES ? it - GFT_STAGES : 0;
+      for (long long j = first; j < it; ++j) {
+        const int s = (int)(j % GFT_STAGES);
+        const long long row0 = (pid0 + j * npid) * 2 * GFT_TILE_ROWS + rank * GFT_TILE_ROWS;
+        mbar_wait(smem_u32(&b_done[s]), (u32)((j / GFT_STAGES) & 1));
+        const u32 src = smem_u32(stages + s * GFT_TILE_BYTES);
+        for (int b = 0; b < GFT_NBOX; ++b)
+          tma_store_2d(&tout, b * GFT_BOXC, (int)row0, src + b * GFT_BOX_BYTES);
+        bulk_commit();
+      }
+      bulk_wait_all();
+    } else if (warp == 9 && rank == 0 && lane == 0) {
+      // ---------------- MMA issuer (leader CTA) ----------------
+      const u32 bsm_s = smem_u32(bsm);
+      for (long long it = 0;; ++it) {
+        if (pid0 + it * npid >= npairs) break;
+        const int b = (int)(it & 1);
+        mbar_wait_acq_cluster(smem_u32(b_staged), (u32)(it & 1));
+        if (it >= 2) mbar_wait_acq_cluster(smem_u32(&b_dfree[b]), (u32)(((it >> 1) - 1) & 1));
+        tc_fence_after();
+        // re-materialise the B base each tile so the ~100 MMA descriptors are not hoisted
+        // out of the loop into registers (this warpgroup runs with 56 registers)
+        u32 bs;
+        asm volatile("mov.b32 %0, %1;" : "=r"(bs) : "r"(bsm_s));
+        gft_issue_ws(tmem, tmem + (u32)(GFT_A_COLS + b * GFT_D_COLS), bs);
+        tc_commit_pair(smem_u32(&b_mma[b]));
+      }
+    }
+  } else if (warp < 4) {
+    // ---------------- stager (row = TMEM lane = tid) ----------------
+    reg_stager();
+    const u32 tm_a = tmem + ((u32)(warp * 32) << 16);
+    const u32 staged0 = map_to_cta(smem_u32(b_staged), 0);
+    for (long long it = 0;; ++it) {
+      const long long p = pid0 + it * npid;
+      if (p >= npairs) break;
+      const int s = (int)(it % GFT_STAGES);
+      mbar_wait(smem_u32(&b_full[s]), (u32)((it / GFT_STAGES) & 1));
+      unsigned char* buf = stages + s * GFT_TILE_BYTES;
+      float x[GFT_N];
+      load_row(buf, tid, x);
+      // before writing the A columns: the MMAs of the previous tile have read them
+      gft_stage(x, tm_a, staged0, buf, tid, smem_u32(&b_mma[(it - 1) & 1]), (u32)(((it - 1) >> 1) & 1), it >= 1);
+#if GFT_SMALL
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&b_rows[s]));   // release: small-leaf outputs in SMEM
+#endif
+    }
+  } else {
+    // ---------------- drainer (row = TMEM lane = tid - 128) ----------------
+    reg_drainer();
+    const int row = tid - 128;
+    const u32 lane_off = (u32)((warp - 4) * 32) << 16;
+    for (long long it = 0;; ++it) {
+      const long long p = pid0 + it * npid;
+      if (p >= npairs) break;
+      const int s = (int)(it % GFT_STAGES);
+      const int b = (int)(it & 1);
+      mbar_wait(smem_u32(&b_mma[b]), (u32)((it >> 1) & 1));
+      tc_fence_after();
+#if GFT_SMALL
+      mbar_wait(smem_u32(&b_rows[s]), (u32)((it / GFT_STAGES) & 1));
+#endif
+      unsigned char* buf = stages + s * GFT_TILE_BYTES;
+      float y[GFT_N];
+      gft_drain(y, tmem + lane_off + (u32)(GFT_A_COLS + b * GFT_D_COLS), buf, row);
+      // D[b] read (tcgen05.ld waited inside gft_drain): let the issuer reuse it
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(map_to_cta(smem_u32(&b_dfree[b]), 0));
+      gft_finish(y);
+      store_row(buf, row, y);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&b_done[s]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();   // the peer may still be reading our B half / arriving on our barriers
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(GFT_TMEM_COLS) : "memory");
+  }
+}

@@ -217,6 +217,38 @@ def test_tensor_core_single_cta_and_pair_variants_agree(monkeypatch):
     assert oracle.relative_error(pair.forward(Xd).cpu().numpy(), single.forward(Xd).cpu().numpy()).max() < 1e-6
 
 
+@pytest.mark.parametrize("inverse_small_leaf", [False, True])
+def test_tensor_core_kernel_variants_agree(monkeypatch, inverse_small_leaf):
+    """n = 64 plans through all four tcgen05 kernels: warp-specialised stager/drainer pair
+    kernel (default, kernel_tc3), two-warpgroup pair kernel (GFT_NO_TC_WS), one-warpgroup pair
+    kernel (+GFT_NO_TC_2WG) and single-CTA kernel (GFT_NO_CTA_PAIR) -- against the oracle and
+    each other.  The second case has a 24-node CUDA-core leaf beside a 40-node tensor-core
+    leaf (stager writes its outputs to SMEM for the drainer)."""
+    a, b = (24, 40) if inverse_small_leaf else (32, 32)
+    s, d, w, loops, _ = workloads.random_bipartite_graph(np.random.default_rng(a), a, b, density=0.3)
+    L = oracle.normalized_laplacian(oracle.laplacian(64, s, d, w, loops))
+    lam_o, U_o = oracle.gft_basis(L)
+    variants = [("tc3_", {}), ("tc2", {"GFT_NO_TC_WS": "1"}),
+                ("tc2_", {"GFT_NO_TC_WS": "1", "GFT_NO_TC_2WG": "1"}), ("tc_", {"GFT_NO_CTA_PAIR": "1"})]
+    X = torch.randn(1000, 64, generator=torch.Generator().manual_seed(5))   # 3 pair tiles + ragged
+    outs = []
+    for tag, env in variants:
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        plan = G.Plan(64, s, d, w, loops, dtypes=("f32",), normalized=True, no_cubin_cache=True)
+        for k in env:
+            monkeypatch.delenv(k)
+        assert tag in plan.kernel_name(G.K_FAST_FWD), (tag, plan.kernel_name(G.K_FAST_FWD))
+        Y = plan.forward(X.cuda())
+        Xr = plan.inverse(Y)
+        torch.cuda.synchronize()
+        check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
+        assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
+        outs.append(Y.cpu().numpy())
+    for o in outs[1:]:
+        assert oracle.relative_error(o, outs[0]).max() < 1e-6
+
+
 @pytest.mark.parametrize("name", ["cfg3", "cfg4"])
 def test_normalized_laplacian_gft(name):
     """GFT of D^{-1/2} L D^{-1/2} through the same fused kernels."""
