@@ -685,19 +685,21 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
           }
       }
     }
-    // warp-specialised pair kernel (stager / drainer, D double-buffered) when its TMEM layout
-    // and FOUR tile buffers fit: a buffer is held from TMA load through staging to the drain,
-    // so with 3 buffers only one tile of prefetch remains and the stager waits on HBM
-    // (measured: n = 64 +9% over the two-warpgroup kernel; n = 128 with 3 buffers -7% vs the
-    // plain pair kernel).  GFT_NO_TC_WS=1 keeps the plain pair kernel (ablation).
+    // warp-specialised pair kernel (stager / drainer, D double-buffered) for n <= 64 when its
+    // TMEM layout and FOUR tile buffers fit: a buffer is held from TMA load through staging to
+    // the drain, so with 3 buffers only one tile of prefetch remains and the stager waits on
+    // HBM.  Measured back to back (tools/gpu_ws_cmp.sh, gpu_ws_stages.sh): n = 64 +9-16% over
+    // the pair kernels; n = 80 a tie; n = 96 -5%; n = 128 (3 buffers) -7%; 5-6 buffers are
+    // slower than 4 at n = 64.  GFT_NO_TC_WS=1 keeps the plain pair kernel (ablation).
     bool ws = false;
     int ws_a = 0, ws_d = 0, ws_tmem = 0;
     std::vector<TcLeaf> Tws;
-    if (ok && pair && getenv("GFT_NO_TC_WS") == nullptr) {
+    if (ok && pair && P.n <= 64 && getenv("GFT_NO_TC_WS") == nullptr) {
       Tws = T;
       if (ws_layout(Tws, ws_a, ws_d, ws_tmem)) {
         const int tile = 128 * ((P.n + 31) / 32 * 32) * 4;
-        int st = 6;
+        const char* es = getenv("GFT_TC_WS_STAGES");   // experiment knob (default: measured 4)
+        int st = (es && *es) ? atoi(es) : 4;
         while (st >= 4 && st * tile + b_bytes + 2048 > 227 * 1024) --st;
         if (st >= 4) {
           ws = true;
