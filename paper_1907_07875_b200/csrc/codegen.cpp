@@ -709,12 +709,31 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
         }
       }
     }
+    // experiment (opt-in, GFT_TC_IOSPLIT=1): for n > 64 split input / output buffers -- 2
+    // input buffers released by the stager right after reading its rows, one output buffer
+    // drained by a storer warp (plans without CUDA-core leaves).  Faster than the pair kernel
+    // in isolation under ncu (cfg5b 183 vs 188 us) but 9% slower back to back (5.55 vs 6.08
+    // TB/s, with or without PDL; tools/gpu_iosplit_cmp.sh, gpu_pdl_ws.sh), so not the default.
+    bool io_split = false;
+    if (ok && pair && !ws && P.n > 64 && T.size() == P.leaves.size() && getenv("GFT_TC_IOSPLIT") != nullptr) {
+      Tws = T;
+      if (ws_layout(Tws, ws_a, ws_d, ws_tmem)) {
+        const int tile = 128 * ((P.n + 31) / 32 * 32) * 4;
+        if (3 * tile + b_bytes + 2048 <= 227 * 1024) {
+          ws = io_split = true;
+          stages = 2;
+          wgs = 1;
+          tmem_cols = ws_tmem;
+        }
+      }
+    }
     if (ok) {
       KernelCfg& c = k.cfg;
       c.tc = 1;
       c.tc_pair = pair ? 1 : 0;
       c.tc_wgs = wgs;
       c.tc_ws = ws ? 1 : 0;
+      c.tc_io_split = io_split ? 1 : 0;
       c.stages = stages;
       c.mode = 0;
       c.boxc = 32;
@@ -731,6 +750,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
       pre << "#define GFT_N " << c.n << "\n#define GFT_STAGES " << c.stages << "\n#define GFT_TMEM_COLS "
           << tmem_cols << "\n";
       if (wgs == 2) pre << "#define GFT_WGS 2\n#define GFT_WG_COLS " << wg_cols << "\n";
+      if (io_split) pre << "#define GFT_IO_SPLIT 1\n";
       const std::string skel(ws ? kSkeletonTC3 : pair ? kSkeletonTC2 : kSkeletonTC);
       const std::string marker = "// @@GFT_GENERATED@@";
       const size_t at = skel.find(marker);
@@ -738,7 +758,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
       const std::string key = pre.str() + gen.str() + skel;
       char hbuf[32];
       std::snprintf(hbuf, sizeof hbuf, "%016llx", (unsigned long long)fnv1a(key));
-      k.name = std::string("gft_") + kKindNameTC[kind] + (ws ? "3" : pair ? (wgs == 2 ? "2w" : "2") : "") + "_f32_n" + std::to_string(c.n) + "_" + hbuf;
+      k.name = std::string("gft_") + kKindNameTC[kind] + (ws ? (io_split ? "3s" : "3") : pair ? (wgs == 2 ? "2w" : "2") : "") + "_f32_n" + std::to_string(c.n) + "_" + hbuf;
       std::ostringstream src;
       src << "// generated by paper_1907_07875_b200 codegen.cpp — plan-specialised GFT kernel with\n"
           << "// tcgen05 3xTF32 leaves (" << T.size() << " tensor-core leaves)\n"

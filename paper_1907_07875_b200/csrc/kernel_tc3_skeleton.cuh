@@ -166,17 +166,26 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   extern __shared__ unsigned char smem_raw[];
   const u32 raw_s = smem_u32(smem_raw);
   unsigned char* smem = smem_raw + ((1024u - (raw_s & 1023u)) & 1023u);
+#ifndef GFT_IO_SPLIT
+#define GFT_IO_SPLIT 0
+#endif
+  // GFT_IO_SPLIT: input ring of GFT_STAGES buffers released by the stager as soon as its rows
+  // are in registers, plus ONE output buffer the drainer fills and a storer warp drains
   unsigned char* stages = smem;
-  unsigned char* bsm = smem + GFT_STAGES * GFT_TILE_BYTES;            // this CTA's half of B
+  unsigned char* outbuf = smem + GFT_STAGES * GFT_TILE_BYTES;
+  unsigned char* bsm = smem + (GFT_STAGES + GFT_IO_SPLIT) * GFT_TILE_BYTES;   // this CTA's half of B
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(bsm + GFT_B_FLOATS * 4);
-  // bars: full[S], done[S], rows[S], staged, mma_done[2], d_free[2]
+  // bars: full[S], done[S] (= input free when IO-split), rows[S], staged, mma_done[2],
+  // d_free[2], out_ready, out_free
   unsigned long long* b_full = bars;
   unsigned long long* b_done = bars + GFT_STAGES;
   unsigned long long* b_rows = bars + 2 * GFT_STAGES;
   unsigned long long* b_staged = bars + 3 * GFT_STAGES;
   unsigned long long* b_mma = bars + 3 * GFT_STAGES + 1;
   unsigned long long* b_dfree = bars + 3 * GFT_STAGES + 3;
-  u32* tmem_slot = reinterpret_cast<u32*>(bars + 3 * GFT_STAGES + 5);
+  unsigned long long* b_outrdy = bars + 3 * GFT_STAGES + 5;
+  unsigned long long* b_outfree = bars + 3 * GFT_STAGES + 6;
+  u32* tmem_slot = reinterpret_cast<u32*>(bars + 3 * GFT_STAGES + 7);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const u32 rank = cluster_rank();
   const long long npairs = (batch + 2 * GFT_TILE_ROWS - 1) / (2 * GFT_TILE_ROWS);
@@ -201,6 +210,8 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       mbar_init(smem_u32(&b_mma[b]), 1);
       mbar_init(smem_u32(&b_dfree[b]), 8);
     }
+    mbar_init(smem_u32(b_outrdy), 4);
+    mbar_init(smem_u32(b_outfree), 1);
     fence_mbar_init();
   }
   const float4* bsrc = reinterpret_cast<const float4*>(gft_tcB[rank]);
@@ -217,6 +228,38 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
 
   if (warp >= 8) {
     reg_control();
+#if GFT_IO_SPLIT
+    if (warp == 8 && lane == 0) {
+      // ---------------- loader: input ring, refilled as soon as the stager has read a tile ----
+      for (long long it = 0;; ++it) {
+        const long long p = pid0 + it * npid;
+        if (p >= npairs) break;
+        const long long row0 = p * 2 * GFT_TILE_ROWS + rank * GFT_TILE_ROWS;
+        const int s = (int)(it % GFT_STAGES);
+        if (it >= GFT_STAGES) mbar_wait(smem_u32(&b_done[s]), (u32)(((it / GFT_STAGES) - 1) & 1));
+        const u32 bar = smem_u32(&b_full[s]);
+        const u32 dst = smem_u32(stages + s * GFT_TILE_BYTES);
+        mbar_expect_tx(bar, GFT_TILE_BYTES);
+        for (int b = 0; b < GFT_NBOX; ++b)
+          tma_load_2d(dst + b * GFT_BOX_BYTES, &tin, b * GFT_BOXC, (int)row0, bar);
+      }
+    } else if (warp == 10 && lane == 0) {
+      // ---------------- storer: the output buffer -> HBM, then hand it back to the drainer ----
+      for (long long it = 0;; ++it) {
+        const long long p = pid0 + it * npid;
+        if (p >= npairs) break;
+        const long long row0 = p * 2 * GFT_TILE_ROWS + rank * GFT_TILE_ROWS;
+        mbar_wait(smem_u32(b_outrdy), (u32)(it & 1));
+        const u32 src = smem_u32(outbuf);
+        for (int b = 0; b < GFT_NBOX; ++b)
+          tma_store_2d(&tout, b * GFT_BOXC, (int)row0, src + b * GFT_BOX_BYTES);
+        bulk_commit();
+        bulk_wait_read0();
+        mbar_arrive(smem_u32(b_outfree));
+      }
+      bulk_wait_all();
+    } else
+#endif
     if (warp == 8 && lane == 0) {
       // ---------------- producer / storer of this CTA's 128 rows per pair tile ----------------
       long long it = 0;
@@ -281,6 +324,10 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       unsigned char* buf = stages + s * GFT_TILE_BYTES;
       float x[GFT_N];
       load_row(buf, tid, x);
+#if GFT_IO_SPLIT
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&b_done[s]));   // input rows consumed: refill
+#endif
       // before writing the A columns: the MMAs of the previous tile have read them
       gft_stage(x, tm_a, staged0, buf, tid, smem_u32(&b_mma[(it - 1) & 1]), (u32)(((it - 1) >> 1) & 1), it >= 1);
 #if GFT_SMALL
@@ -303,7 +350,12 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
 #if GFT_SMALL
       mbar_wait(smem_u32(&b_rows[s]), (u32)((it / GFT_STAGES) & 1));
 #endif
+#if GFT_IO_SPLIT
+      unsigned char* buf = outbuf;
+      if (it >= 1) mbar_wait(smem_u32(b_outfree), (u32)((it - 1) & 1));   // store has read it
+#else
       unsigned char* buf = stages + s * GFT_TILE_BYTES;
+#endif
       float y[GFT_N];
       gft_drain(y, tmem + lane_off + (u32)(GFT_A_COLS + b * GFT_D_COLS), buf, row);
       // D[b] read (tcgen05.ld waited inside gft_drain): let the issuer reuse it
@@ -314,7 +366,11 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       store_row(buf, row, y);
       fence_proxy_async();
       __syncwarp();
+#if GFT_IO_SPLIT
+      if (lane == 0) mbar_arrive(smem_u32(b_outrdy));
+#else
       if (lane == 0) mbar_arrive(smem_u32(&b_done[s]));
+#endif
     }
   }
   tc_fence_before();

@@ -368,3 +368,20 @@ def test_two_sparse_eigenvector_graphs_on_gpu(kind, n, dtype):
     torch.cuda.synchronize()
     check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), TOL[dtype])
     assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL[dtype]
+
+
+def test_tensor_core_io_split_experiment(monkeypatch):
+    """The opt-in IO-split warp-specialised kernel (GFT_TC_IOSPLIT=1, n > 64, all leaves on
+    the tensor core) stays correct: cfg5b forward / inverse vs the oracle."""
+    cfg = workloads.config("cfg5b")
+    monkeypatch.setenv("GFT_TC_IOSPLIT", "1")
+    plan = G.Plan.from_config(cfg, dtypes=("f32",), no_cubin_cache=True)
+    monkeypatch.delenv("GFT_TC_IOSPLIT")
+    assert "tc3s_" in plan.kernel_name(G.K_FAST_FWD)
+    lam_o, U_o = oracle_basis("cfg5b")
+    X = workloads.signals(cfg, batch=1000, dtype="f32")
+    Y = plan.forward(X.cuda())
+    Xr = plan.inverse(Y)
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
