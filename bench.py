@@ -187,6 +187,9 @@ def config_table(args, stream, hbm, device):
                                      "signals_per_s": cfg.batch / ms * 1e3}
         if cfg.batch * cfg.n * esz <= (64 << 20):   # small workloads: launch-bound, replay a graph
             row["fast_fwd"]["graph_ms"] = round(time_graph(lambda: plan.forward(X, Y), 50), 5)
+            # the forward -> inverse pair, also from a graph
+            Z1 = torch.empty_like(X)
+            row["fwd_inv_pair_graph_ms"] = round(time_graph(lambda: (plan.forward(X, Y), plan.inverse(Y, Z1)), 50), 5)
         # the dense kernel is FMA-issue-bound for n >= 64: its fraction of the lane-FMA peak
         row["dense_fwd"]["fma_frac"] = round(cfg.n * cfg.n * cfg.batch / (row["dense_fwd"]["ms"] * 1e-3)
                                              / fma_peak_per_s(dtype), 4)
