@@ -46,7 +46,10 @@ KernelCfg choose_cfg(int n, int dtype, int64_t work) {
     else if (row % 32 == 0) { c.boxc = 32 / c.elem; c.swz_mask = 1; }
     else { c.boxc = n; c.swz_mask = 0; }   // 16*odd bytes: odd chunk pitch, conflict-free
   } else {
-    c.mode = 1;
+    // unaligned row pitch: 1-D bulk copies of whole tiles.  Opt-in (GFT_SUPERROW=1): TMA
+    // tensor copies of the 4-signal super-row view (4n <= 256) -- parity-tested but 3% slower
+    // on cfg3 (5.79 vs 5.95 TB/s back to back, tools/gpu_superrow_cmp.sh)
+    c.mode = (4 * n <= 256 && getenv("GFT_SUPERROW") != nullptr) ? 2 : 1;
     c.boxc = n;
     c.swz_mask = 0;
     // odd row pitch in vector units makes thread-per-row accesses conflict-free

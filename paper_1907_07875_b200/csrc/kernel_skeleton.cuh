@@ -11,6 +11,11 @@
 //   GFT_STAGES    SMEM tiles per warp (loads in flight = GFT_STAGES-1)
 //   GFT_MODE      0: TMA tensor 2-D copies with hardware swizzle (n*sizeof(elem) % 16 == 0)
 //                 1: 1-D bulk copies of whole tiles, unpadded rows (odd n etc.)
+//                 2: rows whose pitch is not 16-byte aligned, as TMA tensor copies of a 2-D
+//                    "super-row" view [batch/4, 4n] (4 signals per super-row: 16-byte pitch),
+//                    no swizzle -- the same unpadded SMEM tile as mode 1, but the TMA tensor
+//                    engine instead of the 1-D bulk copy; a tail of batch % 4 signals takes
+//                    the direct path
 //   GFT_BOXC      columns per TMA box (mode 0); n % GFT_BOXC == 0
 //   GFT_SWZ_MASK  7 / 3 / 1 / 0 for 128B / 64B / 32B / no swizzle (mode 0)
 //   GFT_VEC       elements per SMEM vector access (16, 8 or 4/8 bytes)
@@ -63,7 +68,7 @@ static __device__ __forceinline__ void bulk_wait_read() {
 }
 static __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-#if GFT_MODE == 0
+#if GFT_MODE != 1
 static __device__ __forceinline__ void tma_load_2d(u32 dst, const TmaDesc* desc, int c0, int c1, u32 bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
@@ -73,7 +78,8 @@ static __device__ __forceinline__ void tma_store_2d(const TmaDesc* desc, int c0,
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
                :: "l"((u64)desc), "r"(c0), "r"(c1), "r"(src) : "memory");
 }
-#else
+#endif
+#if GFT_MODE == 1
 static __device__ __forceinline__ void bulk_load(u32 dst, const void* src, u32 bytes, u32 bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
@@ -152,6 +158,8 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   auto is_direct = [&](long long t) -> bool {
 #if GFT_MODE == 1
     return (t + 1) * GFT_TILE_ROWS > batch;
+#elif GFT_MODE == 2
+    return (batch & 3) != 0 && (t + 1) * GFT_TILE_ROWS > (batch & ~3ll);
 #else
     (void)t;
     return false;
@@ -165,6 +173,8 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
 #pragma unroll
     for (int b = 0; b < GFT_NBOX; ++b)
       tma_load_2d(dst + b * GFT_BOX_BYTES, &tin, b * GFT_BOXC, (int)(t * GFT_TILE_ROWS), bar);
+#elif GFT_MODE == 2
+    tma_load_2d(dst, &tin, 0, (int)(t * (GFT_TILE_ROWS / 4)), bar);
 #else
     bulk_load(dst, reinterpret_cast<const unsigned char*>(X) + (size_t)t * GFT_TILE_BYTES,
               GFT_TILE_BYTES, bar);
@@ -176,6 +186,8 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
 #pragma unroll
     for (int b = 0; b < GFT_NBOX; ++b)
       tma_store_2d(&tout, b * GFT_BOXC, (int)(t * GFT_TILE_ROWS), src + b * GFT_BOX_BYTES);
+#elif GFT_MODE == 2
+    tma_store_2d(&tout, 0, (int)(t * (GFT_TILE_ROWS / 4)), src);
 #else
     bulk_store(reinterpret_cast<unsigned char*>(Y) + (size_t)t * GFT_TILE_BYTES, src, GFT_TILE_BYTES);
 #endif

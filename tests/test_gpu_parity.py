@@ -385,3 +385,21 @@ def test_tensor_core_io_split_experiment(monkeypatch):
     torch.cuda.synchronize()
     check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
     assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
+
+
+@pytest.mark.parametrize("batch", [1, 3, 4, 130, 1001])
+def test_superrow_tma_mode_experiment(monkeypatch, batch):
+    """Opt-in super-row TMA mode for odd row pitch (GFT_SUPERROW=1): cfg3 with batches
+    that are / are not multiples of 4 (the batch % 4 tail takes the direct path)."""
+    cfg = workloads.config("cfg3")
+    monkeypatch.setenv("GFT_SUPERROW", "1")
+    plan = G.Plan.from_config(cfg, dtypes=("f32",), no_cubin_cache=True)
+    monkeypatch.delenv("GFT_SUPERROW")
+    assert "#define GFT_MODE 2" in plan.kernel_source(G.K_FAST_FWD, "f32")
+    lam_o, U_o = oracle_basis("cfg3")
+    X = workloads.signals(cfg, batch=batch, dtype="f32")
+    Y = plan.forward(X.cuda())
+    Xr = plan.inverse(Y)
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
