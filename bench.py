@@ -388,6 +388,7 @@ def run_reference(args):
         return 0
     import workloads
     cfg = workloads.config(args.config)
+    n_ = cfg.n
     rows = min(cfg.batch, args.ref_rows)
     X = workloads.signals(cfg, batch=rows, dtype="f32")
     import oracle
@@ -405,7 +406,12 @@ def run_reference(args):
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "signals/s",
            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": {"workload": args.config, "batch": rows, "n": cfg.n},
+           "data": "synthetic",
+           "config": {"workload": "%s: %s" % (args.config, cfg.description), "n": n_,
+                      "global_batch": cfg.batch * ws, "per_gpu_batch": cfg.batch,
+                      "step": "dense fp64 forward + inverse GFT (the oracle), timed on a bounded "
+                              "sample of %d rows per step" % rows,
+                      "parallelism": "rank 0 only (CPU)"},
            "cpu_baseline": {"value": value, "unit": "signals/s", "cores": cores, "kind": "oracle",
                             "sample": "%d of %d rows of %s, dense fp64 Y=XU then X=YU^T (numpy BLAS)"
                                       % (rows, cfg.batch, args.config)},
