@@ -197,9 +197,18 @@ void emit_leaf_givens(std::ostringstream& o, const Leaf& lf, size_t l, Dir d, in
   o << "  (void)a_; }\n";
 }
 
-void emit_leaf_fma(std::ostringstream& o, const Leaf& lf, size_t l, Dir d, int dtype) {
+// stream: every leaf output goes straight to this thread's SMEM row (SOUT) instead of a y
+// register, so only the input row is live during the leaves (wide rows, see generate_kernel)
+std::string sout(int idx) { return "SOUT(" + std::to_string(idx) + ")"; }
+
+void emit_leaf_fma(std::ostringstream& o, const Leaf& lf, size_t l, Dir d, int dtype, bool stream = false) {
   if (lf.approx && d != DIR_FILTER) {   // the fused filter keeps F = M^T diag(h) M dense
     emit_leaf_givens(o, lf, l, d, dtype);
+    if (stream)
+      for (int r = 0; r < lf.k; ++r) {
+        const int oi = out_idx(lf, d, r);
+        o << "  " << sout(oi) << " = y[" << oi << "];\n";
+      }
     return;
   }
   o << "  // ---- leaf " << l << " (k=" << lf.k << ")\n";
@@ -208,7 +217,8 @@ void emit_leaf_fma(std::ostringstream& o, const Leaf& lf, size_t l, Dir d, int d
   for (int r = 0; r < lf.k; ++r) {
     std::vector<double> coef(lf.k);
     for (int i = 0; i < lf.k; ++i) coef[i] = leaf_coef(lf, d, r, i);
-    emit_dot(o, xs("y", out_idx(lf, d, r)), coef, in, dtype);
+    const int oi = out_idx(lf, d, r);
+    emit_dot(o, stream ? sout(oi) : xs("y", oi), coef, in, dtype);
   }
 }
 
@@ -230,16 +240,20 @@ void emit_post_units(std::ostringstream& o, const Plan& P, const char* arr, bool
   o << "  (void)a_; (void)b_; }\n";
 }
 
-void emit_fast(std::ostringstream& o, const Plan& P, int dtype, Dir d) {
+void emit_fast(std::ostringstream& o, const Plan& P, int dtype, Dir d, bool stream = false) {
   if (d == DIR_FILTER && !P.post.empty()) fail(GFT_ERR_COMPILE, "filter plan with right Haar stages");
+  if (stream) o << "  elem_t y[GFT_N];\n";
   if (d != DIR_INV) emit_units_elem(o, P, "x", false, dtype);
   if (d == DIR_INV) emit_post_units(o, P, "x", true, "elem_t");
-  for (size_t l = 0; l < P.leaves.size(); ++l) emit_leaf_fma(o, P.leaves[l], l, d, dtype);
+  for (size_t l = 0; l < P.leaves.size(); ++l) emit_leaf_fma(o, P.leaves[l], l, d, dtype, stream);
+  const bool after = (d == DIR_FWD && !P.post.empty()) || (d != DIR_FWD && !P.ops.empty());
+  if (stream && after) o << "  load_row(buf_, row_, y);   // leaf outputs back for the stages after the leaves\n";
   if (d == DIR_FWD) emit_post_units(o, P, "y", false, "elem_t");
   if (d != DIR_FWD) emit_units_elem(o, P, "y", true, dtype);
+  if (stream && after) o << "  store_row(buf_, row_, y);\n";
 }
 
-void emit_dense(std::ostringstream& o, const Plan& P, int dtype, bool forward) {
+void emit_dense(std::ostringstream& o, const Plan& P, int dtype, bool forward, bool stream = false) {
   const int n = P.n;
   std::vector<std::string> in(n);
   for (int i = 0; i < n; ++i) in[i] = xs("x", i);
@@ -247,7 +261,7 @@ void emit_dense(std::ostringstream& o, const Plan& P, int dtype, bool forward) {
     std::vector<double> coef(n);
     for (int i = 0; i < n; ++i)
       coef[i] = forward ? P.U[(size_t)i * n + k] : P.U[(size_t)k * n + i];
-    emit_dot(o, xs("y", k), coef, in, dtype);
+    emit_dot(o, stream ? sout(k) : xs("y", k), coef, in, dtype);
   }
 }
 
@@ -773,13 +787,29 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
   }
   const KernelCfg& c = k.cfg;
   std::ostringstream body;
-  body << "static __device__ __forceinline__ void gft_body(elem_t (&x)[GFT_N], elem_t (&y)[GFT_N]) {\n";
+  // wide rows stream their leaf outputs to SMEM instead of holding a y row in registers:
+  // only when x + y would be far beyond the register file (2 n words > 320, e.g. f64 n > 80:
+  // a 96-node f64 leaf spills 692 B/thread otherwise, none streamed); at 2 n words = 256
+  // (cfg4 f64, cfg5b dense) the register version is faster (6.31 vs 6.10 TB/s, cfg4 f64
+  // forward; tools/gpu_stream_cmp.sh).  GFT_STREAM=0/1 forces it (experiments)
+  const int words = c.elem / 4;
+  bool stream = 2 * c.n * words > 320;
+  if (const char* e = getenv("GFT_STREAM")) stream = e[0] == '1';
+  if (stream)
+    body << "#define GFT_STREAM 1\n"
+            "static __device__ __forceinline__ unsigned int tile_off(int row, int col);\n"
+            "static __device__ __forceinline__ void load_row(const unsigned char* buf, int row, elem_t (&x)[GFT_N]);\n"
+            "static __device__ __forceinline__ void store_row(unsigned char* buf, int row, const elem_t (&y)[GFT_N]);\n"
+            "#define SOUT(c) (*reinterpret_cast<elem_t*>(buf_ + tile_off(row_, (c))))\n"
+            "static __device__ __forceinline__ void gft_body(elem_t (&x)[GFT_N], unsigned char* buf_, int row_) {\n";
+  else
+    body << "static __device__ __forceinline__ void gft_body(elem_t (&x)[GFT_N], elem_t (&y)[GFT_N]) {\n";
   switch (kind) {
     case K_FAST_FWD:
     case K_FAST_INV:
-    case K_FILTER: emit_fast(body, P, dtype, dir); break;
-    case K_DENSE_FWD: emit_dense(body, P, dtype, true); break;
-    case K_DENSE_INV: emit_dense(body, P, dtype, false); break;
+    case K_FILTER: emit_fast(body, P, dtype, dir, stream); break;
+    case K_DENSE_FWD: emit_dense(body, P, dtype, true, stream); break;
+    case K_DENSE_INV: emit_dense(body, P, dtype, false, stream); break;
     default: fail(GFT_ERR_INVALID_ARG, "bad kernel kind");
   }
   body << "}\n";

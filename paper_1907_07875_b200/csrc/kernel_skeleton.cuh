@@ -217,10 +217,16 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
 #pragma unroll 1
       for (int r = 0; r < GFT_R; ++r) {
         const int row = lane + 32 * r;
+#if defined(GFT_STREAM)
+        elem_t x[GFT_N];
+        load_row(buf, row, x);
+        gft_body(x, buf, row);   // outputs written to the row by the generated code
+#else
         elem_t x[GFT_N], y[GFT_N];
         load_row(buf, row, x);
         gft_body(x, y);
         store_row(buf, row, y);
+#endif
       }
       fence_proxy_async();
       __syncwarp();
@@ -239,12 +245,24 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       for (int r = 0; r < GFT_R; ++r) {
         const long long g = t * GFT_TILE_ROWS + lane + 32 * r;
         if (g < batch) {
+#if defined(GFT_STREAM)
+          // the tile's SMEM slot is unused by a direct tile: outputs go through this row
+          unsigned char* sbuf = wbuf + s * GFT_TILE_BYTES;
+          const int row = lane + 32 * r;
+          elem_t x[GFT_N];
+#pragma unroll
+          for (int c = 0; c < GFT_N; ++c) x[c] = X[g * GFT_N + c];
+          gft_body(x, sbuf, row);
+#pragma unroll
+          for (int c = 0; c < GFT_N; ++c) Y[g * GFT_N + c] = *reinterpret_cast<const elem_t*>(sbuf + tile_off(row, c));
+#else
           elem_t x[GFT_N], y[GFT_N];
 #pragma unroll
           for (int c = 0; c < GFT_N; ++c) x[c] = X[g * GFT_N + c];
           gft_body(x, y);
 #pragma unroll
           for (int c = 0; c < GFT_N; ++c) Y[g * GFT_N + c] = y[c];
+#endif
         }
       }
     }

@@ -403,3 +403,34 @@ def test_superrow_tma_mode_experiment(monkeypatch, batch):
     torch.cuda.synchronize()
     check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
     assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
+
+
+@pytest.mark.parametrize("case", ["wide_f64_leaf", "forced_cfg4_f64"])
+def test_streamed_leaf_outputs(monkeypatch, case):
+    """Wide rows write leaf outputs straight to SMEM (no y register row): a 96-node f64 leaf
+    (automatic), and cfg4 f64 with GFT_STREAM=1 (inverse: outputs reloaded for the reverse
+    butterflies) -- both against the oracle, with a ragged batch."""
+    if case == "wide_f64_leaf":
+        rng = np.random.default_rng(3)
+        n = 96
+        pairs = [(i, j) for i in range(n) for j in range(i + 1, n) if rng.random() < 0.1]
+        s = np.array([p[0] for p in pairs], np.int32)
+        d = np.array([p[1] for p in pairs], np.int32)
+        w = rng.uniform(0.5, 2.0, len(pairs))
+        plan = G.Plan(n, s, d, w, dtypes=("f64",))
+        L = oracle.laplacian(n, s, d, w)
+        lam_o, U_o = oracle.gft_basis(L)
+    else:
+        cfg = workloads.config("cfg4")
+        monkeypatch.setenv("GFT_STREAM", "1")
+        plan = G.Plan.from_config(cfg, dtypes=("f64",), no_cubin_cache=True)
+        monkeypatch.delenv("GFT_STREAM")
+        n = cfg.n
+        lam_o, U_o = oracle_basis("cfg4")
+    assert "GFT_STREAM" in plan.kernel_source(G.K_FAST_FWD, "f64")
+    X = torch.randn(1001, n, generator=torch.Generator().manual_seed(2), dtype=torch.float64)
+    Y = plan.forward(X.cuda())
+    Xr = plan.inverse(Y)
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-12)
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-12
