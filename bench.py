@@ -373,6 +373,37 @@ def cpu_oracle_step_time(cfg, X_cpu, budget_s):
     return min(times), statistics.median(times), reps, t_eig
 
 
+def cpu_oracle_one_thread(cfg, X_cpu):
+    """The same oracle step on one BLAS thread (T = nproc and T = 1)."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:
+        return None
+    import oracle
+    L = oracle.laplacian(cfg.n, cfg.src, cfg.dst, cfg.w, cfg.self_loops)
+    lam, U = oracle.gft_basis(L)
+    Xn = X_cpu.numpy()
+    best = None
+    with threadpool_limits(limits=1):
+        for _ in range(3):
+            t = time.perf_counter()
+            oracle.inverse(oracle.forward(Xn, U), U)
+            dt = time.perf_counter() - t
+            best = dt if best is None else min(best, dt)
+    return best
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -454,7 +485,10 @@ def main():
 
     cfg = workloads.config(args.config)
     dtype = cfg.dtypes[0]
+    t_plan = time.perf_counter()
     plan = gft.Plan.from_config(cfg, dtypes=(dtype,))
+    plan.compile(dtype, kinds=(0, 1))   # host plan + kernel load (AOT cubin or NVRTC), reported
+    plan_ms = (time.perf_counter() - t_plan) * 1e3
     # weak scaling: every rank transforms its own full batch (seed offset by rank)
     X_cpu = workloads.signals(cfg, dtype=dtype, seed=cfg.seed + rank)
     X = X_cpu.to(device)
@@ -502,8 +536,10 @@ def main():
         plan.inverse(Y, Z, stream)
         c.record(stream)
     torch.cuda.synchronize()
-    fwd_ev = sum(ev[i][0].elapsed_time(ev[i][1]) for i in range(nsh)) / nsh
-    inv_ev = sum(ev[i][1].elapsed_time(ev[i][2]) for i in range(nsh)) / nsh
+    fwd_all = sorted(ev[i][0].elapsed_time(ev[i][1]) for i in range(nsh))
+    inv_all = sorted(ev[i][1].elapsed_time(ev[i][2]) for i in range(nsh))
+    fwd_ev = sum(fwd_all) / nsh
+    inv_ev = sum(inv_all) / nsh
     # kernel time inside the timed region = step time x the kernel's share of the step
     fwd_ms = ms_step * fwd_ev / (fwd_ev + inv_ev)
     inv_ms = ms_step * inv_ev / (fwd_ev + inv_ev)
@@ -570,7 +606,12 @@ def main():
         best, med, reps, t_eig = cpu_oracle_step_time(cfg, X_cpu, args.cpu_budget)
         cpu = {"value": B / best, "unit": "signals/s", "cores": blas_threads(), "kind": "oracle",
                "sample": "full %s batch (%d x %d), oracle dense fp64 forward+inverse, best of %d "
-                         "(median %.3fs); eigensolve %.3fs excluded" % (args.config, B, n, reps, med, t_eig)}
+                         "(median %.3fs); eigensolve %.3fs excluded" % (args.config, B, n, reps, med, t_eig),
+               "cpu_model": cpu_model()}
+        one = cpu_oracle_one_thread(cfg, X_cpu[: B // 8])
+        if one is not None:
+            cpu["one_thread_value"] = (B // 8) / one
+            cpu["one_thread_sample"] = "first %d rows (1/8 of the batch), same oracle, 1 BLAS thread" % (B // 8)
 
     if dist:
         dist.barrier()
@@ -596,7 +637,10 @@ def main():
             "gpu_launches": 2 * args.steps,
             "kernels": {"fast_fwd_ms": round(fwd_ms, 5), "fast_inv_ms": round(inv_ms, 5),
                         "dense_fwd_ms": round(dense_fwd, 5), "dense_inv_ms": round(dense_inv, 5),
-                        "fast_vs_dense": round((dense_fwd + dense_inv) / (fwd_ms + inv_ms), 3)},
+                        "fast_vs_dense": round((dense_fwd + dense_inv) / (fwd_ms + inv_ms), 3),
+                        "event_bracketed_fwd_ms_median_min": [round(fwd_all[nsh // 2], 5), round(fwd_all[0], 5)],
+                        "event_bracketed_inv_ms_median_min": [round(inv_all[nsh // 2], 5), round(inv_all[0], 5)],
+                        "plan_create_and_load_ms": round(plan_ms, 1)},
             "clocks": clocks,
             "configs_table": table,
             "right_haar_table": rh_table,

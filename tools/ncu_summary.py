@@ -32,6 +32,12 @@ METRICS = [
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
     ("smsp__inst_executed.sum", "instructions"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall long_sb/issue"),
+    ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall wait/issue"),
+    ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall barrier/issue"),
+    ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio", "stall short_sb/issue"),
+    ("smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio", "stall no_instr/issue"),
+    ("launch__stack_size", "stack (spill) B"),
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
 ]
