@@ -37,7 +37,7 @@ METRICS = [
     ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall barrier/issue"),
     ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio", "stall short_sb/issue"),
     ("smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio", "stall no_instr/issue"),
-    ("launch__stack_size", "stack (spill) B"),
+    ("launch__stack_size", "launch stack B (default 1024)"),
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
 ]
