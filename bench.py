@@ -167,9 +167,13 @@ def config_table(args, stream, hbm, device):
     import workloads
     from paper_1907_07875_b200 import gft
     rows = []
-    for name, dtype in (("cfg1", "f32"), ("cfg2", "f32"), ("cfg2b", "f32"), ("cfg3", "f32"),
-                        ("cfg4", "f32"), ("cfg4", "f64"), ("cfg5a", "f32"), ("cfg5b", "f32")):
-        cfg = workloads.config(name)
+    for name, dtype in (("cfg1", "f32"), ("cfg1@2^24", "f32"), ("cfg2", "f32"), ("cfg2b", "f32"),
+                        ("cfg3", "f32"), ("cfg4", "f32"), ("cfg4", "f64"), ("cfg5a", "f32"), ("cfg5b", "f32")):
+        # cfg1@2^24: SURVEY §8(d)'s optional extra -- the N = 8 line graph at 2^24 signals, a
+        # bandwidth point for the smallest graph (cfg1 itself is launch-bound)
+        cfg = workloads.config(name.split("@")[0])
+        if "@" in name:
+            cfg.batch = 1 << 24
         plan = gft.Plan.from_config(cfg, dtypes=(dtype,))
         tdt = torch.float64 if dtype == "f64" else torch.float32
         g = torch.Generator(device=device).manual_seed(cfg.seed)
