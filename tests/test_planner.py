@@ -392,3 +392,33 @@ def test_tree_search_rescues_large_random_tree():
     plan = G.Plan(90, s, d, w, host_only=True, search_budget=1000)
     assert plan.info()["n_units"] > 0
     check_basis_against_oracle(90, s, d, w, None, plan)
+
+
+def test_tab_runtime_grid_counts_reproduced():
+    """tab:runtime rows for the 6-connected bi-diagonal grid and the z-shaped grid
+     with the graphs of reading R-5 and the paper's own first involutions
+    (diagonal symmetry; centrosymmetry i -> N+1-i): adds exact on
+    all four rows, paper-convention mults (A-23) exact on three; the 4x4 bi-diagonal grid
+    splits into sub-GFTs of length 6, 4, 4 and 2 exactly as PAPER.md:679 states.  The 4x4
+    z-grid prints 112 mults where Sigma k^2 = 2 * 8^2 = 128 (its figure is not available to
+    check which entries the paper did not count)."""
+    rows = {(r[0], int(r[1])): r for r in read_golden("tab_runtime_opcounts.txt")[0]}
+    for topo, f in (("grid6", workloads.bidiag_grid), ("zgrid", workloads.z_grid)):
+        for N in (4, 8):
+            n = N * N
+            s, d, w = f(N)
+            if topo == "grid6":
+                phi = np.array([N * (i % N) + i // N for i in range(n)], np.int32)
+            else:
+                phi = np.array([n - 1 - i for i in range(n)], np.int32)
+            plan = G.Plan(n, s, d, w, None, phi, host_only=True)
+            info = plan.info()
+            _, _, madd, mmul, fadd, fmul = rows[(topo, n)]
+            assert info["dense_adds"] == int(madd) and info["dense_mults"] == int(mmul)
+            assert info["adds"] == int(fadd), (topo, n, info["adds"], fadd)
+            if (topo, n) != ("zgrid", 16):
+                assert info["paper_mults"] == int(fmul), (topo, n, info["paper_mults"], fmul)
+            if (topo, n) == ("grid6", 16):
+                assert sorted(plan.leaf_sizes()) == [2, 4, 4, 6]
+            # the 8x8 z-grid has eigenvalue gaps down to 1e-5: eigenvector error ~ eps |L| / gap
+            check_basis_against_oracle(n, s, d, w, None, plan, atol=1e-8)
