@@ -434,3 +434,41 @@ def test_streamed_leaf_outputs(monkeypatch, case):
     torch.cuda.synchronize()
     check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-12)
     assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-12
+
+
+@pytest.mark.parametrize("case", ["n1", "n2", "edgeless5", "loops_only4", "negative6", "n256_host_only"])
+def test_degenerate_graphs(case):
+    """Degenerate inputs through the C ABI: 1- and 2-node graphs, no edges (L = 0: the GFT is
+    the identity up to order), self-loops only (L diagonal), negative weights (L not PSD), and
+    n = 256 planned host-only (the largest n with kernels is 256)."""
+    if case == "n256_host_only":
+        s, d, w = workloads.cycle_graph(256)
+        plan = G.Plan(256, s, d, w, host_only=True)
+        assert plan.info()["units_per_level"][0] == 128
+        lam = plan.eigenvalues()
+        assert np.abs(np.sort(lam) - np.sort(2 - 2 * np.cos(2 * np.pi * np.arange(256) / 256))).max() < 1e-10
+        return
+    e = np.zeros(0, np.int32)
+    if case == "n1":
+        n, s, d, w, loops = 1, e, e, np.zeros(0), np.array([0.7])
+    elif case == "n2":
+        n, s, d, w, loops = 2, np.array([0], np.int32), np.array([1], np.int32), np.array([1.5]), None
+    elif case == "edgeless5":
+        n, s, d, w, loops = 5, e, e, np.zeros(0), None
+    elif case == "loops_only4":
+        n, s, d, w, loops = 4, e, e, np.zeros(0), np.array([0.5, 2.0, 1.0, 3.0])
+    else:
+        n = 6
+        s, d, w = workloads._edges([(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (0, 5), (1, 4)],
+                                   [1.0, -0.5, 2.0, -0.5, 1.0, 0.7, -1.2])
+        loops = None
+    for dtype in ("f32", "f64"):
+        plan = G.Plan(n, s, d, w, loops, dtypes=(dtype,))
+        L = oracle.laplacian(n, s, d, w, loops)
+        lam_o, U_o = oracle.gft_basis(L)
+        X = torch.randn(65, n, generator=torch.Generator().manual_seed(n), dtype=TDT[dtype])
+        Y = plan.forward(X.cuda())
+        Xr = plan.inverse(Y)
+        torch.cuda.synchronize()
+        check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), TOL[dtype])
+        assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL[dtype]
