@@ -367,9 +367,9 @@ struct Builder {
             std::vector<double> v = comp(j, S, 1.0);
             for (const auto& u : basis) {   // Gram-Schmidt (twice for stability)
               for (int rep = 0; rep < 2; ++rep) {
-                double d = 0;
-                for (size_t t = 0; t < v.size(); ++t) d += v[t] * u[t];
-                for (size_t t = 0; t < v.size(); ++t) v[t] -= d * u[t];
+                double dot = 0;
+                for (size_t t = 0; t < v.size(); ++t) dot += v[t] * u[t];
+                for (size_t t = 0; t < v.size(); ++t) v[t] -= dot * u[t];
               }
             }
             double nv = 0;
@@ -393,9 +393,9 @@ struct Builder {
     auto orth_ok = [](const std::vector<std::vector<double>>& C) {
       for (size_t a = 0; a < C.size(); ++a)
         for (size_t b = a; b < C.size(); ++b) {
-          double d = 0;
-          for (size_t t = 0; t < C[a].size(); ++t) d += C[a][t] * C[b][t];
-          if (std::fabs(d - (a == b ? 1.0 : 0.0)) > 1e-9) return false;
+          double dot = 0;
+          for (size_t t = 0; t < C[a].size(); ++t) dot += C[a][t] * C[b][t];
+          if (std::fabs(dot - (a == b ? 1.0 : 0.0)) > 1e-9) return false;
         }
       return true;
     };
