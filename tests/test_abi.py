@@ -1,6 +1,5 @@
 """C-ABI boundary tests that need no GPU: the library loads, exports every symbol the
 header declares, and reports errors as status codes (never aborts)."""
-import ctypes
 import os
 import re
 

@@ -3,7 +3,6 @@
 The library's decomposition (Theorem 4 closed form) is compared with the oracle's
 B_phi^T L B_phi matrix product; the realised basis U_f exported by gft_plan_basis is
 compared with the oracle's eigenbasis per eigenvalue cluster (reading A-4)."""
-import itertools
 
 import numpy as np
 import pytest
