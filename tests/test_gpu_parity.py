@@ -344,6 +344,28 @@ def test_execute_host_end_to_end():
     assert torch.equal(Y, ref.cpu())
 
 
+@pytest.mark.parametrize("name,dtype,slots,chunk,batch", [("cfg3", "f32", 3, 1000, 12345),
+                                                           ("cfg4", "f64", 4, 777, 5000),
+                                                           ("cfg5b", "f32", 2, 256, 1001)])
+def test_execute_host_slots_and_ragged_chunks(name, dtype, slots, chunk, batch):
+    """Host-buffer path with 2-4 workspace slots (one stream each), chunks that do not divide
+    the batch, odd row pitch (cfg3), fp64 and the tensor-core kernel; inverse of the forward
+    round-trips; results bit-identical to the device-buffer calls."""
+    plan = plan_for(name, dtype)
+    cfg = workloads.config(name)
+    X = workloads.signals(cfg, batch=batch, dtype=dtype).pin_memory()
+    Y = torch.empty_like(X).pin_memory()
+    Z = torch.empty_like(X).pin_memory()
+    ws = torch.empty(slots * chunk * cfg.n, device="cuda", dtype=TDT[dtype])
+    plan.execute_host(0, X, Y, ws, chunk)
+    plan.execute_host(1, Y, Z, ws, chunk)
+    torch.cuda.synchronize()
+    ref = plan.forward(X.cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(Y, ref.cpu())
+    assert oracle.relative_error(Z.numpy(), X.numpy()).max() <= 2 * TOL[dtype]
+
+
 @pytest.mark.parametrize("kind,n,dtype", [("complete", 64, "f32"), ("complete", 64, "f64"),
                                           ("star", 33, "f32"), ("star", 100, "f64")])
 def test_two_sparse_eigenvector_graphs_on_gpu(kind, n, dtype):
