@@ -454,10 +454,15 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, bool pair, 
       }
     }
     if (pair) {
-      // 8 warps of the pair arrive on the leader's `staged` barrier; the leader's issuer warp
-      // (gft_issue_pair) waits for it and issues -- compute warps never block on the issue
-      if (ti + 1 == T.size()) o << "  signal_staged(staged0);\n";   // one arrive per warp per tile
-      if (ti == 0) iss << "  mbar_wait_acq_cluster(staged_local, par); tc_fence_after();\n";
+      // 8 warps of the pair arrive on the leader's `staged` barrier of this leaf; the leader's
+      // issuer warp (gft_issue_pair) waits for it and issues the leaf's MMAs while the next
+      // leaf is being staged -- compute warps never block on the issue
+      // (GFT_TC_STAGED_ONCE=1: one signal after the last leaf, the previous protocol)
+      const bool once = getenv("GFT_TC_STAGED_ONCE") != nullptr;
+      if (!once || ti + 1 == T.size())
+        o << "  signal_staged(staged0 + " << (once ? 0 : 8 * ti) << "u);\n";
+      if (!once || ti == 0)
+        iss << "  mbar_wait_acq_cluster(staged_local + " << (once ? 0 : 8 * ti) << "u, par); tc_fence_after();\n";
       iss << mm.str();
       if (ti + 1 == T.size()) iss << "  tc_commit_pair(mbar);\n";   // tracks all MMAs issued before it
     } else {

@@ -170,8 +170,9 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   unsigned char* stages = smem;
   unsigned char* bsm = smem + GFT_STAGES * GFT_TILE_BYTES;            // this CTA's half of B
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(bsm + GFT_B_FLOATS * 4);
-  // bars: full[S], done[S], mma[GFT_WGS], staged[GFT_WGS] (staged used in the leader only)
-  u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * GFT_STAGES + 2 * GFT_WGS);
+  // bars: full[S], done[S], mma[GFT_WGS], staged[GFT_WGS][GFT_NTC] (one per tensor-core leaf,
+  // used in the leader only: the issuer starts a leaf's MMAs while the next leaf is staged)
+  u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * GFT_STAGES + GFT_WGS + GFT_WGS * GFT_NTC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const u32 rank = cluster_rank();
   const long long npairs = (batch + 2 * GFT_TILE_ROWS - 1) / (2 * GFT_TILE_ROWS);
@@ -192,7 +193,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
     }
     for (int g = 0; g < GFT_WGS; ++g) {
       mbar_init(smem_u32(&bars[2 * GFT_STAGES + g]), 1);
-      mbar_init(smem_u32(&bars[2 * GFT_STAGES + GFT_WGS + g]), 8);
+      for (int i = 0; i < GFT_NTC; ++i) mbar_init(smem_u32(&bars[2 * GFT_STAGES + GFT_WGS + g * GFT_NTC + i]), 8);
     }
     fence_mbar_init();
   }
@@ -253,7 +254,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
         if (pid0 + it * npid >= npairs) break;
         const int g = (int)(it % GFT_WGS);
         gft_issue_pair(tmem + (u32)(g * GFT_WG_COLS), bsm_s, smem_u32(&bars[2 * GFT_STAGES + g]),
-                       smem_u32(&bars[2 * GFT_STAGES + GFT_WGS + g]), (u32)((it / GFT_WGS) & 1));
+                       smem_u32(&bars[2 * GFT_STAGES + GFT_WGS + g * GFT_NTC]), (u32)((it / GFT_WGS) & 1));
       }
     }
   } else {
@@ -264,8 +265,8 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
     const u32 bsm_s = smem_u32(bsm);
     const u32 mbar = smem_u32(&bars[2 * GFT_STAGES + g]);
     // `staged` barriers live in the leader CTA (rank 0)
-    const u32 staged0 = map_to_cta(smem_u32(&bars[2 * GFT_STAGES + GFT_WGS + g]), 0);
-    const u32 staged_local = smem_u32(&bars[2 * GFT_STAGES + GFT_WGS + g]);
+    const u32 staged0 = map_to_cta(smem_u32(&bars[2 * GFT_STAGES + GFT_WGS + g * GFT_NTC]), 0);
+    const u32 staged_local = smem_u32(&bars[2 * GFT_STAGES + GFT_WGS + g * GFT_NTC]);
     for (long long it = g;; it += GFT_WGS) {
       const long long p = pid0 + it * npid;
       if (p >= npairs) break;

@@ -37,7 +37,7 @@ struct KernelCfg {
   int threads() const { return tc ? (tc_ws ? 384 : tc_pair ? 32 * (4 * tc_wgs + 2) : 160) : warps * 32; }
   int tiles_per_cta() const { return tc ? 1 : warps; }   // tiles processed concurrently per CTA
   int smem_bytes() const {
-    if (tc) return (stages + tc_io_split) * tile_bytes() + tc_b_bytes + (3 * stages + 10) * 8 + 16 + 1024;
+    if (tc) return (stages + tc_io_split) * tile_bytes() + tc_b_bytes + (3 * stages + 24) * 8 + 16 + 1024;
     return warps * stages * tile_bytes() + warps * stages * 8 + 1024;
   }
   int swizzle_bytes() const { return swz_mask == 7 ? 128 : swz_mask == 3 ? 64 : swz_mask == 1 ? 32 : 0; }
