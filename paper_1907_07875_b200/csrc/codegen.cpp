@@ -404,7 +404,16 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, bool pair, 
     o << buf << ((i % 8 == 7) ? "\n" : "");
   }
   o << "};\n";
-  o << "#define GFT_NTC " << T.size() << "\n";
+  // pair kernel: one `staged` mbarrier per 32-column staging chunk of every tensor-core leaf
+  // (the issuer starts a chunk's MMAs while the next chunk is staged); single CTA: one
+  // MMA-completion mbarrier per leaf
+  const bool stage_per_leaf = getenv("GFT_TC_STAGED_LEAF") != nullptr;
+  const bool stage_once = getenv("GFT_TC_STAGED_ONCE") != nullptr;
+  int nstaged = 0;
+  for (const auto& t : T) nstaged += stage_per_leaf ? 1 : (t.kp8 + 31) / 32;
+  if (stage_once) nstaged = 1;
+  o << "#define GFT_NTC " << (pair ? nstaged : (int)T.size()) << "\n";
+  int si = 0;   // running staged-barrier index (pair)
   if (pair)
     o << "static __device__ __forceinline__ void gft_tile(float (&x)[GFT_N], float (&y)[GFT_N], u32 tm,\n"
          "    u32 tmem, u32 bsm, u32 mbar, u32 staged0, u32 staged_local, u32 par, int tid, u32 rank) {\n";
@@ -435,6 +444,27 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, bool pair, 
       emit_tmem_st(o, "h", t.hi_col + c0, w);
       emit_tmem_st(o, "l", t.lo_col + c0, w);
       o << "  }\n";
+      if (pair && !stage_per_leaf && !stage_once) {
+        // this chunk's k-steps, all three 3xTF32 passes, as soon as the chunk is staged
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(t.np >> 3) << 17) | (16u << 24);
+        const int atom_bytes = (t.np / 2) * 128;
+        o << "  signal_staged(staged0 + " << 8 * si << "u);\n";
+        iss << "  mbar_wait_acq_cluster(staged_local + " << 8 * si << "u, par); tc_fence_after();\n";
+        for (int pass = 0; pass < 3; ++pass) {
+          const int acol = pass == 2 ? t.lo_col : t.hi_col;
+          const int boff = pass == 1 ? t.blo_off : t.bhi_off;
+          for (int j = c0 / 8; j < (c0 + w) / 8; ++j) {
+            const int bo = boff + (j / 4) * atom_bytes + (j % 4) * 32;
+            iss << "  mma_ts2(tmem + " << t.d_col << "u, tmem + " << (acol + 8 * j) << "u, smem_desc_sw128(bsm + "
+                << bo << "u), " << idesc << "u, " << ((pass == 0 && j == 0) ? 0 : 1) << "u);\n";
+          }
+        }
+        ++si;
+      }
+    }
+    if (pair && !stage_per_leaf && !stage_once) {
+      if (ti + 1 == T.size()) iss << "  tc_commit_pair(mbar);\n";
+      continue;
     }
     // ---- this leaf's MMAs (issued by one thread once all lanes are staged) ----
     std::ostringstream mm;
@@ -457,8 +487,8 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, bool pair, 
       // 8 warps of the pair arrive on the leader's `staged` barrier of this leaf; the leader's
       // issuer warp (gft_issue_pair) waits for it and issues the leaf's MMAs while the next
       // leaf is being staged -- compute warps never block on the issue
-      // (GFT_TC_STAGED_ONCE=1: one signal after the last leaf, the previous protocol)
-      const bool once = getenv("GFT_TC_STAGED_ONCE") != nullptr;
+      // (GFT_TC_STAGED_LEAF=1: one signal per leaf; GFT_TC_STAGED_ONCE=1: one per tile)
+      const bool once = stage_once;
       if (!once || ti + 1 == T.size())
         o << "  signal_staged(staged0 + " << (once ? 0 : 8 * ti) << "u);\n";
       if (!once || ti == 0)

@@ -1,7 +1,7 @@
 #!/bin/bash
-# pair tcgen05 kernel: per-leaf `staged` signals (default) vs one signal per tile
+# pair tcgen05 kernel: per-chunk `staged` signals (default) vs one per leaf (GFT_TC_STAGED_LEAF=1)
 for V in 0 1 0 1; do
-  if [ $V = 1 ]; then export GFT_TC_STAGED_ONCE=1; else unset GFT_TC_STAGED_ONCE; fi
+  if [ $V = 1 ]; then export GFT_TC_STAGED_LEAF=1; else unset GFT_TC_STAGED_LEAF; fi
   for k in 0 1; do
     python tools/profile_kernel.py --config cfg5b --kind $k --iters 2 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('ONCE=$V cfg5b k$k', d['kernel'][:24], round(d['b2b_gbs']))"
   done
