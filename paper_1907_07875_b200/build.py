@@ -180,12 +180,26 @@ def build_aot_cubins(jobs=8, verbose=True):
     return sorted(todo)
 
 
+def build_c_example(verbose=True):
+    """examples/gft_example.c: a plain-C consumer of the C ABI (libgft + CUDA runtime)."""
+    exe = os.path.join(LIBDIR, "gft_example")
+    cmd = ["gcc", "-O2", "-std=c11", "-Wall", "-I", os.path.join(ROOT, "include"),
+           "-I", os.path.join(CUDA_HOME, "include"), os.path.join(ROOT, "examples", "gft_example.c"),
+           "-L", LIBDIR, "-lgft", "-L", os.path.join(CUDA_HOME, "lib64"), "-lcudart",
+           "-Wl,-rpath,$ORIGIN", "-Wl,-rpath," + os.path.join(CUDA_HOME, "lib64"), "-lm", "-o", exe]
+    subprocess.check_call(cmd)
+    if verbose:
+        print("built", exe)
+    return exe
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--no-aot", action="store_true")
     a = ap.parse_args(argv)
     build_library(force=a.force)
+    build_c_example()
     if not a.no_aot:
         build_aot_cubins()
 
