@@ -173,7 +173,7 @@ def build_aot_cubins(jobs=8, verbose=True):
             os.replace(out + ".tmp", out)
     # prune cubins that no longer correspond to a generated kernel
     for f in os.listdir(KDIR):
-        if f.endswith(".cubin") and f[:-6] not in todo:
+        if (f.endswith(".cubin") and f[:-6] not in todo) or f.endswith(".cubin.tmp"):
             os.remove(os.path.join(KDIR, f))
     if verbose:
         print("AOT cubins: %d (%d compiled now) in %s" % (len(todo), len(pending), KDIR))
