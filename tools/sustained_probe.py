@@ -59,9 +59,13 @@ def run(label, plan, cfg, seconds=2.0):
                       "launches": iters}), flush=True)
 
 
-for name in ("cfg2", "cfg5a", "cfg5b"):
-    cfg = workloads.config(name)
-    run(name, G.Plan.from_config(cfg, dtypes=("f32",)), cfg)
-cfg = workloads.config("cfg5b")
-os.environ["GFT_TC_IOSPLIT"] = "1"
-run("cfg5b io-split WS", G.Plan.from_config(cfg, dtypes=("f32",)), cfg)
+if __name__ == "__main__":
+    names = sys.argv[1:] or ["cfg2", "cfg5a", "cfg5b"]
+    for name in names:
+        cfg = workloads.config(name)
+        run(name + (" suspend=%s" % os.environ["GFT_SUSPEND_NS"] if "GFT_SUSPEND_NS" in os.environ else ""),
+            G.Plan.from_config(cfg, dtypes=("f32",)), cfg)
+    if not sys.argv[1:]:
+        cfg = workloads.config("cfg5b")
+        os.environ["GFT_TC_IOSPLIT"] = "1"
+        run("cfg5b io-split WS", G.Plan.from_config(cfg, dtypes=("f32",)), cfg)
