@@ -706,7 +706,10 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
     // every big leaf must land on the tensor core for the pair variant to be chosen
     int nbig = 0;
     for (const auto& lf : P.leaves) nbig += lf.k >= 32 && !lf.approx;
-    for (int st = 3; st >= 2 && !ok; --st)
+    // up to 4 tile buffers when they fit (n <= 96: +5% over 3 at n = 80 / 96; cfg5b's 64 KiB
+    // tiles fit 3; tools/gpu_pair_stages.sh); GFT_TC_PAIR_MAXSTAGES overrides
+    const char* pst = getenv("GFT_TC_PAIR_MAXSTAGES");
+    for (int st = (pst && *pst) ? atoi(pst) : 4; st >= 2 && !ok; --st)
       if (plan_tc(P, dtype, st, true, T, tmem_cols, b_bytes) && (int)T.size() == nbig &&
           getenv("GFT_NO_CTA_PAIR") == nullptr) {
         ok = pair = true;
