@@ -155,6 +155,20 @@ GFT_API gft_status gft_plan_create(gft_plan* out, int32_t n, int64_t n_edges,
 
 GFT_API gft_status gft_plan_destroy(gft_plan plan);   /* caller must have synchronised its streams */
 
+/* Plan persistence: the complete factorisation (butterfly units, leaf matrices / Givens
+ * layers, right Haar stages, realised basis and eigenvalues, statistics) as a versioned
+ * little-endian byte string -- no involution search or eigensolve when it is loaded.
+ * gft_plan_serialize: buf == NULL -> *size_out = required bytes, GFT_OK; otherwise cap must
+ * be >= that size (else GFT_ERR_INVALID_ARG, *size_out set).
+ * gft_plan_deserialize: rebuilds a plan from such bytes (every index and size is validated:
+ * GFT_ERR_INVALID_ARG on malformed input, GFT_ERR_UNSUPPORTED on another format version);
+ * opts supplies only dtypes and flags for kernel generation (the planning options are part
+ * of the serialized plan).  Kernels are regenerated deterministically, so they carry the same
+ * names as the original plan's and reuse its AOT / NVRTC cubins. */
+GFT_API gft_status gft_plan_serialize(gft_plan plan, void* buf, size_t cap, size_t* size_out);
+GFT_API gft_status gft_plan_deserialize(gft_plan* out, const void* buf, size_t size,
+                                        const gft_plan_opts* opts);
+
 /* ---- hot path (device memory, asynchronous on `stream`) ----------------------------- */
 
 /* Y[b,:] = U^T X[b,:] for b < batch using the fused fast kernel (butterflies + dense

@@ -28,7 +28,7 @@ LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libgft.so")
 KDIR = os.path.join(LIBDIR, "kernels")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
-SOURCES = ["plan.cpp", "search.cpp", "codegen.cpp", "cuda_rt.cpp", "capi.cpp"]
+SOURCES = ["plan.cpp", "search.cpp", "codegen.cpp", "cuda_rt.cpp", "capi.cpp", "serialize.cpp"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 

@@ -77,7 +77,49 @@ gft_status run(gft_plan plan, int kind, const void* in, void* out, int64_t batch
 }
 }  // namespace
 
+// kernel sources for the dtypes / flags of `o` (nothing for HOST_ONLY)
+void make_kernels(gft_plan_s& p, const gft_plan_opts& o) {
+  p.flags = o.flags;
+  if (o.flags & GFT_FLAG_HOST_ONLY) return;
+  if (p.P.n > 256) gft::fail(GFT_ERR_UNSUPPORTED, "kernel generation supports n <= 256 (use HOST_ONLY)");
+  p.dtypes = o.dtypes;
+  for (int dt = 0; dt < 2; ++dt) {
+    if (!(o.dtypes & (1u << dt))) continue;
+    for (int kind = 0; kind < gft::K_NUM; ++kind) {
+      p.k[dt][kind].reset(new gft::Kernel);
+      gft::generate_kernel(p.P, kind, dt, *p.k[dt][kind], !(o.flags & GFT_FLAG_NO_TENSOR_CORES),
+                           (o.flags & GFT_FLAG_DENSE_TC) != 0);
+    }
+  }
+}
+
 extern "C" {
+
+gft_status gft_plan_serialize(gft_plan plan, void* buf, size_t cap, size_t* size_out) {
+  return guard([&] {
+    if (!plan || !size_out) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
+    const std::vector<uint8_t> b = gft::serialize_plan(plan->P);
+    *size_out = b.size();
+    if (!buf) return;   // size query
+    if (cap < b.size()) gft::fail(GFT_ERR_INVALID_ARG, "buffer too small (see *size_out)");
+    std::memcpy(buf, b.data(), b.size());
+  });
+}
+
+gft_status gft_plan_deserialize(gft_plan* out, const void* buf, size_t size, const gft_plan_opts* opts) {
+  return guard([&] {
+    if (!out || !buf) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
+    *out = nullptr;
+    gft_plan_opts o;
+    gft_plan_opts_default(&o);
+    if (opts) o = *opts;
+    if (o.dtypes & ~3u) gft::fail(GFT_ERR_UNSUPPORTED, "unknown dtype bits");
+    std::unique_ptr<gft_plan_s> p(new gft_plan_s);
+    p->P = gft::deserialize_plan(static_cast<const uint8_t*>(buf), size);
+    make_kernels(*p, o);
+    *out = p.release();
+  });
+}
 
 void gft_plan_opts_default(gft_plan_opts* o) {
   if (!o) return;
@@ -116,19 +158,7 @@ gft_status gft_plan_create(gft_plan* out, int32_t n, int64_t n_edges, const int3
     gft::SubGraph g = gft::graph_from_edges(n, n_edges, src, dst, w, self_loops);
     std::unique_ptr<gft_plan_s> p(new gft_plan_s);
     p->P = gft::build_plan(g, phi, po);
-    p->flags = o.flags;
-    if (!(o.flags & GFT_FLAG_HOST_ONLY)) {
-      if (n > 256) gft::fail(GFT_ERR_UNSUPPORTED, "kernel generation supports n <= 256 (use HOST_ONLY)");
-      p->dtypes = o.dtypes;
-      for (int dt = 0; dt < 2; ++dt) {
-        if (!(o.dtypes & (1u << dt))) continue;
-        for (int kind = 0; kind < gft::K_NUM; ++kind) {
-          p->k[dt][kind].reset(new gft::Kernel);
-          gft::generate_kernel(p->P, kind, dt, *p->k[dt][kind], !(o.flags & GFT_FLAG_NO_TENSOR_CORES),
-                               (o.flags & GFT_FLAG_DENSE_TC) != 0);
-        }
-      }
-    }
+    make_kernels(*p, o);
     *out = p.release();
   });
 }

@@ -176,4 +176,9 @@ void truncated_jacobi(int k, const std::vector<double>& A, int J, std::vector<st
 
 Plan build_plan(const SubGraph& g, const int32_t* user_phi, const PlanOptions& opt);
 
+// Plan persistence (serialize.cpp): a versioned byte string of the whole factorisation;
+// deserialize validates every index and size and throws GFT_ERR_INVALID_ARG on malformed input.
+std::vector<uint8_t> serialize_plan(const Plan& P);
+Plan deserialize_plan(const uint8_t* buf, size_t size);
+
 }  // namespace gft

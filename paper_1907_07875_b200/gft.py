@@ -39,7 +39,8 @@ EXPORTS = ["gft_plan_opts_default", "gft_plan_create", "gft_plan_destroy", "gft_
            "gft_plan_leaf_sizes", "gft_plan_kernel_source", "gft_plan_kernel_name",
            "gft_plan_launch_config", "gft_laplacian", "gft_decompose", "gft_find_involution",
            "gft_status_str", "gft_last_error", "gft_abi_version", "gft_filter_create",
-           "gft_filter_apply", "gft_filter_kernel_name", "gft_filter_kernel_source", "gft_filter_destroy"]
+           "gft_filter_apply", "gft_filter_kernel_name", "gft_filter_kernel_source", "gft_filter_destroy",
+           "gft_plan_serialize", "gft_plan_deserialize"]
 
 
 class GFTError(RuntimeError):
@@ -115,6 +116,8 @@ def lib():
         "gft_filter_kernel_name": (c_int32, [P, c_int32, c_char_p, c_size_t]),
         "gft_filter_kernel_source": (c_int32, [P, c_int32, c_char_p, c_size_t, POINTER(c_size_t)]),
         "gft_filter_destroy": (c_int32, [P]),
+        "gft_plan_serialize": (c_int32, [P, P, c_size_t, POINTER(c_size_t)]),
+        "gft_plan_deserialize": (c_int32, [POINTER(c_void_p), P, c_size_t, POINTER(gft_plan_opts)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -202,6 +205,23 @@ def gft_plan_create(n, src, dst, w, self_loops=None, phi=None, opts=None):
 
 def gft_plan_destroy(h):
     _check(lib().gft_plan_destroy(h))
+
+
+def gft_plan_serialize(h):
+    size = c_size_t()
+    _check(lib().gft_plan_serialize(h, None, 0, ctypes.byref(size)))
+    buf = ctypes.create_string_buffer(size.value)
+    _check(lib().gft_plan_serialize(h, buf, size.value, ctypes.byref(size)))
+    return buf.raw[: size.value]
+
+
+def gft_plan_deserialize(data, opts=None):
+    data = bytes(data)
+    buf = ctypes.create_string_buffer(data, len(data))
+    h = c_void_p()
+    _check(lib().gft_plan_deserialize(ctypes.byref(h), buf, len(data),
+                                      None if opts is None else ctypes.byref(opts)))
+    return h
 
 
 def _run(fn, h, a, b, batch, dtype, stream):
@@ -410,6 +430,26 @@ class Plan:
                    | (0 if right_haar else GFT_FLAG_NO_RIGHT_HAAR))
         self.n = int(n)
         self._h = gft_plan_create(n, src, dst, w, self_loops, phi, o)
+
+    def save(self):
+        """The plan as bytes (gft_plan_serialize)."""
+        return gft_plan_serialize(self._h)
+
+    @classmethod
+    def load(cls, data, *, dtypes=("f32", "f64"), host_only=False, no_cubin_cache=False,
+             no_tensor_cores=False, dense_tc=False):
+        """Rebuild a plan from Plan.save() bytes (gft_plan_deserialize): no search, no
+        eigensolve; kernels regenerated for `dtypes`."""
+        o = gft_plan_opts_default()
+        o.dtypes = 0
+        for d in dtypes:
+            o.dtypes |= 1 << _dtype_code(d)
+        o.flags = ((GFT_FLAG_HOST_ONLY if host_only else 0) | (GFT_FLAG_NO_CUBIN_CACHE if no_cubin_cache else 0)
+                   | (GFT_FLAG_NO_TENSOR_CORES if no_tensor_cores else 0) | (GFT_FLAG_DENSE_TC if dense_tc else 0))
+        self = cls.__new__(cls)
+        self._h = gft_plan_deserialize(data, o)
+        self.n = self.info()["n"]
+        return self
 
     @classmethod
     def from_config(cls, cfg, **kw):
