@@ -45,11 +45,25 @@ KernelCfg choose_cfg(int n, int dtype, int64_t work) {
     else if (row % 64 == 0) { c.boxc = 64 / c.elem; c.swz_mask = 3; }
     else if (row % 32 == 0) { c.boxc = 32 / c.elem; c.swz_mask = 1; }
     else { c.boxc = n; c.swz_mask = 0; }   // 16*odd bytes: odd chunk pitch, conflict-free
+    // rows of 16/32/64 bytes: TMA boxes that narrow move few bytes per request (n = 8 f32:
+    // ~5.4 TB/s whatever the geometry, tools/gpu_r01_persist_cfg1.sh).  Packed view instead:
+    // [batch / g, g*n] with g = 128 / row, one 128-byte box row = g signals, 128B swizzle --
+    // thread-per-row 16-byte LDS stay conflict-free (8 threads of a phase cover two box rows
+    // whose chunk parities the swizzle separates).  GFT_PACK=0 disables.
+    const char* pk = getenv("GFT_PACK");
+    const bool pack_on = pk ? pk[0] != '0' : (row <= 32);
+    if (row < 128 && 128 % row == 0 && pack_on) {
+      c.mode = 2;
+      c.pack = 128 / row;
+      c.boxc = n;
+      c.swz_mask = 7;
+    }
   } else {
     // unaligned row pitch: 1-D bulk copies of whole tiles.  Opt-in (GFT_SUPERROW=1): TMA
     // tensor copies of the 4-signal super-row view (4n <= 256) -- parity-tested but 3% slower
     // on cfg3 (5.79 vs 5.95 TB/s back to back, tools/gpu_superrow_cmp.sh)
     c.mode = (4 * n <= 256 && getenv("GFT_SUPERROW") != nullptr) ? 2 : 1;
+    c.pack = c.mode == 2 ? 4 : 1;
     c.boxc = n;
     c.swz_mask = 0;
     // odd row pitch in vector units makes thread-per-row accesses conflict-free
@@ -73,6 +87,8 @@ KernelCfg choose_cfg(int n, int dtype, int64_t work) {
   c.R = std::max(1, std::min(8, env_int("GFT_TUNE_R", c.R)));
   c.stages = std::max(2, std::min(8, env_int("GFT_TUNE_STAGES", c.stages)));
   c.warps = std::max(1, std::min(16, env_int("GFT_TUNE_WARPS", c.warps)));
+  // the 128B swizzle atom needs 1024-byte aligned tile buffers; TMA boxes hold <= 256 rows
+  while (c.mode == 2 && c.swz_mask && c.tile_bytes() % 1024 != 0 && c.R < 8) c.R *= 2;
   if (c.smem_bytes() > 227 * 1024) c.stages = 2;
   if (c.smem_bytes() > 227 * 1024) c.warps = 2;
   return c;
@@ -857,7 +873,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
   if (dtype == GFT_F64) pre << "#define GFT_ELEM_IS_DOUBLE 1\n";
   pre << "#define GFT_N " << c.n << "\n#define GFT_R " << c.R << "\n#define GFT_WARPS " << c.warps
       << "\n#define GFT_STAGES " << c.stages << "\n#define GFT_MODE " << c.mode << "\n#define GFT_BOXC "
-      << c.boxc << "\n#define GFT_SWZ_MASK " << c.swz_mask << "\n#define GFT_VEC " << c.vec << "\n";
+      << c.boxc << "\n#define GFT_SWZ_MASK " << c.swz_mask << "\n#define GFT_VEC " << c.vec << "\n#define GFT_PACK " << c.pack << "\n";
   // name = kind/dtype/n + hash of everything that determines the code
   std::string key = pre.str() + body.str() + kSkeleton;
   char hbuf[32];

@@ -216,11 +216,11 @@ LoadedFn& ensure_loaded(Kernel& k, CUcontext ctx, bool allow_cache) {
 void encode_map(CUtensorMap* m, const Kernel& k, const void* ptr, int64_t rows) {
   Driver& d = need_driver();
   const KernelCfg& c = k.cfg;
-  // mode 2: the super-row view [rows / 4, 4n] (4 signals per TMA row: 16-byte pitch)
-  const int64_t g = c.mode == 2 ? 4 : 1;
+  // mode 2: the packed view [rows / g, g*n] (g = c.pack signals per TMA row)
+  const int64_t g = c.mode == 2 ? c.pack : 1;
   cuuint64_t dims[2] = {(cuuint64_t)(c.n * g), (cuuint64_t)(rows / g)};
   cuuint64_t strides[1] = {(cuuint64_t)(c.n * c.elem * g)};
-  cuuint32_t box[2] = {(cuuint32_t)(c.mode == 2 ? 4 * c.n : c.boxc), (cuuint32_t)(c.tile_rows() / g)};
+  cuuint32_t box[2] = {(cuuint32_t)(c.mode == 2 ? g * c.n : c.boxc), (cuuint32_t)(c.tile_rows() / g)};
   cuuint32_t estr[2] = {1, 1};
   CUtensorMapSwizzle sw = c.swz_mask == 7 ? CU_TENSOR_MAP_SWIZZLE_128B
                           : c.swz_mask == 3 ? CU_TENSOR_MAP_SWIZZLE_64B
@@ -344,7 +344,7 @@ void launch_kernel(Kernel& k, const void* in, void* out, int64_t batch, void* st
     alignas(64) CUtensorMap tin, tout;
     std::memset(&tin, 0, sizeof tin);
     std::memset(&tout, 0, sizeof tout);
-    if (c.mode == 0 || (c.mode == 2 && rows >= 4)) {
+    if (c.mode == 0 || (c.mode == 2 && rows >= c.pack)) {
       encode_map(&tin, k, pin, rows);
       encode_map(&tout, k, pout, rows);
     }

@@ -11,13 +11,15 @@
 //   GFT_STAGES    SMEM tiles per warp (loads in flight = GFT_STAGES-1)
 //   GFT_MODE      0: TMA tensor 2-D copies with hardware swizzle (n*sizeof(elem) % 16 == 0)
 //                 1: 1-D bulk copies of whole tiles, unpadded rows (odd n etc.)
-//                 2: rows whose pitch is not 16-byte aligned, as TMA tensor copies of a 2-D
-//                    "super-row" view [batch/4, 4n] (4 signals per super-row: 16-byte pitch),
-//                    no swizzle -- the same unpadded SMEM tile as mode 1, but the TMA tensor
-//                    engine instead of the 1-D bulk copy; a tail of batch % 4 signals takes
-//                    the direct path
+//                 2: TMA tensor copies of a packed 2-D view [batch/GFT_PACK, GFT_PACK*n]
+//                    (GFT_PACK signals per TMA row) -- rows of 16/32/64 bytes as 128-byte
+//                    box rows with 128B swizzle, or (opt-in) rows whose pitch is not 16-byte
+//                    aligned as 4-signal super-rows without swizzle; the SMEM tile is the
+//                    unpadded row-major tile (swizzled in the first case); a tail of
+//                    batch % GFT_PACK signals takes the direct path
 //   GFT_BOXC      columns per TMA box (mode 0); n % GFT_BOXC == 0
-//   GFT_SWZ_MASK  7 / 3 / 1 / 0 for 128B / 64B / 32B / no swizzle (mode 0)
+//   GFT_SWZ_MASK  7 / 3 / 1 / 0 for 128B / 64B / 32B / no swizzle (modes 0 and 2)
+//   GFT_PACK      signals per TMA row of the packed view (mode 2)
 //   GFT_VEC       elements per SMEM vector access (16, 8 or 4/8 bytes)
 //   GFT_KNAME     kernel symbol
 //
@@ -96,6 +98,9 @@ static __device__ __forceinline__ u32 tile_off(int row, int col) {
   const u32 lin = (u32)((col / GFT_BOXC) * GFT_BOX_BYTES + row * GFT_BOX_ROWB +
                         (col % GFT_BOXC) * (int)sizeof(elem_t));
   return lin ^ (((lin >> 7) & GFT_SWZ_MASK) << 4);   // TMA swizzle: chunk16 ^= bits[7..]
+#elif GFT_MODE == 2
+  const u32 lin = (u32)((row * GFT_N + col) * (int)sizeof(elem_t));
+  return lin ^ (((lin >> 7) & GFT_SWZ_MASK) << 4);   // packed 128-byte box rows
 #else
   return (u32)((row * GFT_N + col) * (int)sizeof(elem_t));
 #endif
@@ -159,7 +164,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
 #if GFT_MODE == 1
     return (t + 1) * GFT_TILE_ROWS > batch;
 #elif GFT_MODE == 2
-    return (batch & 3) != 0 && (t + 1) * GFT_TILE_ROWS > (batch & ~3ll);
+    return (batch % GFT_PACK) != 0 && (t + 1) * GFT_TILE_ROWS > batch - batch % GFT_PACK;
 #else
     (void)t;
     return false;
@@ -174,7 +179,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
     for (int b = 0; b < GFT_NBOX; ++b)
       tma_load_2d(dst + b * GFT_BOX_BYTES, &tin, b * GFT_BOXC, (int)(t * GFT_TILE_ROWS), bar);
 #elif GFT_MODE == 2
-    tma_load_2d(dst, &tin, 0, (int)(t * (GFT_TILE_ROWS / 4)), bar);
+    tma_load_2d(dst, &tin, 0, (int)(t * (GFT_TILE_ROWS / GFT_PACK)), bar);
 #else
     bulk_load(dst, reinterpret_cast<const unsigned char*>(X) + (size_t)t * GFT_TILE_BYTES,
               GFT_TILE_BYTES, bar);
@@ -187,7 +192,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
     for (int b = 0; b < GFT_NBOX; ++b)
       tma_store_2d(&tout, b * GFT_BOXC, (int)(t * GFT_TILE_ROWS), src + b * GFT_BOX_BYTES);
 #elif GFT_MODE == 2
-    tma_store_2d(&tout, 0, (int)(t * (GFT_TILE_ROWS / 4)), src);
+    tma_store_2d(&tout, 0, (int)(t * (GFT_TILE_ROWS / GFT_PACK)), src);
 #else
     bulk_store(reinterpret_cast<unsigned char*>(Y) + (size_t)t * GFT_TILE_BYTES, src, GFT_TILE_BYTES);
 #endif

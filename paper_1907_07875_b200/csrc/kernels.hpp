@@ -19,7 +19,8 @@ enum KernelKind { K_FAST_FWD = 0, K_FAST_INV = 1, K_DENSE_FWD = 2, K_DENSE_INV =
 struct KernelCfg {
   int n = 0, elem = 4;          // signal length, bytes per element
   int R = 1, warps = 4, stages = 3;
-  int mode = 0;                 // 0 TMA tensor 2-D + swizzle, 1 bulk 1-D
+  int mode = 0;                 // 0 TMA tensor 2-D + swizzle, 1 bulk 1-D, 2 packed view
+  int pack = 1;                 // signals per TMA row of the packed view (mode 2)
   int boxc = 0, swz_mask = 0;   // TMA box columns, swizzle mask (7/3/1/0)
   int vec = 1;                  // elements per SMEM vector access
   // tensor-core variant (kernel_tc_skeleton.cuh): one 128-row tile per CTA iteration,

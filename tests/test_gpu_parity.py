@@ -494,3 +494,28 @@ def test_degenerate_graphs(case):
         torch.cuda.synchronize()
         check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), TOL[dtype])
         assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL[dtype]
+
+
+@pytest.mark.parametrize("n,dtype,force", [(8, "f32", False), (4, "f32", False), (4, "f64", False),
+                                           (8, "f64", True), (16, "f32", True)])
+@pytest.mark.parametrize("batch", [1, 3, 4, 130, 1001, 70001])
+def test_packed_view_mode(monkeypatch, n, dtype, force, batch):
+    """Rows of 16/32/64 bytes move as a packed [batch/g, g*n] TMA view with 128-byte box rows
+    and 128B swizzle (default for rows <= 32 B, GFT_PACK=1 forces 64-B rows): a cycle plan vs
+    the oracle with ragged batches (batch % g signals take the direct path, batch < g too)."""
+    s = np.arange(n, dtype=np.int32)
+    d = ((s + 1) % n).astype(np.int32)
+    w = np.random.default_rng(n).uniform(0.5, 2.0, n)
+    if force:
+        monkeypatch.setenv("GFT_PACK", "1")
+    plan = G.Plan(n, s, d, w, dtypes=(dtype,), no_cubin_cache=force)
+    monkeypatch.delenv("GFT_PACK", raising=False)
+    src = plan.kernel_source(G.K_FAST_FWD, dtype)
+    assert "#define GFT_MODE 2" in src and f"#define GFT_PACK {128 // (n * (8 if dtype == 'f64' else 4))}" in src
+    lam_o, U_o = oracle.gft_basis(oracle.laplacian(n, s, d, w))
+    X = torch.randn(batch, n, generator=torch.Generator().manual_seed(batch), dtype=TDT[dtype])
+    Y = plan.forward(X.cuda())
+    Xr = plan.inverse(Y)
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), TOL[dtype])
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL[dtype]
