@@ -303,14 +303,36 @@ float tf32_rna_host(float v) {
   return r;
 }
 
+// Approximate leaves (J Givens layers) are cheap in FFMAs but the straight-line rotation code
+// costs one issue slot per FFMA: past ~32 n instructions per signal the CUDA-core kernel is
+// issue-bound (n = 64: J = 20, ~22 n, runs at 0.93 of HBM; J = 40, ~42 n, at 0.52 --
+// ncu: issue active 60%, no_instruction stalls on the 2600-instruction body).  Such plans
+// multiply each approximate leaf out (M = the folded U_hat_l^T, the same linear map) and run
+// it as a tcgen05 leaf, which is HBM-bound at any k.  GFT_APPROX_TC=0/1 forces the choice.
+static bool approx_on_tc(const Plan& P, int dtype) {
+  if (P.n_approx_leaves == 0 || dtype != GFT_F32) return false;
+  const char* e = getenv("GFT_APPROX_TC");
+  if (e && *e) return e[0] != '0';
+  const int64_t instr = 2 * (int64_t)P.n_units + P.sum_k2 + 2 * (int64_t)P.n_givens + P.n_approx_scale +
+                        2 * (int64_t)P.n_post;
+  return instr > 32 * (int64_t)P.n;
+}
+
+// leaves that go to the tensor core when they fit: exact leaves of k >= 32 (below that the
+// k^2 FFMAs are cheaper than the MMA chain), approximate leaves of k >= 16 when densified
+static bool tc_candidate(const Plan& P, const Leaf& lf, bool approx_tc) {
+  return lf.approx ? (approx_tc && lf.k >= 16) : lf.k >= 32;
+}
+
 // pair: CTA-pair (cta_group::2) variant -- each CTA stores half of every B operand.
 bool plan_tc(const Plan& P, int dtype, int stages, bool pair, std::vector<TcLeaf>& out, int& tmem_cols,
              int& b_bytes) {
   out.clear();
   if (dtype != GFT_F32 || P.n % 4 != 0 || P.n > 256) return false;   // 16-byte rows for TMA
+  const bool atc = approx_on_tc(P, dtype);
   std::vector<int> order;
   for (int l = 0; l < (int)P.leaves.size(); ++l)
-    if (P.leaves[l].k >= 32 && !P.leaves[l].approx) order.push_back(l);
+    if (tc_candidate(P, P.leaves[l], atc)) order.push_back(l);
   std::stable_sort(order.begin(), order.end(),
                    [&](int a, int b) { return P.leaves[a].k > P.leaves[b].k; });
   const int tile = 128 * ((P.n + 31) / 32 * 32) * 4;   // padded to whole TMA boxes
@@ -721,7 +743,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
     // CTA pair first (3 tile buffers if they fit, else 2), then the single-CTA variant;
     // every big leaf must land on the tensor core for the pair variant to be chosen
     int nbig = 0;
-    for (const auto& lf : P.leaves) nbig += lf.k >= 32 && !lf.approx;
+    for (const auto& lf : P.leaves) nbig += tc_candidate(P, lf, approx_on_tc(P, dtype));
     // up to 4 tile buffers when they fit (n <= 96: +5% over 3 at n = 80 / 96; cfg5b's 64 KiB
     // tiles fit 3; tools/gpu_pair_stages.sh); GFT_TC_PAIR_MAXSTAGES overrides
     const char* pst = getenv("GFT_TC_PAIR_MAXSTAGES");

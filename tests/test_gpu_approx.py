@@ -64,3 +64,34 @@ def test_approximate_filter_is_dense_block():
     ref = oracle.graph_filter(X.numpy(), U_o, np.exp(-0.3 * lam_o))
     err = np.linalg.norm(Y.cpu().numpy() - ref, axis=1) / np.linalg.norm(X.numpy().astype(np.float64), axis=1)
     assert err.max() <= 2e-5, err.max()
+
+
+@pytest.mark.parametrize("name,J,depth,force", [("bidiag", 40, 0, None), ("bidiag", 40, 1, None),
+                                                ("z", 40, 1, None), ("z", 10, 1, "1"),
+                                                ("bidiag", 5, 0, "1"), ("bidiag", 40, 0, "0")])
+def test_approximate_leaves_on_tensor_cores(monkeypatch, name, J, depth, force):
+    """Issue-bound approximate plans (many Givens layers) run their approximate leaves as
+    densified tcgen05 leaves (the same linear map U_hat_l, multiplied out); GFT_APPROX_TC=1/0
+    forces the choice.  Either way the result is the approximate oracle's U_hat^T x."""
+    s, d, w = workloads.bidiag_grid() if name == "bidiag" else workloads.z_grid()
+    L = oracle.laplacian(64, s, d, w)
+    phi = PHI[name] if depth else None
+    if force is not None:
+        monkeypatch.setenv("GFT_APPROX_TC", force)
+    plan = G.Plan(64, s, d, w, None, phi, dtypes=("f32",), max_depth=depth, approx_layers=J,
+                  no_cubin_cache=force is not None)
+    monkeypatch.delenv("GFT_APPROX_TC", raising=False)
+    on_tc = "tc" in plan.kernel_name(G.K_FAST_FWD, "f32").split("_")[1]
+    assert on_tc == (force != "0"), plan.kernel_name(G.K_FAST_FWD, "f32")
+    if depth == 0:
+        _, _, U_o, lam_o = oracle.truncated_jacobi(L, J)
+    else:
+        lam_o, U_o = oracle.haar_approx_basis(L, phi, J)
+    X = torch.randn(4099, 64, generator=torch.Generator().manual_seed(J + depth))
+    Y = plan.forward(X.cuda())
+    Xr = plan.inverse(Y)
+    torch.cuda.synchronize()
+    R = oracle.cluster_rotation(U_o, plan.basis(), lam_o)
+    e = oracle.aligned_error(Y.cpu().numpy(), oracle.forward(X.numpy(), U_o), R)
+    assert e.max() <= 1e-5, e.max()
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
