@@ -123,6 +123,41 @@ def main():
     with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
         json.dump({"round": a.round, "kernels": rows, "launch_shares": {k: v / tot for k, v in shares.items()}},
                   f, indent=1)
+    # multi-kernel capture of tools/profile_many.py (right Haar / approximate rows): every
+    # kernel is launched twice, the second (warm-module) launch of each spec is reported
+    rep = os.path.join(a.dir, "prof_next_rows.ncu-rep")
+    if os.path.exists(rep):
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        with open(os.path.join(outdir, "raw_next_rows.csv"), "w") as f:
+            f.write(raw)
+        r = list(csv.reader(io.StringIO(raw)))
+        specs = []
+        pm = os.path.join(a.dir, "plain_many.log")
+        if os.path.exists(pm):
+            for line in open(pm):
+                try:
+                    v = json.loads(line)
+                except ValueError:
+                    continue
+                specs.extend(v if isinstance(v, list) else [v])
+        if len(r) >= 3:
+            hdr, units = r[0], r[1]
+            cols = [("Kernel Name", "kernel")] + METRICS[:11]
+            with open(os.path.join(outdir, "ncu_next_rows.md"), "w") as f:
+                f.write("# ncu --set full: right Haar / approximate kernels (%s)\n\nSource: `ncu --set full "
+                        "--clock-control none -k regex:gft_` of `tools/profile_many.py` (each kernel launched "
+                        "twice, cold, serialised; the second launch is listed).  Raw page: `raw_next_rows.csv`.  "
+                        "Durations under ncu are not bench numbers.\n\n" % a.round)
+                f.write("| spec | " + " | ".join(l for _, l in cols) + " |\n|" + "---|" * (len(cols) + 1) + "\n")
+                for i, vals in enumerate(r[2:]):
+                    if i % 2 == 0:
+                        continue
+                    spec = specs[i // 2].get("spec", "") if i // 2 < len(specs) else ""
+                    cells = []
+                    for k, _ in cols:
+                        j = hdr.index(k) if k in hdr else -1
+                        cells.append("" if j < 0 else vals[j] + ((" " + units[j]) if units[j] else ""))
+                    f.write("| %s | %s |\n" % (spec, " | ".join(cells)))
     print("wrote", outdir)
 
 
