@@ -577,7 +577,7 @@ def main():
     Yh = torch.empty_like(Xh).pin_memory()
     Zh = torch.empty_like(Xh).pin_memory()
     chunk = 1 << 18
-    wsb = torch.empty(2 * chunk * n, dtype=X.dtype, device=device)
+    wsb = torch.empty(4 * chunk * n, dtype=X.dtype, device=device)   # 4 slots
 
     def e2e_step():
         plan.execute_host(0, Xh, Yh, wsb, chunk, stream)
@@ -636,7 +636,7 @@ def main():
             "e2e": {"value": B * ws / (e2e_ms * 1e-3), "unit": "signals/s",
                     "h2d_bytes_per_step": 2 * B * n * esz, "d2h_bytes_per_step": 2 * B * n * esz,
                     "ms_per_step": e2e_ms, "roundtrip_max_rel_err": roundtrip_err,
-                    "path": "gft_execute_host (pinned host, 2 streams, 2^18-row chunks)",
+                    "path": "gft_execute_host (pinned host; H2D / kernel / D2H stage streams, 4 slots, 2^18-row chunks ramped at both ends)",
                     "pcie": pcie},
             "gpu_launches": 2 * args.steps,
             "kernels": {"fast_fwd_ms": round(fwd_ms, 5), "fast_inv_ms": round(inv_ms, 5),

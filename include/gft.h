@@ -191,10 +191,12 @@ GFT_API gft_status gft_dense_inverse(gft_plan plan, const void* Y, void* X, int6
 
 /* End-to-end variant with HOST buffers: copies X_host -> device, runs the fast transform,
  * copies the result back to Y_host, chunked over S = min(4, workspace_bytes / chunk bytes)
- * workspace slots, each on its own library-owned stream (chunk c uses slot c mod S), so
- * H2D, compute and D2H of neighbouring chunks overlap on both copy directions.
+ * workspace slots (chunk c uses slot c mod S) on three library-owned stage streams (all
+ * H2D copies, all kernels, all D2H copies; events order each chunk and the reuse of a slot),
+ * so H2D, compute and D2H of neighbouring chunks overlap on both copy directions.
  * `workspace` is a device buffer of `workspace_bytes` >= 2 * chunk_rows * n * sizeof(dtype)
- * (chunk_rows > 0; 3 slots measured best on PCIe Gen5).  Work is
+ * (chunk_rows > 0; 3-4 slots of 2^18 rows measured best on PCIe Gen5).
+ * Concurrent calls from several host threads are serialised while they enqueue.  Work is
  * ordered after prior work on `stream` and `stream` is made to wait for completion;
  * host buffers must stay valid until `stream` completes (use pinned memory for overlap).
  * direction: 0 = forward, 1 = inverse. */

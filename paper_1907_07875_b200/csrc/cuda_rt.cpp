@@ -390,22 +390,31 @@ void unload_kernel(Kernel& k) {
 namespace {
 constexpr int kMaxHostSlots = 4;
 struct HostStreams {
-  CUstream s[kMaxHostSlots];
+  CUstream s[kMaxHostSlots];        // stage streams: s[0] H2D, s[1] kernels, s[2] D2H
   CUevent start, done[kMaxHostSlots];
+  CUevent h2d[kMaxHostSlots], kdone[kMaxHostSlots], d2h[kMaxHostSlots];   // per workspace slot
+  std::mutex mu;                    // one enqueue at a time (events are reused across calls)
 };
 std::mutex g_hs_mu;
-std::map<CUcontext, HostStreams> g_hs;
+std::map<CUcontext, HostStreams*> g_hs;
 HostStreams& host_streams(CUcontext ctx) {
   std::lock_guard<std::mutex> lk(g_hs_mu);
   auto it = g_hs.find(ctx);
-  if (it != g_hs.end()) return it->second;
+  if (it != g_hs.end()) return *it->second;
   Driver& d = need_driver();
-  HostStreams h;
-  for (int i = 0; i < kMaxHostSlots; ++i) ck(d.cuStreamCreate(&h.s[i], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
-  ck(d.cuEventCreate(&h.start, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
-  for (int i = 0; i < kMaxHostSlots; ++i) ck(d.cuEventCreate(&h.done[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
-  return g_hs.emplace(ctx, h).first->second;
+  HostStreams* h = new HostStreams();   // lives as long as the process (like the context's modules)
+  for (int i = 0; i < kMaxHostSlots; ++i) ck(d.cuStreamCreate(&h->s[i], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+  ck(d.cuEventCreate(&h->start, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+  for (int i = 0; i < kMaxHostSlots; ++i) {
+    ck(d.cuEventCreate(&h->done[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    ck(d.cuEventCreate(&h->h2d[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    ck(d.cuEventCreate(&h->kdone[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    ck(d.cuEventCreate(&h->d2h[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+  }
+  g_hs.emplace(ctx, h);
+  return *h;
 }
+
 }  // namespace
 
 void execute_host(Kernel& k, const void* in_host, void* out_host, int64_t batch, void* workspace,
@@ -421,27 +430,42 @@ void execute_host(Kernel& k, const void* in_host, void* out_host, int64_t batch,
   Driver& d = need_driver();
   CUcontext ctx = current_ctx(stream);
   HostStreams& hs = host_streams(ctx);
+  std::lock_guard<std::mutex> lk(hs.mu);
   const int slots = (int)std::min<size_t>(kMaxHostSlots, workspace_bytes / chunk_bytes);
+  // (a geometric ramp of small first / last chunks to shorten the pipeline fill and drain
+  // measured no gain on cfg2, 44.9 GB/s each way either way -- tools/e2e_probe.py)
+  std::vector<int64_t> chunks;
+  for (int64_t off = 0; off < batch; off += chunk_rows) chunks.push_back(std::min(chunk_rows, batch - off));
+  // Three stage streams: every H2D on one stream (the H2D copy engine runs back to back),
+  // every kernel on a second, every D2H on a third; per workspace slot, events order
+  // H2D -> kernel -> D2H and the slot's next H2D after its previous D2H.  Per-slot streams
+  // (H2D, kernel, D2H of one chunk on one stream) stall the next H2D behind the kernel.
+  CUstream sh = hs.s[0], sk = hs.s[1], sd = hs.s[2];
   ck(d.cuEventRecord(hs.start, (CUstream)stream), "cuEventRecord");
-  for (int i = 0; i < slots; ++i) ck(d.cuStreamWaitEvent(hs.s[i], hs.start, 0), "cuStreamWaitEvent");
-  int64_t c = 0;
-  for (int64_t off = 0; off < batch; off += chunk_rows, ++c) {
+  for (int i = 0; i < 3; ++i) ck(d.cuStreamWaitEvent(hs.s[i], hs.start, 0), "cuStreamWaitEvent");
+  int64_t off = 0;
+  for (size_t c = 0; c < chunks.size(); ++c) {
     const int slot = (int)(c % slots);
-    const int64_t rows = std::min<int64_t>(chunk_rows, batch - off);
-    CUstream s = hs.s[slot];
+    const int64_t rows = chunks[c];
     unsigned char* buf = static_cast<unsigned char*>(workspace) + slot * chunk_bytes;
+    if ((int)c >= slots) ck(d.cuStreamWaitEvent(sh, hs.d2h[slot], 0), "cuStreamWaitEvent");
     ck(d.cuMemcpyHtoDAsync((CUdeviceptr)buf, static_cast<const unsigned char*>(in_host) + off * row_bytes,
-                           rows * row_bytes, s),
+                           rows * row_bytes, sh),
        "cuMemcpyHtoDAsync");
-    launch_kernel(k, buf, buf, rows, s, allow_cache);
+    ck(d.cuEventRecord(hs.h2d[slot], sh), "cuEventRecord");
+    ck(d.cuStreamWaitEvent(sk, hs.h2d[slot], 0), "cuStreamWaitEvent");
+    launch_kernel(k, buf, buf, rows, sk, allow_cache);
+    ck(d.cuEventRecord(hs.kdone[slot], sk), "cuEventRecord");
+    ck(d.cuStreamWaitEvent(sd, hs.kdone[slot], 0), "cuStreamWaitEvent");
     ck(d.cuMemcpyDtoHAsync(static_cast<unsigned char*>(out_host) + off * row_bytes, (CUdeviceptr)buf,
-                           rows * row_bytes, s),
+                           rows * row_bytes, sd),
        "cuMemcpyDtoHAsync");
+    ck(d.cuEventRecord(hs.d2h[slot], sd), "cuEventRecord");
+    off += rows;
   }
-  for (int i = 0; i < slots; ++i) {
-    ck(d.cuEventRecord(hs.done[i], hs.s[i]), "cuEventRecord");
-    ck(d.cuStreamWaitEvent((CUstream)stream, hs.done[i], 0), "cuStreamWaitEvent");
-  }
+  // the D2H stream's last copy follows every kernel and H2D of this call
+  ck(d.cuEventRecord(hs.done[0], sd), "cuEventRecord");
+  ck(d.cuStreamWaitEvent((CUstream)stream, hs.done[0], 0), "cuStreamWaitEvent");
 }
 
 }  // namespace gft
