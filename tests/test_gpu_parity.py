@@ -348,7 +348,7 @@ def test_execute_host_end_to_end():
                                                            ("cfg4", "f64", 4, 777, 5000),
                                                            ("cfg5b", "f32", 2, 256, 1001)])
 def test_execute_host_slots_and_ragged_chunks(name, dtype, slots, chunk, batch):
-    """Host-buffer path with 2-4 workspace slots (one stream each), chunks that do not divide
+    """Host-buffer path with 2-4 workspace slots (H2D / kernel / D2H stage streams), chunks that do not divide
     the batch, odd row pitch (cfg3), fp64 and the tensor-core kernel; inverse of the forward
     round-trips; results bit-identical to the device-buffer calls."""
     plan = plan_for(name, dtype)
@@ -364,6 +364,32 @@ def test_execute_host_slots_and_ragged_chunks(name, dtype, slots, chunk, batch):
     torch.cuda.synchronize()
     assert torch.equal(Y, ref.cpu())
     assert oracle.relative_error(Z.numpy(), X.numpy()).max() <= 2 * TOL[dtype]
+
+
+def test_execute_host_concurrent_threads():
+    """Four host threads, each with its own caller stream, workspace and data, call the
+    host-buffer path at once (the shared stage streams / events are enqueued under a lock):
+    every result equals the device-buffer forward."""
+    plan = plan_for("cfg2", "f32")
+    n = workloads.config("cfg2").n
+    jobs = []
+    for t in range(4):
+        X = torch.randn(50000 + 999 * t, n, generator=torch.Generator().manual_seed(t)).pin_memory()
+        jobs.append((X, torch.empty_like(X).pin_memory(), torch.empty(3 * 4096 * n, device="cuda"),
+                     torch.cuda.Stream()))
+
+    def run(job):
+        X, Y, ws, st = job
+        for _ in range(3):
+            plan.execute_host(0, X, Y, ws, 4096, st)
+        st.synchronize()
+
+    with cf.ThreadPoolExecutor(4) as ex:
+        list(ex.map(run, jobs))
+    for X, Y, _, _ in jobs:
+        ref = plan.forward(X.cuda())
+        torch.cuda.synchronize()
+        assert torch.equal(Y, ref.cpu())
 
 
 @pytest.mark.parametrize("kind,n,dtype", [("complete", 64, "f32"), ("complete", 64, "f64"),
