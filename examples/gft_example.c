@@ -2,7 +2,8 @@
  *
  * Builds the fast-GFT plan of an n-node cycle (a reflection symmetry at
  * every level), transforms a batch of signals on the GPU and back, checks the round trip,
- * Parseval's identity and the lowest coefficient of a constant signal, and prints the plan
+ * Parseval's identity and the lowest coefficient of a constant signal, saves and reloads
+ * the plan (gft_plan_serialize / _deserialize: bit-identical forward), and prints the plan
  * shape.  Device memory comes from the CUDA runtime; the library itself only needs a
  * current CUDA context (gft_forward runs on the given stream, NULL = legacy default).
  *
@@ -14,6 +15,7 @@
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <cuda_runtime_api.h>
 
@@ -83,6 +85,25 @@ int main(int argc, char** argv) {
   CHECK_GFT(gft_inverse(plan, dy, dx, batch, GFT_F32, NULL));   /* back into dx */
   CHECK_CUDA(cudaMemcpy(hz, dx, sizeof(float) * count, cudaMemcpyDeviceToHost));
 
+  /* plan persistence: serialise (size query first), reload, and the reloaded plan's
+   * forward must be bit-identical (same decomposition -> same generated kernel) */
+  size_t blob_size = 0;
+  CHECK_GFT(gft_plan_serialize(plan, NULL, 0, &blob_size));
+  void* blob = malloc(blob_size);
+  CHECK_GFT(gft_plan_serialize(plan, blob, blob_size, &blob_size));
+  gft_plan plan2;
+  CHECK_GFT(gft_plan_deserialize(&plan2, blob, blob_size, &opts));
+  free(blob);
+  float* hw = malloc(sizeof(float) * count);
+  CHECK_CUDA(cudaMemcpy(dy, hx, sizeof(float) * count, cudaMemcpyHostToDevice));
+  CHECK_GFT(gft_forward(plan2, dy, dy, batch, GFT_F32, NULL));   /* in place */
+  CHECK_CUDA(cudaMemcpy(hw, dy, sizeof(float) * count, cudaMemcpyDeviceToHost));
+  size_t mismatches = 0;
+  for (size_t i = 0; i < count; ++i) mismatches += memcmp(&hw[i], &hy[i], sizeof(float)) != 0;
+  CHECK_GFT(gft_plan_destroy(plan2));
+  free(hw);
+  printf("plan saved (%zu bytes) and reloaded: %zu mismatching outputs\n", blob_size, mismatches);
+
   double worst_rt = 0, worst_parseval = 0;
   for (long long b = 0; b < batch; ++b) {
     double nx = 0, ny = 0, nd = 0;
@@ -101,7 +122,7 @@ int main(int argc, char** argv) {
   const double c0_err = fabs(hy[0] - sqrt((double)n)) + sqrt(rest);
   printf("round trip max rel err %.2e, Parseval max dev %.2e, constant-signal error %.2e\n",
          worst_rt, worst_parseval, c0_err);
-  const int ok = worst_rt < 2e-5 && worst_parseval < 1e-5 && c0_err < 1e-4 * sqrt((double)n);
+  const int ok = worst_rt < 2e-5 && worst_parseval < 1e-5 && c0_err < 1e-4 * sqrt((double)n) && mismatches == 0;
 
   cudaFree(dx);
   cudaFree(dy);
