@@ -571,6 +571,16 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, bool pair, 
 // stager (front butterflies, hi/lo -> TMEM A, small leaves -> SMEM row) and a drainer
 // (TMEM D -> registers, back / coefficient butterflies); D double-buffered in TMEM.
 // Returns false if the TMEM layout (A + 2 D) does not fit in 512 columns.
+// Opt-in (GFT_TC_WS_A2=1): A (the staged hi/lo operand) double-buffered in TMEM when it fits
+// beside the two D buffers -- the stager of tile t+1 then waits for MMA(t-1), not MMA(t).
+// Measured back to back at n = 64 (tools/gpu_ws_a2_cmp.sh): +1.5-2% with one 64-leaf, -3%
+// with two 32-leaves, a tie on G_z -- staging is not what bounds these kernels, so one A
+// buffer stays the default.
+int ws_a_bufs(int a_cols, int d_cols) {
+  if (getenv("GFT_TC_WS_A2") == nullptr) return 1;
+  return 2 * a_cols + 2 * d_cols <= 512 ? 2 : 1;
+}
+
 bool ws_layout(std::vector<TcLeaf>& T, int& a_cols, int& d_cols, int& tmem_cols) {
   a_cols = d_cols = 0;
   for (auto& t : T) {
@@ -584,7 +594,7 @@ bool ws_layout(std::vector<TcLeaf>& T, int& a_cols, int& d_cols, int& tmem_cols)
   }
   if (a_cols + 2 * d_cols > 512) return false;
   tmem_cols = 32;
-  while (tmem_cols < a_cols + 2 * d_cols) tmem_cols *= 2;
+  while (tmem_cols < ws_a_bufs(a_cols, d_cols) * a_cols + 2 * d_cols) tmem_cols *= 2;
   return true;
 }
 
@@ -610,8 +620,10 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
             }
     }
   const size_t per_cta = B.size() / 2;
-  o << "#define GFT_B_FLOATS " << per_cta << "\n#define GFT_A_COLS " << a_cols << "\n#define GFT_D_COLS "
-    << d_cols << "\n#define GFT_SMALL " << (T.size() < P.leaves.size() ? 1 : 0) << "\n";
+  const int abufs = ws_a_bufs(a_cols, d_cols);
+  o << "#define GFT_B_FLOATS " << per_cta << "\n#define GFT_A_COLS " << a_cols << "\n#define GFT_A_BUFS " << abufs
+    << "\n#define GFT_D_BASE " << abufs * a_cols << "\n#define GFT_D_COLS " << d_cols << "\n#define GFT_SMALL "
+    << (T.size() < P.leaves.size() ? 1 : 0) << "\n";
   o << "__device__ __align__(16) const float gft_tcB[2][" << per_cta << "] = {\n";
   for (size_t i = 0; i < B.size(); ++i) {
     char buf[48];
@@ -629,7 +641,7 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
   if (d != DIR_INV) emit_units(o, P, "x", false, dtype);
   if (d == DIR_FILTER && !P.post.empty()) fail(GFT_ERR_COMPILE, "filter plan with right Haar stages");
   if (d == DIR_INV) emit_post_units(o, P, "x", true, "float");
-  o << "  if (await_a) { mbar_wait(abar, apar); tc_fence_after(); }   // MMA(t-1) has read A\n";
+  o << "  if (await_a) { mbar_wait(abar, apar); tc_fence_after(); }   // the MMAs that last read this A buffer are done\n";
   for (const TcLeaf& t : T) {
     const Leaf& lf = P.leaves[t.leaf];
     for (int c0 = 0; c0 < t.kp8; c0 += 32) {

@@ -17,10 +17,12 @@
 //                             WG2 drops to 56, the stager rises to 248, the drainer to 200).
 // The stager of tile t+1 only waits for MMA(t) to have READ the A columns (mma_done(t)),
 // so staging t+1, the MMAs of t and the drain of t-1 run concurrently.
-// TMEM: A = all leaves' hi/lo columns (single buffer), D = all leaves' D columns x 2.
+// With GFT_A_BUFS == 2 the A columns are double-buffered too (tile t uses A[t % 2]) and the
+// stager of tile t+1 only waits for MMA(t-1).
+// TMEM: A = all leaves' hi/lo columns (x GFT_A_BUFS), D = all leaves' D columns x 2.
 // Generated part: GFT_N, GFT_STAGES, GFT_TMEM_COLS, GFT_B_FLOATS, GFT_KNAME, gft_tcB[2][],
-// GFT_A_COLS (D buffer 0 base), GFT_D_COLS (per buffer), GFT_SMALL (1 if CUDA-core leaves
-// exist), gft_stage(), gft_drain(), gft_issue_ws().
+// GFT_A_COLS (per A buffer), GFT_A_BUFS, GFT_D_BASE (D buffer 0 base), GFT_D_COLS (per
+// buffer), GFT_SMALL (1 if CUDA-core leaves exist), gft_stage(), gft_drain(), gft_issue_ws().
 typedef unsigned int u32;
 typedef unsigned long long u64;
 typedef float elem_t;
@@ -175,17 +177,18 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   unsigned char* outbuf = smem + GFT_STAGES * GFT_TILE_BYTES;
   unsigned char* bsm = smem + (GFT_STAGES + GFT_IO_SPLIT) * GFT_TILE_BYTES;   // this CTA's half of B
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(bsm + GFT_B_FLOATS * 4);
-  // bars: full[S], done[S] (= input free when IO-split), rows[S], staged, mma_done[2],
-  // d_free[2], out_ready, out_free
+  // bars: full[S], done[S] (= input free when IO-split), rows[S], staged[2], mma_done[2],
+  // d_free[2], out_ready, out_free (staged alternates per tile, so a stager running a tile
+  // ahead -- two A buffers -- can never complete a phase the issuer has not yet observed)
   unsigned long long* b_full = bars;
   unsigned long long* b_done = bars + GFT_STAGES;
   unsigned long long* b_rows = bars + 2 * GFT_STAGES;
   unsigned long long* b_staged = bars + 3 * GFT_STAGES;
-  unsigned long long* b_mma = bars + 3 * GFT_STAGES + 1;
-  unsigned long long* b_dfree = bars + 3 * GFT_STAGES + 3;
-  unsigned long long* b_outrdy = bars + 3 * GFT_STAGES + 5;
-  unsigned long long* b_outfree = bars + 3 * GFT_STAGES + 6;
-  u32* tmem_slot = reinterpret_cast<u32*>(bars + 3 * GFT_STAGES + 7);
+  unsigned long long* b_mma = bars + 3 * GFT_STAGES + 2;
+  unsigned long long* b_dfree = bars + 3 * GFT_STAGES + 4;
+  unsigned long long* b_outrdy = bars + 3 * GFT_STAGES + 6;
+  unsigned long long* b_outfree = bars + 3 * GFT_STAGES + 7;
+  u32* tmem_slot = reinterpret_cast<u32*>(bars + 3 * GFT_STAGES + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const u32 rank = cluster_rank();
   const long long npairs = (batch + 2 * GFT_TILE_ROWS - 1) / (2 * GFT_TILE_ROWS);
@@ -205,8 +208,8 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       mbar_init(smem_u32(&b_done[s]), 4);
       mbar_init(smem_u32(&b_rows[s]), 4);
     }
-    mbar_init(smem_u32(b_staged), 8);
     for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&b_staged[b]), 8);
       mbar_init(smem_u32(&b_mma[b]), 1);
       mbar_init(smem_u32(&b_dfree[b]), 8);
     }
@@ -300,14 +303,14 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       for (long long it = 0;; ++it) {
         if (pid0 + it * npid >= npairs) break;
         const int b = (int)(it & 1);
-        mbar_wait_acq_cluster(smem_u32(b_staged), (u32)(it & 1));
+        mbar_wait_acq_cluster(smem_u32(&b_staged[b]), (u32)((it >> 1) & 1));
         if (it >= 2) mbar_wait_acq_cluster(smem_u32(&b_dfree[b]), (u32)(((it >> 1) - 1) & 1));
         tc_fence_after();
         // re-materialise the B base each tile so the ~100 MMA descriptors are not hoisted
         // out of the loop into registers (this warpgroup runs with 56 registers)
         u32 bs;
         asm volatile("mov.b32 %0, %1;" : "=r"(bs) : "r"(bsm_s));
-        gft_issue_ws(tmem, tmem + (u32)(GFT_A_COLS + b * GFT_D_COLS), bs);
+        gft_issue_ws(tmem + (u32)((GFT_A_BUFS == 2 ? b : 0) * GFT_A_COLS), tmem + (u32)(GFT_D_BASE + b * GFT_D_COLS), bs);
         tc_commit_pair(smem_u32(&b_mma[b]));
       }
     }
@@ -315,7 +318,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
     // ---------------- stager (row = TMEM lane = tid) ----------------
     reg_stager();
     const u32 tm_a = tmem + ((u32)(warp * 32) << 16);
-    const u32 staged0 = map_to_cta(smem_u32(b_staged), 0);
+    const u32 staged0[2] = {map_to_cta(smem_u32(&b_staged[0]), 0), map_to_cta(smem_u32(&b_staged[1]), 0)};
     for (long long it = 0;; ++it) {
       const long long p = pid0 + it * npid;
       if (p >= npairs) break;
@@ -328,8 +331,14 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&b_done[s]));   // input rows consumed: refill
 #endif
-      // before writing the A columns: the MMAs of the previous tile have read them
-      gft_stage(x, tm_a, staged0, buf, tid, smem_u32(&b_mma[(it - 1) & 1]), (u32)(((it - 1) >> 1) & 1), it >= 1);
+      // before writing the A columns: the MMAs that last read this A buffer (tile t-1, or
+      // t-2 with two buffers) are done
+#if GFT_A_BUFS == 2
+      gft_stage(x, tm_a + (u32)((it & 1) * GFT_A_COLS), staged0[it & 1], buf, tid, smem_u32(&b_mma[it & 1]),
+                (u32)(((it - 2) >> 1) & 1), it >= 2);
+#else
+      gft_stage(x, tm_a, staged0[it & 1], buf, tid, smem_u32(&b_mma[(it - 1) & 1]), (u32)(((it - 1) >> 1) & 1), it >= 1);
+#endif
 #if GFT_SMALL
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&b_rows[s]));   // release: small-leaf outputs in SMEM
@@ -357,7 +366,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       unsigned char* buf = stages + s * GFT_TILE_BYTES;
 #endif
       float y[GFT_N];
-      gft_drain(y, tmem + lane_off + (u32)(GFT_A_COLS + b * GFT_D_COLS), buf, row);
+      gft_drain(y, tmem + lane_off + (u32)(GFT_D_BASE + b * GFT_D_COLS), buf, row);
       // D[b] read (tcgen05.ld waited inside gft_drain): let the issuer reuse it
       tc_fence_before();
       __syncwarp();

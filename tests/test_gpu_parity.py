@@ -435,6 +435,38 @@ def test_tensor_core_io_split_experiment(monkeypatch):
     assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
 
 
+@pytest.mark.parametrize("leaves", [1, 2])
+def test_tensor_core_ws_double_a_experiment(monkeypatch, leaves):
+    """Opt-in double-buffered A operand of the warp-specialised kernel (GFT_TC_WS_A2=1): a
+    64-node graph with one 64-leaf (no symmetry: random weights) or a mirror-symmetric one
+    with two 32-leaves, forward / inverse vs the oracle over several tiles + a ragged tail."""
+    rng = np.random.default_rng(7 + leaves)
+    n = 64
+    if leaves == 1:
+        pairs = [(i, j) for i in range(n) for j in range(i + 1, n) if rng.random() < 0.15]
+        w = rng.uniform(0.5, 2.0, len(pairs))
+    else:
+        half = [(i, j) for i in range(32) for j in range(i + 1, 32) if rng.random() < 0.2]
+        wh = rng.uniform(0.5, 2.0, len(half))
+        pairs = half + [(63 - i, 63 - j) for i, j in half] + [(i, 63 - i) for i in range(32)]
+        w = np.concatenate([wh, wh, np.full(32, 0.7)])
+    s = np.array([p[0] for p in pairs], np.int32)
+    d = np.array([p[1] for p in pairs], np.int32)
+    monkeypatch.setenv("GFT_TC_WS_A2", "1")
+    plan = G.Plan(n, s, d, w, dtypes=("f32",), no_cubin_cache=True)
+    monkeypatch.delenv("GFT_TC_WS_A2")
+    src = plan.kernel_source(G.K_FAST_FWD, "f32")
+    assert "tc3_" in plan.kernel_name(G.K_FAST_FWD) and "#define GFT_A_BUFS 2" in src
+    assert plan.leaf_sizes() == ([64] if leaves == 1 else [32, 32])
+    lam_o, U_o = oracle.gft_basis(oracle.laplacian(n, s, d, w))
+    X = torch.randn(5000, n, generator=torch.Generator().manual_seed(leaves))
+    Y = plan.forward(X.cuda())
+    Xr = plan.inverse(Y)
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
+
+
 @pytest.mark.parametrize("batch", [1, 3, 4, 130, 1001])
 def test_superrow_tma_mode_experiment(monkeypatch, batch):
     """Opt-in super-row TMA mode for odd row pitch (GFT_SUPERROW=1): cfg3 with batches
