@@ -247,10 +247,11 @@ constexpr int64_t kMaxRowsPerLaunch = (int64_t)1 << 30;
 
 }  // namespace
 
-bool tuned_geometry(int n, int dtype, int64_t work, int& R, int& S, int& W) {
-  // lines: "fma <n> <f32|f64> <R> <S> <W> [work=<FMAs per signal>]"; an entry with a work key
-  // applies only to kernels with exactly that much leaf work (plan-specific measurement)
-  struct Entry { int n, dt, R, S, W; int64_t work; };
+bool tuned_geometry(int n, int dtype, int64_t work, int& R, int& S, int& W, int& pace_ns) {
+  // lines: "fma <n> <f32|f64> <R> <S> <W> [work=<FMAs per signal>] [pace=<ns>]"; an entry with
+  // a work key applies only to kernels with exactly that much leaf work (plan-specific
+  // measurement); pace = per-tile __nanosleep of the FMA skeleton (0 = none)
+  struct Entry { int n, dt, R, S, W, pace; int64_t work; };
   static const std::vector<Entry> table = [] {
     std::vector<Entry> t;
     const char* e = getenv("GFT_TUNING_FILE");
@@ -265,7 +266,11 @@ bool tuned_geometry(int n, int dtype, int64_t work, int& R, int& S, int& W) {
       if (!(ss >> mode >> x.n >> dt >> x.R >> x.S >> x.W) || mode != "fma") continue;
       x.dt = dt == "f64" ? GFT_F64 : GFT_F32;
       x.work = -1;
-      if ((ss >> extra) && extra.rfind("work=", 0) == 0) x.work = std::atoll(extra.c_str() + 5);
+      x.pace = 0;
+      while ((ss >> extra) && extra[0] != '#') {
+        if (extra.rfind("work=", 0) == 0) x.work = std::atoll(extra.c_str() + 5);
+        else if (extra.rfind("pace=", 0) == 0) x.pace = std::atoi(extra.c_str() + 5);
+      }
       t.push_back(x);
     }
     return t;
@@ -277,7 +282,7 @@ bool tuned_geometry(int n, int dtype, int64_t work, int& R, int& S, int& W) {
       if (x.work == work) break;
     }
   if (!hit) return false;
-  R = hit->R; S = hit->S; W = hit->W;
+  R = hit->R; S = hit->S; W = hit->W; pace_ns = hit->pace;
   return true;
 }
 

@@ -235,6 +235,14 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       }
       fence_proxy_async();
       __syncwarp();
+#if defined(GFT_PACE_NS)
+      // request pacing (tuning.tsv pace=): with few warps per SM and little arithmetic per
+      // row, warps finishing together issue their store + refill in bursts; a short sleep
+      // spreads them out.  Measured on cfg3 (n = 25, 1 CTA x 4 warps x 3 stages of 96 rows):
+      // 5.91 -> 6.31 TB/s for 300-500 ns, a loss on the configs already at the HBM roof
+      // (profiles/r01/autotune/pace_*.log)
+      __nanosleep(GFT_PACE_NS);
+#endif
       if (lane == 0) {
         issue_store(t, s);
         // the buffer consumed in the previous iteration is free once its store has read it

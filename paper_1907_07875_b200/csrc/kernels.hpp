@@ -23,6 +23,7 @@ struct KernelCfg {
   int pack = 1;                 // signals per TMA row of the packed view (mode 2)
   int boxc = 0, swz_mask = 0;   // TMA box columns, swizzle mask (7/3/1/0)
   int vec = 1;                  // elements per SMEM vector access
+  int pace_ns = 0;              // FMA skeleton: per-tile __nanosleep before the store (tuning.tsv pace=)
   // tensor-core variant (kernel_tc_skeleton.cuh): one 128-row tile per CTA iteration,
   // 4 compute warps + 1 TMA warp, big leaves as tcgen05 3xTF32 micro-GEMMs
   int tc = 0;
@@ -88,6 +89,6 @@ std::string cubin_cache_dir();
 // Measured geometry table (paper_1907_07875_b200/tuning.tsv, written by
 // tools/gpu_autotune.py on a B200): lines "fma <n> <f32|f64> <R> <S> <W>".  Returns false
 // if (n, dtype) has no entry.  GFT_TUNING_FILE overrides the path ("none" disables).
-bool tuned_geometry(int n, int dtype, int64_t work, int& R, int& S, int& W);
+bool tuned_geometry(int n, int dtype, int64_t work, int& R, int& S, int& W, int& pace_ns);
 
 }  // namespace gft
