@@ -53,6 +53,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--round", default="r01")
     ap.add_argument("--dir", default=os.path.join(ROOT, "gpurun_out"))
+    ap.add_argument("--merge", action="store_true",
+                    help="keep the rows of profiles/ncu_summary.json not re-captured this time")
     a = ap.parse_args()
     outdir = os.path.join(ROOT, "profiles", a.round)
     os.makedirs(outdir, exist_ok=True)
@@ -81,6 +83,14 @@ def main():
         if rb is not None:
             row["dram_bytes_per_launch"] = to_bytes(rb, ru) + to_bytes(wb, wu)
         rows.append(row)
+    if a.merge:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            old_rows = json.load(f)["kernels"]
+        fresh = {(r["config"], r["kind"], r["tag"]) for r in rows}
+        rows = [r for r in old_rows if (r["config"], r["kind"], r["tag"]) not in fresh] + rows
+        order = ["cfg1big", "cfg2", "cfg2b", "cfg3", "cfg4", "cfg5a", "cfg5b"]
+        rows.sort(key=lambda r: (order.index(r["config"]) if r["config"] in order else 99, r["kind"],
+                                 r["tag"] or ""))
     # launch list
     shares = {}
     lc = os.path.join(a.dir, "launches.csv")
