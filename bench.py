@@ -257,6 +257,14 @@ def right_haar_table(args, stream, hbm, device):
                 ms = time_kernel(lambda: f(X, Y, stream), stream, 3, args.table_iters)
                 r[KIND_NAMES[k]] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
                                     "frac": round(nbytes / ms / 1e6 / hbm, 4)}
+            # measured pacing (gft_plan_tune) for FMA-skeleton kernels, then re-timed
+            paces = plan.tune(dtype, (0, 1), X, Y, stream=stream)
+            for k, f in ((0, plan.forward), (1, plan.inverse)):
+                if k in paces:
+                    ms = time_kernel(lambda: f(X, Y, stream), stream, 3, args.table_iters)
+                    r[KIND_NAMES[k] + "_tuned"] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
+                                                   "frac": round(nbytes / ms / 1e6 / hbm, 4),
+                                                   "pace_ns": paces[k]}
             row[tag] = r
             plan.close()
         row["right_vs_one_block_fwd"] = round(row["one_block"]["fast_fwd"]["ms"] / row["right_haar"]["fast_fwd"]["ms"], 3)
@@ -313,6 +321,12 @@ def approx_table(args, stream, hbm, device):
         else:
             Uh = plan.basis()
             row.update(delta=round(delta(Uh, exact[label]), 5), epsilon=round(eps(Uh, exact[label]), 5))
+        # measured pacing (gft_plan_tune) for FMA-skeleton kernels, then re-timed
+        paces = plan.tune("f32", (0,), X, Y, stream=stream)
+        if 0 in paces:
+            ms = time_kernel(lambda: plan.forward(X, Y, stream), stream, 3, args.table_iters)
+            row["fast_fwd_tuned"] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
+                                     "frac": round(nbytes / ms / 1e6 / hbm, 4), "pace_ns": paces[0]}
         rows.append(row)
         plan.close()
     return rows

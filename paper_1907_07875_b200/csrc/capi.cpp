@@ -364,6 +364,67 @@ gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask)
   });
 }
 
+gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, const void* X, void* Y,
+                         int64_t batch, int32_t reps, gft_stream stream, int32_t* pace_ns_out) {
+  return guard([&] {
+    if (!plan) gft::fail(GFT_ERR_INVALID_ARG, "NULL plan");
+    if (batch <= 0) gft::fail(GFT_ERR_INVALID_ARG, "batch must be > 0");
+    check_io(X, Y);
+    if (X == Y) gft::fail(GFT_ERR_INVALID_ARG, "X and Y must be distinct buffers");
+    if (kinds_mask == 0) kinds_mask = (1u << gft::K_FAST_FWD) | (1u << gft::K_FAST_INV);
+    if (kinds_mask >> (gft::K_DENSE_INV + 1)) gft::fail(GFT_ERR_INVALID_ARG, "kinds_mask: bits 0..3 only");
+    if (reps <= 0) reps = 10;
+    if (pace_ns_out)
+      for (int i = 0; i < 4; ++i) pace_ns_out[i] = -1;
+    static const int kCand[] = {0, 150, 300, 450};
+    const bool cache = !(plan->flags & GFT_FLAG_NO_CUBIN_CACHE);
+    const bool allow_tc = !(plan->flags & GFT_FLAG_NO_TENSOR_CORES);
+    const bool dense_tc = (plan->flags & GFT_FLAG_DENSE_TC) != 0;
+    for (int kind = gft::K_FAST_FWD; kind <= gft::K_DENSE_INV; ++kind) {
+      if (!(kinds_mask & (1u << kind))) continue;
+      gft::Kernel& cur = kernel_of(plan, kind, dtype);
+      if (cur.cfg.tc) continue;
+      // candidates: generated and compiled in parallel (NVRTC unless already cached)
+      std::vector<std::unique_ptr<gft::Kernel>> cand;
+      for (int pace : kCand) {
+        cand.emplace_back(new gft::Kernel);
+        gft::generate_kernel(plan->P, kind, dtype, *cand.back(), allow_tc, dense_tc, pace);
+      }
+      std::vector<gft::Error> errs(cand.size(), gft::Error{GFT_OK, ""});
+      std::vector<std::thread> th;
+      for (size_t i = 0; i < cand.size(); ++i)
+        th.emplace_back([&, i] {
+          try {
+            std::lock_guard<std::mutex> lk(cand[i]->mu);
+            gft::compile_kernel(*cand[i], cache);
+          } catch (const gft::Error& e) {
+            errs[i] = e;
+          }
+        });
+      for (auto& t : th) t.join();
+      for (auto& e : errs)
+        if (e.status != GFT_OK) throw e;
+      const double t_cur = gft::time_kernel_ms(cur, X, Y, batch, stream, 2, reps, cache);
+      double best = t_cur;
+      int best_i = -1;
+      for (size_t i = 0; i < cand.size(); ++i) {
+        if (cand[i]->name == cur.name) continue;   // same code as the current kernel
+        const double t = gft::time_kernel_ms(*cand[i], X, Y, batch, stream, 2, reps, cache);
+        if (t < best) { best = t; best_i = (int)i; }
+      }
+      int chosen = cur.cfg.pace_ns;
+      if (best_i >= 0 && best < 0.99 * t_cur) {
+        gft::unload_kernel(cur);
+        plan->k[dtype][kind] = std::move(cand[best_i]);
+        chosen = kCand[best_i];
+      }
+      for (auto& c : cand)
+        if (c) gft::unload_kernel(*c);
+      if (pace_ns_out) pace_ns_out[kind] = chosen;
+    }
+  });
+}
+
 gft_status gft_plan_info_get(gft_plan plan, gft_plan_info* info) {
   return guard([&] {
     if (!plan || !info) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");

@@ -722,7 +722,8 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
 
 }  // namespace
 
-void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc, bool dense_tc) {
+void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc, bool dense_tc,
+                     int pace_ns) {
   if (dense_tc && allow_tc && (kind == K_DENSE_FWD || kind == K_DENSE_INV)) {
     // dense U^T x on tensor cores: the whole basis as ONE leaf (no butterflies), generated by
     // the same tcgen05 path -- the strongest dense comparison for n >= 32
@@ -748,6 +749,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
   k.kind = kind;
   k.dtype = dtype;
   k.cfg = choose_cfg(P.n, dtype, (kind == K_DENSE_FWD || kind == K_DENSE_INV) ? (int64_t)P.n * P.n : P.sum_k2);
+  if (pace_ns >= 0) k.cfg.pace_ns = pace_ns;
   static const char* kKindNameTC[] = {"fwdtc", "invtc", "", "", "filttc"};
   const Dir dir = kind == K_FAST_INV ? DIR_INV : kind == K_FILTER ? DIR_FILTER : DIR_FWD;
   if (allow_tc && (kind == K_FAST_FWD || kind == K_FAST_INV || kind == K_FILTER)) {

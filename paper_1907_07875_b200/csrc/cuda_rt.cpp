@@ -51,6 +51,9 @@ struct Driver {
   CUresult (*cuEventCreate)(CUevent*, unsigned);
   CUresult (*cuEventRecord)(CUevent, CUstream);
   CUresult (*cuStreamWaitEvent)(CUstream, CUevent, unsigned);
+  CUresult (*cuEventSynchronize)(CUevent);
+  CUresult (*cuEventElapsedTime)(float*, CUevent, CUevent);
+  CUresult (*cuEventDestroy)(CUevent);
 };
 
 struct Nvrtc {
@@ -94,7 +97,8 @@ Driver& drv() {
   GFT_GET(cuFuncGetAttribute); GFT_GET(cuOccupancyMaxActiveBlocksPerMultiprocessor);
   GFT_GET(cuLaunchKernel); GFT_GET(cuLaunchKernelEx); GFT_GET(cuTensorMapEncodeTiled); GFT_GET(cuMemcpyHtoDAsync);
   GFT_GET(cuMemcpyDtoHAsync); GFT_GET(cuStreamCreate); GFT_GET(cuEventCreate);
-  GFT_GET(cuEventRecord); GFT_GET(cuStreamWaitEvent);
+  GFT_GET(cuEventRecord); GFT_GET(cuStreamWaitEvent); GFT_GET(cuEventSynchronize);
+  GFT_GET(cuEventElapsedTime); GFT_GET(cuEventDestroy);
 #undef GFT_GET
   if (!ok) return d;
   CUresult r = d.cuInit(0);
@@ -376,6 +380,35 @@ void launch_kernel(Kernel& k, const void* in, void* out, int64_t batch, void* st
     lc.numAttrs = 1;
     ck(d.cuLaunchKernelEx(&lc, (CUfunction)L.fn, args, nullptr), "cuLaunchKernelEx");
   }
+}
+
+double time_kernel_ms(Kernel& k, const void* in, void* out, int64_t batch, void* stream, int warm,
+                      int reps, bool allow_cache) {
+  Driver& d = need_driver();
+  current_ctx(stream);
+  for (int i = 0; i < warm; ++i) launch_kernel(k, in, out, batch, stream, allow_cache);
+  CUevent a, b;
+  ck(d.cuEventCreate(&a, CU_EVENT_DEFAULT), "cuEventCreate");
+  if (d.cuEventCreate(&b, CU_EVENT_DEFAULT) != CUDA_SUCCESS) {
+    d.cuEventDestroy(a);
+    fail(GFT_ERR_CUDA, "cuEventCreate");
+  }
+  float ms = 0.f;
+  CUresult r = d.cuEventRecord(a, (CUstream)stream);
+  try {
+    for (int i = 0; i < reps && r == CUDA_SUCCESS; ++i) launch_kernel(k, in, out, batch, stream, allow_cache);
+  } catch (...) {
+    d.cuEventDestroy(a);
+    d.cuEventDestroy(b);
+    throw;
+  }
+  if (r == CUDA_SUCCESS) r = d.cuEventRecord(b, (CUstream)stream);
+  if (r == CUDA_SUCCESS) r = d.cuEventSynchronize(b);
+  if (r == CUDA_SUCCESS) r = d.cuEventElapsedTime(&ms, a, b);
+  d.cuEventDestroy(a);
+  d.cuEventDestroy(b);
+  ck(r, "timing events");
+  return (double)ms / std::max(1, reps);
 }
 
 void unload_kernel(Kernel& k) {

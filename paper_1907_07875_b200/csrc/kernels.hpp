@@ -68,7 +68,9 @@ struct Kernel {
 // Emits the full CUDA source (prelude + gft_body + skeleton) for a plan.
 // allow_tc: fast kernels of fp32 plans with leaves >= 32 use the tcgen05 3xTF32 skeleton.
 // dense_tc: the dense comparison kernels use the tcgen05 path (whole basis as one leaf).
-void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc, bool dense_tc = false);
+// pace_ns >= 0 overrides the FMA skeleton's request pacing (gft_plan_tune candidates).
+void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc, bool dense_tc = false,
+                     int pace_ns = -1);
 
 // Compiles k.source to an sm_100a cubin (AOT cache lookup first unless disabled).
 void compile_kernel(Kernel& k, bool allow_cache);
@@ -78,6 +80,10 @@ void launch_kernel(Kernel& k, const void* in, void* out, int64_t batch, void* st
 void kernel_launch_config(Kernel& k, int64_t batch, int* grid, int* block, int* smem, int* regs,
                           bool allow_cache);
 void unload_kernel(Kernel& k);
+// Mean ms of `reps` back-to-back launches of `k` (after `warm` untimed ones), timed with
+// driver events on `stream`; synchronous (gft_plan_tune).
+double time_kernel_ms(Kernel& k, const void* in, void* out, int64_t batch, void* stream, int warm,
+                      int reps, bool allow_cache);
 
 // Host<->device pipelined execution (gft_execute_host).
 struct HostExec;

@@ -1,0 +1,59 @@
+"""gft_plan_tune (measured request pacing): the tuned kernels compute
+bit-identical outputs (only the per-tile sleep differs), the chosen pacing is one of the
+candidates, tensor-core kernels are left alone, and bad arguments fail loudly."""
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import workloads  # noqa: E402
+from paper_1907_07875_b200 import gft  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+CAND = {0, 150, 300, 450}
+
+
+@pytest.mark.parametrize("name,dtype", [("cfg3", "f32"), ("cfg2b", "f32"), ("cfg4", "f64")])
+def test_tune_bit_identical(name, dtype):
+    cfg = workloads.config(name)
+    plan = gft.Plan.from_config(cfg, dtypes=(dtype,))
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(11)
+    X = torch.randn(300_001, cfg.n, generator=g, device="cuda", dtype=tdt)   # ragged tail
+    Y0 = plan.forward(X)
+    Z0 = plan.inverse(Y0)
+    paces = plan.tune(dtype, (0, 1), batch=1 << 18, reps=3)
+    assert set(paces) == {0, 1} and set(paces.values()) <= CAND
+    Y1 = plan.forward(X)
+    Z1 = plan.inverse(Y1)
+    torch.cuda.synchronize()
+    assert torch.equal(Y0, Y1) and torch.equal(Z0, Z1)
+    plan.close()
+
+
+def test_tune_skips_tensor_core_kernels():
+    cfg = workloads.config("cfg5b")
+    plan = gft.Plan.from_config(cfg, dtypes=("f32",))
+    assert "tc" in plan.kernel_name(0, "f32")
+    name = plan.kernel_name(0, "f32")
+    paces = plan.tune("f32", (0, 1), batch=1 << 12, reps=1)
+    assert paces == {} and plan.kernel_name(0, "f32") == name
+    plan.close()
+
+
+def test_tune_errors():
+    cfg = workloads.config("cfg1")
+    plan = gft.Plan.from_config(cfg, dtypes=("f32",))
+    X = torch.randn(4096, 8, device="cuda")
+    with pytest.raises(gft.GFTError, match="INVALID_ARG"):
+        gft.gft_plan_tune(plan._h, "f32", 3, X, X, 4096)          # X == Y
+    with pytest.raises(gft.GFTError, match="INVALID_ARG"):
+        gft.gft_plan_tune(plan._h, "f32", 1 << 5, X, torch.empty_like(X), 4096)
+    with pytest.raises(gft.GFTError, match="INVALID_ARG"):
+        gft.gft_plan_tune(plan._h, "f32", 3, X, torch.empty_like(X), 0)
+    with pytest.raises(gft.GFTError, match="UNSUPPORTED"):
+        gft.gft_plan_tune(plan._h, "f64", 3, X, torch.empty_like(X), 4096)
+    # the plan still works and matches the oracle-free identity round trip
+    Y = plan.forward(X)
+    Z = plan.inverse(Y)
+    assert float((Z - X).norm() / X.norm()) < 1e-5
+    plan.close()
