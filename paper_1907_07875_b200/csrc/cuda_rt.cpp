@@ -6,6 +6,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -217,6 +218,21 @@ LoadedFn& ensure_loaded(Kernel& k, CUcontext ctx, bool allow_cache) {
   return k.loaded.emplace(ctx, L).first->second;
 }
 
+std::atomic<uint64_t> g_kernel_uid{1};
+
+// Per-thread cache of the last tensor maps built for a (kernel, in, out, rows) launch: a
+// serving loop that re-launches on the same buffers skips two cuTensorMapEncodeTiled calls.
+struct MapCacheEntry {
+  uint64_t uid = 0;
+  const void* in = nullptr;
+  void* out = nullptr;
+  int64_t rows = -1;
+  CUtensorMap tin, tout;
+};
+constexpr int kMapCacheWays = 4;
+thread_local MapCacheEntry t_map_cache[kMapCacheWays];
+thread_local int t_map_next = 0;
+
 void encode_map(CUtensorMap* m, const Kernel& k, const void* ptr, int64_t rows) {
   Driver& d = need_driver();
   const KernelCfg& c = k.cfg;
@@ -354,8 +370,22 @@ void launch_kernel(Kernel& k, const void* in, void* out, int64_t batch, void* st
     std::memset(&tin, 0, sizeof tin);
     std::memset(&tout, 0, sizeof tout);
     if (c.mode == 0 || (c.mode == 2 && rows >= c.pack)) {
-      encode_map(&tin, k, pin, rows);
-      encode_map(&tout, k, pout, rows);
+      MapCacheEntry* hit = nullptr;
+      for (auto& e : t_map_cache)
+        if (e.uid == k.uid && e.in == pin && e.out == pout && e.rows == rows) { hit = &e; break; }
+      if (!hit) {
+        hit = &t_map_cache[t_map_next];
+        t_map_next = (t_map_next + 1) % kMapCacheWays;
+        hit->uid = 0;   // invalid until both maps are encoded
+        encode_map(&hit->tin, k, pin, rows);
+        encode_map(&hit->tout, k, pout, rows);
+        hit->uid = k.uid;
+        hit->in = pin;
+        hit->out = pout;
+        hit->rows = rows;
+      }
+      std::memcpy(&tin, &hit->tin, sizeof tin);
+      std::memcpy(&tout, &hit->tout, sizeof tout);
     }
     const int64_t tiles = (rows + c.tile_rows() - 1) / c.tile_rows();
     int64_t ctas = (tiles + c.tiles_per_cta() - 1) / c.tiles_per_cta();
@@ -505,5 +535,7 @@ void execute_host(Kernel& k, const void* in_host, void* out_host, int64_t batch,
   ck(d.cuEventRecord(hs.done[0], sd), "cuEventRecord");
   ck(d.cuStreamWaitEvent((CUstream)stream, hs.done[0], 0), "cuStreamWaitEvent");
 }
+
+Kernel::Kernel() : uid(g_kernel_uid.fetch_add(1)) {}
 
 }  // namespace gft

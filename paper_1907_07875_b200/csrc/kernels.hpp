@@ -56,6 +56,8 @@ struct LoadedFn {
 };
 
 struct Kernel {
+  Kernel();
+  uint64_t uid;             // process-unique id (keys the per-thread tensor-map cache)
   int kind = 0, dtype = 0;
   KernelCfg cfg;
   std::string name, source;

@@ -138,19 +138,33 @@ def _ptr(a):
 
 
 def _dev_ptr(t):
-    """Device address of a torch tensor (or an int address)."""
+    """Device address of a torch tensor (or an int address), as an int (ctypes converts it
+    for c_void_p arguments)."""
     if isinstance(t, int):
-        return c_void_p(t)
-    return c_void_p(t.data_ptr())
+        return t
+    return t.data_ptr()
 
 
-def _stream_handle(stream):
+_raw_stream = None
+
+
+def _stream_handle(stream, device_index=None):
+    """CUstream handle (int): the given torch stream / raw handle, else the current stream of
+    `device_index` (default: the current device)."""
+    global _raw_stream
     if stream is None:
         import torch
-        return c_void_p(torch.cuda.current_stream().cuda_stream)
+        if _raw_stream is None:
+            # the raw-handle query avoids building a torch.cuda.Stream object per call (~2 us)
+            _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", False)
+        if device_index is None:
+            device_index = torch.cuda.current_device()
+        if _raw_stream:
+            return _raw_stream(device_index)
+        return torch.cuda.current_stream(device_index).cuda_stream
     if isinstance(stream, int):
-        return c_void_p(stream)
-    return c_void_p(stream.cuda_stream)
+        return stream
+    return stream.cuda_stream
 
 
 def _dtype_code(dtype):
@@ -226,7 +240,10 @@ def gft_plan_deserialize(data, opts=None):
 
 
 def _run(fn, h, a, b, batch, dtype, stream):
-    _check(fn(h, _dev_ptr(a), _dev_ptr(b), int(batch), _dtype_code(dtype), _stream_handle(stream)))
+    dev = None if isinstance(a, int) else a.get_device()
+    st = fn(h, _dev_ptr(a), _dev_ptr(b), int(batch), _dtype_code(dtype), _stream_handle(stream, dev))
+    if st:
+        _check(st)
 
 
 def gft_forward(h, X, Y, batch, dtype=GFT_F32, stream=None):
@@ -498,14 +515,15 @@ class Plan:
         import torch
         if not a.is_cuda:
             raise ValueError("device tensors required (use execute_host for host buffers)")
-        if a.dim() != 2 or a.shape[1] != self.n or not a.is_contiguous():
+        shape = a.shape
+        if len(shape) != 2 or shape[1] != self.n or not a.is_contiguous():
             raise ValueError("expected a contiguous [batch, %d] tensor" % self.n)
         if b is None:
             b = torch.empty_like(a)
-        dt = GFT_F64 if a.dtype == torch.float64 else GFT_F32
-        if a.dtype not in (torch.float32, torch.float64) or b.dtype != a.dtype:
+        adt = a.dtype
+        if b.dtype != adt or (adt is not torch.float32 and adt is not torch.float64):
             raise ValueError("float32/float64 tensors of equal dtype required")
-        fn(self._h, a, b, a.shape[0], dt, stream)
+        fn(self._h, a, b, shape[0], GFT_F64 if adt is torch.float64 else GFT_F32, stream)
         return b
 
     def execute_host(self, direction, in_host, out_host, workspace, chunk_rows, stream=None):
