@@ -264,7 +264,7 @@ def right_haar_table(args, stream, hbm, device):
                     ms = time_kernel(lambda: f(X, Y, stream), stream, 3, args.table_iters)
                     r[KIND_NAMES[k] + "_tuned"] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
                                                    "frac": round(nbytes / ms / 1e6 / hbm, 4),
-                                                   "pace_ns": paces[k]}
+                                                   "geometry_pace": paces[k]}
             row[tag] = r
             plan.close()
         row["right_vs_one_block_fwd"] = round(row["one_block"]["fast_fwd"]["ms"] / row["right_haar"]["fast_fwd"]["ms"], 3)
@@ -326,7 +326,7 @@ def approx_table(args, stream, hbm, device):
         if 0 in paces:
             ms = time_kernel(lambda: plan.forward(X, Y, stream), stream, 3, args.table_iters)
             row["fast_fwd_tuned"] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
-                                     "frac": round(nbytes / ms / 1e6 / hbm, 4), "pace_ns": paces[0]}
+                                     "frac": round(nbytes / ms / 1e6 / hbm, 4), "geometry_pace": paces[0]}
         rows.append(row)
         plan.close()
     return rows

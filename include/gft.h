@@ -231,26 +231,32 @@ GFT_API gft_status gft_filter_destroy(gft_filter f);
  * 0 = all) now instead of at first launch, one host thread per kernel.  Needs no GPU. */
 GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask);
 
-/* Measured tuning of the FMA-skeleton request pacing (DESIGN.md §4 "Request pacing"; the
- * analogue of FFTW_MEASURE — not part of the paper's method, which fixes only the arithmetic).
- * For every kernel kind in kinds_mask (bits as in gft_plan_compile; 0 = fast-fwd | fast-inv)
- * that runs on the FMA skeleton, the kernel is regenerated with each candidate per-tile
- * pacing in {0, 150, 300, 450} ns (NVRTC), timed over `reps` back-to-back launches (after 2
- * untimed ones) on X -> Y with driver events on `stream`, and the fastest replaces the
- * plan's kernel if it beats the current one by more than 1%.  Tensor-core kernels are left
- * as they are (pace_ns_out = -1).  The arithmetic is unchanged, so every candidate computes
+/* Measured tuning of the FMA-skeleton kernels of a plan (DESIGN.md §4 "Request pacing" and
+ * "Measured tuning"; the analogue of FFTW_MEASURE — not part of the paper's method, which
+ * fixes only the arithmetic).  For every kernel kind in kinds_mask (bits as in
+ * gft_plan_compile; 0 = fast-fwd | fast-inv) that runs on the FMA skeleton:
+ *   1. with GFT_TUNE_GEOMETRY in flags, the kernel is regenerated for every warp-tile geometry
+ *      (rows per thread R in {1,2,4,8}, stages {2,3,4}, warps {4,8,12}; 1-32 KiB tiles that
+ *      fit shared memory) and the fastest geometry is kept for step 2;
+ *   2. the kernel is regenerated with each per-tile pacing in {0, 150, 300, 450} ns;
+ * candidates are compiled in parallel (NVRTC) and timed twice over `reps` back-to-back
+ * launches (after 2 untimed ones) on X -> Y with driver events on `stream`; the fastest
+ * replaces the plan's kernel if it beats the current one by more than 1%.  Tensor-core
+ * kernels are left as they are.  The arithmetic is unchanged, so every candidate computes
  * bit-identical outputs.
  * X, Y: caller-owned device buffers of >= batch x n elements of `dtype` (16-byte aligned,
  *   distinct); X is read, Y is overwritten.  batch should exceed L2 (e.g. >= 256 MiB of rows)
  *   for the timing to reflect HBM streaming.  reps <= 0 selects 10.
- * pace_ns_out: NULL or int32_t[4], the chosen pacing per kind (-1 = not tuned).
+ * choice_out: NULL or int32_t[16]; for kind k, choice_out[4k..4k+3] = {R, stages, warps,
+ *   pace_ns} of the kernel kept (-1s: kind not tuned / tensor-core kernel).
  * Synchronous on `stream`.  Not thread-safe with respect to concurrent calls on the same plan
  * (it replaces kernels); the choice is per process (not serialised with the plan).
- * Errors: GFT_ERR_INVALID_ARG (NULL / bad sizes), GFT_ERR_ALIGNMENT, GFT_ERR_UNSUPPORTED
- * (dtype not prepared), GFT_ERR_NO_DEVICE / GFT_ERR_CUDA. */
-GFT_API gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, const void* X,
-                                 void* Y, int64_t batch, int32_t reps, gft_stream stream,
-                                 int32_t* pace_ns_out);
+ * Errors: GFT_ERR_INVALID_ARG (NULL / bad sizes / unknown flags), GFT_ERR_ALIGNMENT,
+ * GFT_ERR_UNSUPPORTED (dtype not prepared), GFT_ERR_COMPILE, GFT_ERR_NO_DEVICE / GFT_ERR_CUDA. */
+#define GFT_TUNE_GEOMETRY 1u
+GFT_API gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, uint32_t flags,
+                                 const void* X, void* Y, int64_t batch, int32_t reps, gft_stream stream,
+                                 int32_t* choice_out);
 
 /* ---- introspection (host) ------------------------------------------------------------ */
 

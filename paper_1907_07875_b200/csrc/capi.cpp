@@ -4,7 +4,9 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
+#include <set>
 #include <string>
 #include <thread>
 #include <vector>
@@ -364,8 +366,35 @@ gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask)
   });
 }
 
-gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, const void* X, void* Y,
-                         int64_t batch, int32_t reps, gft_stream stream, int32_t* pace_ns_out) {
+namespace {
+// one tuning candidate: an FMA-skeleton kernel regenerated with geometry / pacing overrides
+struct TuneCand {
+  gft::CfgOverride ov;
+  std::unique_ptr<gft::Kernel> k;
+  double ms = 1e30;
+};
+
+void compile_parallel(std::vector<TuneCand>& cs, bool cache) {
+  std::vector<gft::Error> errs(cs.size(), gft::Error{GFT_OK, ""});
+  std::vector<std::thread> th;
+  for (size_t i = 0; i < cs.size(); ++i)
+    th.emplace_back([&, i] {
+      try {
+        std::lock_guard<std::mutex> lk(cs[i].k->mu);
+        gft::compile_kernel(*cs[i].k, cache);
+      } catch (const gft::Error& e) {
+        errs[i] = e;
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : errs)
+    if (e.status != GFT_OK) throw e;
+}
+}  // namespace
+
+gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, uint32_t flags,
+                         const void* X, void* Y, int64_t batch, int32_t reps, gft_stream stream,
+                         int32_t* choice_out) {
   return guard([&] {
     if (!plan) gft::fail(GFT_ERR_INVALID_ARG, "NULL plan");
     if (batch <= 0) gft::fail(GFT_ERR_INVALID_ARG, "batch must be > 0");
@@ -373,10 +402,11 @@ gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, co
     if (X == Y) gft::fail(GFT_ERR_INVALID_ARG, "X and Y must be distinct buffers");
     if (kinds_mask == 0) kinds_mask = (1u << gft::K_FAST_FWD) | (1u << gft::K_FAST_INV);
     if (kinds_mask >> (gft::K_DENSE_INV + 1)) gft::fail(GFT_ERR_INVALID_ARG, "kinds_mask: bits 0..3 only");
+    if (flags & ~(uint32_t)GFT_TUNE_GEOMETRY) gft::fail(GFT_ERR_INVALID_ARG, "unknown tune flags");
     if (reps <= 0) reps = 10;
-    if (pace_ns_out)
-      for (int i = 0; i < 4; ++i) pace_ns_out[i] = -1;
-    static const int kCand[] = {0, 150, 300, 450};
+    if (choice_out)
+      for (int i = 0; i < 16; ++i) choice_out[i] = -1;
+    static const int kPace[] = {0, 150, 300, 450};
     const bool cache = !(plan->flags & GFT_FLAG_NO_CUBIN_CACHE);
     const bool allow_tc = !(plan->flags & GFT_FLAG_NO_TENSOR_CORES);
     const bool dense_tc = (plan->flags & GFT_FLAG_DENSE_TC) != 0;
@@ -384,43 +414,65 @@ gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, co
       if (!(kinds_mask & (1u << kind))) continue;
       gft::Kernel& cur = kernel_of(plan, kind, dtype);
       if (cur.cfg.tc) continue;
-      // candidates: generated and compiled in parallel (NVRTC unless already cached)
-      std::vector<std::unique_ptr<gft::Kernel>> cand;
-      for (int pace : kCand) {
-        cand.emplace_back(new gft::Kernel);
-        gft::generate_kernel(plan->P, kind, dtype, *cand.back(), allow_tc, dense_tc, pace);
-      }
-      std::vector<gft::Error> errs(cand.size(), gft::Error{GFT_OK, ""});
-      std::vector<std::thread> th;
-      for (size_t i = 0; i < cand.size(); ++i)
-        th.emplace_back([&, i] {
-          try {
-            std::lock_guard<std::mutex> lk(cand[i]->mu);
-            gft::compile_kernel(*cand[i], cache);
-          } catch (const gft::Error& e) {
-            errs[i] = e;
-          }
-        });
-      for (auto& t : th) t.join();
-      for (auto& e : errs)
-        if (e.status != GFT_OK) throw e;
       const double t_cur = gft::time_kernel_ms(cur, X, Y, batch, stream, 2, reps, cache);
-      double best = t_cur;
-      int best_i = -1;
-      for (size_t i = 0; i < cand.size(); ++i) {
-        if (cand[i]->name == cur.name) continue;   // same code as the current kernel
-        const double t = gft::time_kernel_ms(*cand[i], X, Y, batch, stream, 2, reps, cache);
-        if (t < best) { best = t; best_i = (int)i; }
+      std::set<std::string> seen{cur.name};
+      std::vector<TuneCand> pool;   // every timed candidate (the winner is moved out of it)
+      // candidates -> generated (deduplicated by kernel name) -> compiled -> timed twice
+      auto run_stage = [&](const std::vector<gft::CfgOverride>& ovs) {
+        std::vector<TuneCand> cs;
+        for (const auto& ov : ovs) {
+          TuneCand c;
+          c.ov = ov;
+          c.k.reset(new gft::Kernel);
+          gft::generate_kernel(plan->P, kind, dtype, *c.k, allow_tc, dense_tc, &ov);
+          if (c.k->cfg.tc || !seen.insert(c.k->name).second) continue;
+          cs.push_back(std::move(c));
+        }
+        compile_parallel(cs, cache);
+        for (int round = 0; round < 2; ++round)
+          for (auto& c : cs)
+            c.ms = std::min(c.ms, gft::time_kernel_ms(*c.k, X, Y, batch, stream, 2, reps, cache));
+        for (auto& c : cs) pool.push_back(std::move(c));
+      };
+      auto best_of_pool = [&]() -> TuneCand* {
+        TuneCand* b = nullptr;
+        for (auto& c : pool)
+          if (c.k && (!b || c.ms < b->ms)) b = &c;
+        return b;
+      };
+      gft::KernelCfg g = cur.cfg;   // geometry the pacing stage starts from
+      if (flags & GFT_TUNE_GEOMETRY) {
+        std::vector<gft::CfgOverride> ovs;
+        const int row = g.n * g.elem;
+        for (int R : {1, 2, 4, 8})
+          for (int S : {2, 3, 4})
+            for (int W : {4, 8, 12}) {
+              const int tile = 32 * R * row;
+              if (tile < 1024 || tile > 32768 || W * S * (tile + 8) + 1024 > 227 * 1024) continue;
+              ovs.push_back(gft::CfgOverride{R, S, W, 0});
+            }
+        run_stage(ovs);
+        TuneCand* b = best_of_pool();
+        if (b && b->ms < t_cur) g = b->k->cfg;
       }
-      int chosen = cur.cfg.pace_ns;
-      if (best_i >= 0 && best < 0.99 * t_cur) {
+      std::vector<gft::CfgOverride> ovs;
+      for (int pace : kPace) ovs.push_back(gft::CfgOverride{g.R, g.stages, g.warps, pace});
+      run_stage(ovs);
+      TuneCand* b = best_of_pool();
+      const gft::KernelCfg* chosen = &cur.cfg;
+      if (b && b->ms < 0.99 * t_cur) {
         gft::unload_kernel(cur);
-        plan->k[dtype][kind] = std::move(cand[best_i]);
-        chosen = kCand[best_i];
+        plan->k[dtype][kind] = std::move(b->k);
+        chosen = &plan->k[dtype][kind]->cfg;
       }
-      for (auto& c : cand)
-        if (c) gft::unload_kernel(*c);
-      if (pace_ns_out) pace_ns_out[kind] = chosen;
+      for (auto& c : pool)
+        if (c.k) gft::unload_kernel(*c.k);
+      if (choice_out) {
+        choice_out[4 * kind + 0] = chosen->R;
+        choice_out[4 * kind + 1] = chosen->stages;
+        choice_out[4 * kind + 2] = chosen->warps;
+        choice_out[4 * kind + 3] = chosen->pace_ns;
+      }
     }
   });
 }

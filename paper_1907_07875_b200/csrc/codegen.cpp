@@ -33,7 +33,7 @@ static const char* kSkeletonTC3 =
 #include "skeleton_tc3_inc.h"
     ;
 
-KernelCfg choose_cfg(int n, int dtype, int64_t work) {
+KernelCfg choose_cfg(int n, int dtype, int64_t work, const CfgOverride* ov) {
   KernelCfg c;
   c.n = n;
   c.elem = dtype == GFT_F64 ? 8 : 4;
@@ -69,12 +69,15 @@ KernelCfg choose_cfg(int n, int dtype, int64_t work) {
     // odd row pitch in vector units makes thread-per-row accesses conflict-free
     c.vec = (c.elem == 4 && n % 2 == 0) ? 2 : 1;
   }
-  // Default geometry (what the B200 sweeps in profiles/r01/autotune favour): warp tiles of
-  // ~8 KiB, double-buffered, up to 8 warps = ~128 KiB SMEM and one persistent CTA per SM.
+  // Default geometry for an (n, dtype) without a tuning entry: the largest warp tile of at
+  // most 8 KiB, double-buffered, as many warps (<= 12) as ~150 KiB of SMEM holds -- one
+  // persistent CTA per SM.  The measured geometry search of gft_plan_tune on graphs outside
+  // the table picked 4-8 KiB tiles with 12 warps (n = 40, 48: +15%, +36% over the previous
+  // default of >= 8 KiB tiles and <= 8 warps; tools/tune_probe.py).
   c.R = 1;
-  while (c.R < 8 && c.tile_bytes() < 8192 && 2 * c.tile_bytes() <= 16384) c.R *= 2;
+  while (c.R < 8 && 2 * c.tile_bytes() <= 8192) c.R *= 2;
   c.stages = 2;
-  c.warps = std::max(2, std::min(8, (128 * 1024) / (c.stages * c.tile_bytes())));
+  c.warps = std::max(2, std::min(12, (150 * 1024) / (c.stages * c.tile_bytes())));
   // measured geometry for this (n, dtype) if the tuning table has one (tools/gpu_autotune.py)
   int tR, tS, tW, tP;
   if (tuned_geometry(n, dtype, work, tR, tS, tW, tP)) {
@@ -89,6 +92,12 @@ KernelCfg choose_cfg(int n, int dtype, int64_t work) {
   c.stages = std::max(2, std::min(8, env_int("GFT_TUNE_STAGES", c.stages)));
   c.warps = std::max(1, std::min(16, env_int("GFT_TUNE_WARPS", c.warps)));
   c.pace_ns = std::max(0, std::min(100000, env_int("GFT_PACE_NS", c.pace_ns)));
+  if (ov) {
+    if (ov->R > 0) c.R = std::min(8, ov->R);
+    if (ov->stages > 0) c.stages = std::max(2, std::min(8, ov->stages));
+    if (ov->warps > 0) c.warps = std::min(16, ov->warps);
+    if (ov->pace_ns >= 0) c.pace_ns = std::min(100000, ov->pace_ns);
+  }
   // the 128B swizzle atom needs 1024-byte aligned tile buffers; TMA boxes hold <= 256 rows
   while (c.mode == 2 && c.swz_mask && c.tile_bytes() % 1024 != 0 && c.R < 8) c.R *= 2;
   if (c.smem_bytes() > 227 * 1024) c.stages = 2;
@@ -723,7 +732,7 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
 }  // namespace
 
 void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc, bool dense_tc,
-                     int pace_ns) {
+                     const CfgOverride* ov) {
   if (dense_tc && allow_tc && (kind == K_DENSE_FWD || kind == K_DENSE_INV)) {
     // dense U^T x on tensor cores: the whole basis as ONE leaf (no butterflies), generated by
     // the same tcgen05 path -- the strongest dense comparison for n >= 32
@@ -748,8 +757,8 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
   }
   k.kind = kind;
   k.dtype = dtype;
-  k.cfg = choose_cfg(P.n, dtype, (kind == K_DENSE_FWD || kind == K_DENSE_INV) ? (int64_t)P.n * P.n : P.sum_k2);
-  if (pace_ns >= 0) k.cfg.pace_ns = pace_ns;
+  k.cfg = choose_cfg(P.n, dtype, (kind == K_DENSE_FWD || kind == K_DENSE_INV) ? (int64_t)P.n * P.n : P.sum_k2,
+                     ov);
   static const char* kKindNameTC[] = {"fwdtc", "invtc", "", "", "filttc"};
   const Dir dir = kind == K_FAST_INV ? DIR_INV : kind == K_FILTER ? DIR_FILTER : DIR_FWD;
   if (allow_tc && (kind == K_FAST_FWD || kind == K_FAST_INV || kind == K_FILTER)) {

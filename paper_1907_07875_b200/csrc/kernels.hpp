@@ -46,7 +46,9 @@ struct KernelCfg {
 };
 
 // work = FMAs per signal of the kernel body (selects plan-specific tuning entries)
-KernelCfg choose_cfg(int n, int dtype, int64_t work = -1);
+// Geometry / pacing overrides of the FMA skeleton (gft_plan_tune candidates); -1 = keep.
+struct CfgOverride { int R = -1, stages = -1, warps = -1, pace_ns = -1; };
+KernelCfg choose_cfg(int n, int dtype, int64_t work = -1, const CfgOverride* ov = nullptr);
 
 struct LoadedFn {
   void* module = nullptr;   // CUmodule
@@ -70,9 +72,9 @@ struct Kernel {
 // Emits the full CUDA source (prelude + gft_body + skeleton) for a plan.
 // allow_tc: fast kernels of fp32 plans with leaves >= 32 use the tcgen05 3xTF32 skeleton.
 // dense_tc: the dense comparison kernels use the tcgen05 path (whole basis as one leaf).
-// pace_ns >= 0 overrides the FMA skeleton's request pacing (gft_plan_tune candidates).
+// ov: geometry / pacing overrides of the FMA skeleton (gft_plan_tune candidates).
 void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc, bool dense_tc = false,
-                     int pace_ns = -1);
+                     const CfgOverride* ov = nullptr);
 
 // Compiles k.source to an sm_100a cubin (AOT cache lookup first unless disabled).
 void compile_kernel(Kernel& k, bool allow_cache);

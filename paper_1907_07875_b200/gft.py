@@ -96,7 +96,7 @@ def lib():
         "gft_dense_inverse": (c_int32, [P, P, P, c_int64, c_int32, P]),
         "gft_execute_host": (c_int32, [P, c_int32, P, P, c_int64, c_int32, P, c_size_t, c_int64, P]),
         "gft_plan_compile": (c_int32, [P, c_int32, c_uint32]),
-        "gft_plan_tune": (c_int32, [P, c_int32, c_uint32, P, P, c_int64, c_int32, P, P]),
+        "gft_plan_tune": (c_int32, [P, c_int32, c_uint32, c_uint32, P, P, c_int64, c_int32, P, P]),
         "gft_plan_info_get": (c_int32, [P, POINTER(gft_plan_info)]),
         "gft_plan_eigenvalues": (c_int32, [P, P]),
         "gft_plan_basis": (c_int32, [P, P]),
@@ -274,12 +274,15 @@ def gft_plan_compile(h, dtype, kinds_mask=0):
     _check(lib().gft_plan_compile(h, _dtype_code(dtype), int(kinds_mask)))
 
 
-def gft_plan_tune(h, dtype, kinds_mask, X, Y, batch, reps=0, stream=None):
-    """Returns the chosen pacing (ns) per kernel kind, -1 where not tuned."""
-    out = (ctypes.c_int32 * 4)()
-    _check(lib().gft_plan_tune(h, _dtype_code(dtype), int(kinds_mask), _dev_ptr(X), _dev_ptr(Y),
-                               int(batch), int(reps), _stream_handle(stream), out))
-    return list(out)
+GFT_TUNE_GEOMETRY = 1
+
+
+def gft_plan_tune(h, dtype, kinds_mask, X, Y, batch, reps=0, stream=None, flags=0):
+    """Returns {kind: (R, stages, warps, pace_ns)} for the kinds tuned (FMA-skeleton kernels)."""
+    out = (ctypes.c_int32 * 16)()
+    _check(lib().gft_plan_tune(h, _dtype_code(dtype), int(kinds_mask), int(flags), _dev_ptr(X),
+                               _dev_ptr(Y), int(batch), int(reps), _stream_handle(stream), out))
+    return {k: tuple(out[4 * k: 4 * k + 4]) for k in range(4) if out[4 * k] >= 0}
 
 
 def gft_plan_info_get(h):
@@ -536,10 +539,11 @@ class Plan:
     def compile(self, dtype="f32", kinds=(0, 1, 2, 3)):
         gft_plan_compile(self._h, dtype, sum(1 << k for k in kinds))
 
-    def tune(self, dtype="f32", kinds=(0, 1), X=None, Y=None, batch=None, reps=0, stream=None):
+    def tune(self, dtype="f32", kinds=(0, 1), X=None, Y=None, batch=None, reps=0, stream=None,
+             geometry=False):
         """gft_plan_tune on the device tensors X -> Y (or on scratch buffers of `batch` rows,
-        default 256 MiB of rows, > L2).  Returns {kind: chosen pacing in ns} for the kinds
-        that run on the FMA skeleton."""
+        default 256 MiB of rows, > L2); geometry=True also searches the warp-tile geometry.
+        Returns {kind: (R, stages, warps, pace_ns)} for the kinds on the FMA skeleton."""
         import torch
         tdt = torch.float64 if dtype == "f64" else torch.float32
         if X is None:
@@ -550,9 +554,8 @@ class Plan:
             Y = torch.empty_like(X)
         if X.dtype != tdt or Y.dtype != tdt or X.shape[1] != self.n or Y.shape != X.shape:
             raise ValueError("X, Y: [batch, %d] tensors of the tuned dtype" % self.n)
-        batch = X.shape[0]
-        paces = gft_plan_tune(self._h, dtype, sum(1 << k for k in kinds), X, Y, batch, reps, stream)
-        return {k: paces[k] for k in kinds if paces[k] >= 0}
+        return gft_plan_tune(self._h, dtype, sum(1 << k for k in kinds), X, Y, X.shape[0], reps, stream,
+                             GFT_TUNE_GEOMETRY if geometry else 0)
 
     def info(self):
         return gft_plan_info_get(self._h).as_dict()

@@ -22,7 +22,7 @@ def test_tune_bit_identical(name, dtype):
     Y0 = plan.forward(X)
     Z0 = plan.inverse(Y0)
     paces = plan.tune(dtype, (0, 1), batch=1 << 18, reps=3)
-    assert set(paces) == {0, 1} and set(paces.values()) <= CAND
+    assert set(paces) == {0, 1} and {p[3] for p in paces.values()} <= CAND
     Y1 = plan.forward(X)
     Z1 = plan.inverse(Y1)
     torch.cuda.synchronize()
@@ -52,8 +52,39 @@ def test_tune_errors():
         gft.gft_plan_tune(plan._h, "f32", 3, X, torch.empty_like(X), 0)
     with pytest.raises(gft.GFTError, match="UNSUPPORTED"):
         gft.gft_plan_tune(plan._h, "f64", 3, X, torch.empty_like(X), 4096)
+    with pytest.raises(gft.GFTError, match="INVALID_ARG"):
+        gft.gft_plan_tune(plan._h, "f32", 3, X, torch.empty_like(X), 4096, flags=2)
     # the plan still works and matches the oracle-free identity round trip
     Y = plan.forward(X)
     Z = plan.inverse(Y)
     assert float((Z - X).norm() / X.norm()) < 1e-5
+    plan.close()
+
+
+def test_tune_geometry_bit_identical():
+    """GFT_TUNE_GEOMETRY: a geometry search on a graph outside the tuning table (random
+    phi-symmetric, n = 40); the kept geometry computes the same bits."""
+    import numpy as np
+    n = 40
+    rng = np.random.default_rng(7)
+    s_, d_, w_ = [], [], []
+    for i in range(n // 2):                      # mirror-symmetric random graph
+        for j in range(i + 1, n // 2):
+            if rng.random() < 0.2:
+                w = rng.uniform(0.5, 2.0)
+                s_ += [i, n - 1 - i]
+                d_ += [j, n - 1 - j]
+                w_ += [w, w]
+        s_.append(i)
+        d_.append(n - 1 - i)
+        w_.append(rng.uniform(0.5, 2.0))
+    plan = gft.Plan(n, np.array(s_, np.int32), np.array(d_, np.int32), np.array(w_), dtypes=("f32",))
+    X = torch.randn(200_003, n, device="cuda")
+    Y0 = plan.forward(X)
+    ch = plan.tune("f32", (0,), batch=1 << 18, reps=2, geometry=True)
+    R, S, W, P = ch[0]
+    assert R in (1, 2, 4, 8) and 2 <= S <= 8 and 1 <= W <= 16 and P in CAND
+    Y1 = plan.forward(X)
+    torch.cuda.synchronize()
+    assert torch.equal(Y0, Y1)
     plan.close()
