@@ -206,6 +206,13 @@ def config_table(args, stream, hbm, device):
                          "frac": round(nbytes / ms / 1e6 / hbm, 4), "signals_per_s": cfg.batch / ms * 1e3,
                          "kernel": filt.kernel_name(dtype)}
         row["fused_filter_vs_two_pass"] = round((row["fast_fwd"]["ms"] + row["fast_inv"]["ms"]) / ms, 3)
+        if not args.no_tune and cfg.batch * cfg.n * esz > (64 << 20):
+            # measured geometry + pacing (gft_filter_tune), then re-timed
+            ch = filt.tune(X, Y, dtype, stream=stream, geometry=True)
+            if ch is not None:
+                ms = time_kernel(lambda: filt.apply(X, Y, stream), stream, 3, args.table_iters)
+                row["filter_tuned"] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
+                                       "frac": round(nbytes / ms / 1e6 / hbm, 4), "geometry_pace": ch}
         # cuBLAS SGEMM/DGEMM with TF32 disabled (SURVEY §7 step 6 cross-check of "dense")
         U = torch.from_numpy(plan.basis()).to(device=device, dtype=tdt)
         tf32 = torch.backends.cuda.matmul.allow_tf32
@@ -224,6 +231,16 @@ def config_table(args, stream, hbm, device):
                                    "kernel": dplan.kernel_name(2, dtype)}
             row["fast_vs_dense_tc_fwd"] = round(ms / row["fast_fwd"]["ms"], 3)
             dplan.close()
+        if not args.no_tune and cfg.batch * cfg.n * esz > (64 << 20):
+            # measured geometry + pacing of the fast kernels (gft_plan_tune), then re-timed:
+            # shows whether the committed tuning table still holds on this box
+            ch = plan.tune(dtype, (0, 1), X, Y, stream=stream, geometry=True)
+            for kind, f in ((0, plan.forward), (1, plan.inverse)):
+                if kind in ch:
+                    ms = time_kernel(lambda: f(X, Y, stream), stream, 3, args.table_iters)
+                    row[KIND_NAMES[kind] + "_tuned"] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
+                                                        "frac": round(nbytes / ms / 1e6 / hbm, 4),
+                                                        "geometry_pace": ch[kind]}
         rows.append(row)
         del X, Y
         filt.close()
@@ -479,6 +496,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-table", action="store_true", help="skip the all-config side table")
     ap.add_argument("--table-iters", type=int, default=20)
+    ap.add_argument("--no-tune", action="store_true", help="skip the measured-tuning columns of the tables")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle CPU timing")
     ap.add_argument("--ref-rows", type=int, default=1 << 20)
     ap.add_argument("--e2e-steps", type=int, default=5)

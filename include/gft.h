@@ -257,6 +257,11 @@ GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kin
 GFT_API gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, uint32_t flags,
                                  const void* X, void* Y, int64_t batch, int32_t reps, gft_stream stream,
                                  int32_t* choice_out);
+/* The same measured tuning for a filter's kernel (gft_filter_apply): X, Y, batch, reps,
+ * flags, stream as above; choice_out: NULL or int32_t[4] = {R, stages, warps, pace_ns}
+ * (-1s for a tensor-core filter kernel). */
+GFT_API gft_status gft_filter_tune(gft_filter f, gft_dtype dtype, uint32_t flags, const void* X, void* Y,
+                                   int64_t batch, int32_t reps, gft_stream stream, int32_t* choice_out);
 
 /* ---- introspection (host) ------------------------------------------------------------ */
 

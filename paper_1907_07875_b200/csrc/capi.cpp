@@ -390,6 +390,80 @@ void compile_parallel(std::vector<TuneCand>& cs, bool cache) {
   for (auto& e : errs)
     if (e.status != GFT_OK) throw e;
 }
+
+// Measured tuning of one kernel slot (gft_plan_tune / gft_filter_tune); out4 = {R, stages,
+// warps, pace_ns} of the kernel kept, untouched for tensor-core kernels.
+void tune_slot(const gft::Plan& P, std::unique_ptr<gft::Kernel>& slot, int kind, int dtype, bool allow_tc,
+               bool dense_tc, bool cache, uint32_t flags, const void* X, void* Y, int64_t batch,
+               int reps, gft_stream stream, int32_t* out4) {
+  static const int kPace[] = {0, 150, 300, 450};
+  gft::Kernel& cur = *slot;
+  if (cur.cfg.tc) return;
+  const double t_cur = gft::time_kernel_ms(cur, X, Y, batch, stream, 2, reps, cache);
+  std::set<std::string> seen{cur.name};
+  std::vector<TuneCand> pool;   // every timed candidate (the winner is moved out of it)
+  // candidates -> generated (deduplicated by kernel name) -> compiled -> timed twice
+  auto run_stage = [&](const std::vector<gft::CfgOverride>& ovs) {
+    std::vector<TuneCand> cs;
+    for (const auto& ov : ovs) {
+      TuneCand c;
+      c.ov = ov;
+      c.k.reset(new gft::Kernel);
+      gft::generate_kernel(P, kind, dtype, *c.k, allow_tc, dense_tc, &ov);
+      if (c.k->cfg.tc || !seen.insert(c.k->name).second) continue;
+      cs.push_back(std::move(c));
+    }
+    compile_parallel(cs, cache);
+    for (int round = 0; round < 2; ++round)
+      for (auto& c : cs)
+        c.ms = std::min(c.ms, gft::time_kernel_ms(*c.k, X, Y, batch, stream, 2, reps, cache));
+    for (auto& c : cs) pool.push_back(std::move(c));
+  };
+  auto best_of_pool = [&]() -> TuneCand* {
+    TuneCand* b = nullptr;
+    for (auto& c : pool)
+      if (c.k && (!b || c.ms < b->ms)) b = &c;
+    return b;
+  };
+  gft::KernelCfg g = cur.cfg;   // geometry the pacing stage starts from
+  if (flags & GFT_TUNE_GEOMETRY) {
+    std::vector<gft::CfgOverride> ovs;
+    const int row = g.n * g.elem;
+    for (int R : {1, 2, 4, 8})
+      for (int S : {2, 3, 4})
+        for (int W : {4, 8, 12}) {
+          const int tile = 32 * R * row;
+          if (tile < 1024 || tile > 32768 || W * S * (tile + 8) + 1024 > 227 * 1024) continue;
+          ovs.push_back(gft::CfgOverride{R, S, W, 0});
+        }
+    run_stage(ovs);
+    TuneCand* b = best_of_pool();
+    if (b && b->ms < t_cur) g = b->k->cfg;
+  }
+  std::vector<gft::CfgOverride> ovs;
+  for (int pace : kPace) ovs.push_back(gft::CfgOverride{g.R, g.stages, g.warps, pace});
+  run_stage(ovs);
+  TuneCand* b = best_of_pool();
+  if (b && b->ms < 0.99 * t_cur) {
+    gft::unload_kernel(cur);
+    slot = std::move(b->k);
+  }
+  for (auto& c : pool)
+    if (c.k) gft::unload_kernel(*c.k);
+  if (out4) {
+    out4[0] = slot->cfg.R;
+    out4[1] = slot->cfg.stages;
+    out4[2] = slot->cfg.warps;
+    out4[3] = slot->cfg.pace_ns;
+  }
+}
+
+void check_tune_args(const void* X, void* Y, int64_t batch, uint32_t flags) {
+  if (batch <= 0) gft::fail(GFT_ERR_INVALID_ARG, "batch must be > 0");
+  check_io(X, Y);
+  if (X == Y) gft::fail(GFT_ERR_INVALID_ARG, "X and Y must be distinct buffers");
+  if (flags & ~(uint32_t)GFT_TUNE_GEOMETRY) gft::fail(GFT_ERR_INVALID_ARG, "unknown tune flags");
+}
 }  // namespace
 
 gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, uint32_t flags,
@@ -397,83 +471,33 @@ gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, ui
                          int32_t* choice_out) {
   return guard([&] {
     if (!plan) gft::fail(GFT_ERR_INVALID_ARG, "NULL plan");
-    if (batch <= 0) gft::fail(GFT_ERR_INVALID_ARG, "batch must be > 0");
-    check_io(X, Y);
-    if (X == Y) gft::fail(GFT_ERR_INVALID_ARG, "X and Y must be distinct buffers");
+    check_tune_args(X, Y, batch, flags);
     if (kinds_mask == 0) kinds_mask = (1u << gft::K_FAST_FWD) | (1u << gft::K_FAST_INV);
     if (kinds_mask >> (gft::K_DENSE_INV + 1)) gft::fail(GFT_ERR_INVALID_ARG, "kinds_mask: bits 0..3 only");
-    if (flags & ~(uint32_t)GFT_TUNE_GEOMETRY) gft::fail(GFT_ERR_INVALID_ARG, "unknown tune flags");
-    if (reps <= 0) reps = 10;
     if (choice_out)
       for (int i = 0; i < 16; ++i) choice_out[i] = -1;
-    static const int kPace[] = {0, 150, 300, 450};
-    const bool cache = !(plan->flags & GFT_FLAG_NO_CUBIN_CACHE);
-    const bool allow_tc = !(plan->flags & GFT_FLAG_NO_TENSOR_CORES);
-    const bool dense_tc = (plan->flags & GFT_FLAG_DENSE_TC) != 0;
     for (int kind = gft::K_FAST_FWD; kind <= gft::K_DENSE_INV; ++kind) {
       if (!(kinds_mask & (1u << kind))) continue;
-      gft::Kernel& cur = kernel_of(plan, kind, dtype);
-      if (cur.cfg.tc) continue;
-      const double t_cur = gft::time_kernel_ms(cur, X, Y, batch, stream, 2, reps, cache);
-      std::set<std::string> seen{cur.name};
-      std::vector<TuneCand> pool;   // every timed candidate (the winner is moved out of it)
-      // candidates -> generated (deduplicated by kernel name) -> compiled -> timed twice
-      auto run_stage = [&](const std::vector<gft::CfgOverride>& ovs) {
-        std::vector<TuneCand> cs;
-        for (const auto& ov : ovs) {
-          TuneCand c;
-          c.ov = ov;
-          c.k.reset(new gft::Kernel);
-          gft::generate_kernel(plan->P, kind, dtype, *c.k, allow_tc, dense_tc, &ov);
-          if (c.k->cfg.tc || !seen.insert(c.k->name).second) continue;
-          cs.push_back(std::move(c));
-        }
-        compile_parallel(cs, cache);
-        for (int round = 0; round < 2; ++round)
-          for (auto& c : cs)
-            c.ms = std::min(c.ms, gft::time_kernel_ms(*c.k, X, Y, batch, stream, 2, reps, cache));
-        for (auto& c : cs) pool.push_back(std::move(c));
-      };
-      auto best_of_pool = [&]() -> TuneCand* {
-        TuneCand* b = nullptr;
-        for (auto& c : pool)
-          if (c.k && (!b || c.ms < b->ms)) b = &c;
-        return b;
-      };
-      gft::KernelCfg g = cur.cfg;   // geometry the pacing stage starts from
-      if (flags & GFT_TUNE_GEOMETRY) {
-        std::vector<gft::CfgOverride> ovs;
-        const int row = g.n * g.elem;
-        for (int R : {1, 2, 4, 8})
-          for (int S : {2, 3, 4})
-            for (int W : {4, 8, 12}) {
-              const int tile = 32 * R * row;
-              if (tile < 1024 || tile > 32768 || W * S * (tile + 8) + 1024 > 227 * 1024) continue;
-              ovs.push_back(gft::CfgOverride{R, S, W, 0});
-            }
-        run_stage(ovs);
-        TuneCand* b = best_of_pool();
-        if (b && b->ms < t_cur) g = b->k->cfg;
-      }
-      std::vector<gft::CfgOverride> ovs;
-      for (int pace : kPace) ovs.push_back(gft::CfgOverride{g.R, g.stages, g.warps, pace});
-      run_stage(ovs);
-      TuneCand* b = best_of_pool();
-      const gft::KernelCfg* chosen = &cur.cfg;
-      if (b && b->ms < 0.99 * t_cur) {
-        gft::unload_kernel(cur);
-        plan->k[dtype][kind] = std::move(b->k);
-        chosen = &plan->k[dtype][kind]->cfg;
-      }
-      for (auto& c : pool)
-        if (c.k) gft::unload_kernel(*c.k);
-      if (choice_out) {
-        choice_out[4 * kind + 0] = chosen->R;
-        choice_out[4 * kind + 1] = chosen->stages;
-        choice_out[4 * kind + 2] = chosen->warps;
-        choice_out[4 * kind + 3] = chosen->pace_ns;
-      }
+      kernel_of(plan, kind, dtype);   // validates dtype / preparation
+      tune_slot(plan->P, plan->k[dtype][kind], kind, dtype, !(plan->flags & GFT_FLAG_NO_TENSOR_CORES),
+                (plan->flags & GFT_FLAG_DENSE_TC) != 0, !(plan->flags & GFT_FLAG_NO_CUBIN_CACHE), flags, X, Y,
+                batch, reps <= 0 ? 10 : reps, stream, choice_out ? choice_out + 4 * kind : nullptr);
     }
+  });
+}
+
+gft_status gft_filter_tune(gft_filter f, gft_dtype dtype, uint32_t flags, const void* X, void* Y,
+                           int64_t batch, int32_t reps, gft_stream stream, int32_t* choice_out) {
+  return guard([&] {
+    if (!f) gft::fail(GFT_ERR_INVALID_ARG, "NULL filter");
+    if (dtype != GFT_F32 && dtype != GFT_F64) gft::fail(GFT_ERR_UNSUPPORTED, "unsupported dtype");
+    if (!f->k[dtype]) gft::fail(GFT_ERR_UNSUPPORTED, "dtype not prepared in this filter");
+    check_tune_args(X, Y, batch, flags);
+    if (choice_out)
+      for (int i = 0; i < 4; ++i) choice_out[i] = -1;
+    tune_slot(f->P, f->k[dtype], gft::K_FILTER, dtype, !(f->flags & GFT_FLAG_NO_TENSOR_CORES), false,
+              !(f->flags & GFT_FLAG_NO_CUBIN_CACHE), flags, X, Y, batch, reps <= 0 ? 10 : reps, stream,
+              choice_out);
   });
 }
 

@@ -40,7 +40,7 @@ EXPORTS = ["gft_plan_opts_default", "gft_plan_create", "gft_plan_destroy", "gft_
            "gft_plan_launch_config", "gft_laplacian", "gft_decompose", "gft_find_involution",
            "gft_status_str", "gft_last_error", "gft_abi_version", "gft_filter_create",
            "gft_filter_apply", "gft_filter_kernel_name", "gft_filter_kernel_source", "gft_filter_destroy",
-           "gft_plan_serialize", "gft_plan_deserialize", "gft_plan_tune"]
+           "gft_plan_serialize", "gft_plan_deserialize", "gft_plan_tune", "gft_filter_tune"]
 
 
 class GFTError(RuntimeError):
@@ -97,6 +97,7 @@ def lib():
         "gft_execute_host": (c_int32, [P, c_int32, P, P, c_int64, c_int32, P, c_size_t, c_int64, P]),
         "gft_plan_compile": (c_int32, [P, c_int32, c_uint32]),
         "gft_plan_tune": (c_int32, [P, c_int32, c_uint32, c_uint32, P, P, c_int64, c_int32, P, P]),
+        "gft_filter_tune": (c_int32, [P, c_int32, c_uint32, P, P, c_int64, c_int32, P, P]),
         "gft_plan_info_get": (c_int32, [P, POINTER(gft_plan_info)]),
         "gft_plan_eigenvalues": (c_int32, [P, P]),
         "gft_plan_basis": (c_int32, [P, P]),
@@ -285,6 +286,14 @@ def gft_plan_tune(h, dtype, kinds_mask, X, Y, batch, reps=0, stream=None, flags=
     return {k: tuple(out[4 * k: 4 * k + 4]) for k in range(4) if out[4 * k] >= 0}
 
 
+def gft_filter_tune(f, dtype, X, Y, batch, reps=0, stream=None, flags=0):
+    """Returns (R, stages, warps, pace_ns) of the kept filter kernel, or None (tensor cores)."""
+    out = (ctypes.c_int32 * 4)()
+    _check(lib().gft_filter_tune(f, _dtype_code(dtype), int(flags), _dev_ptr(X), _dev_ptr(Y),
+                                 int(batch), int(reps), _stream_handle(stream), out))
+    return tuple(out) if out[0] >= 0 else None
+
+
 def gft_plan_info_get(h):
     info = gft_plan_info()
     _check(lib().gft_plan_info_get(h, ctypes.byref(info)))
@@ -416,6 +425,15 @@ class Filter:
         dt = GFT_F64 if X.dtype == torch.float64 else GFT_F32
         gft_filter_apply(self._h, X, Y, X.shape[0], dt, stream)
         return Y
+
+    def tune(self, X, Y=None, dtype="f32", reps=0, stream=None, geometry=False):
+        """gft_filter_tune on the device tensors X -> Y: (R, stages, warps, pace_ns) kept, or
+        None for a tensor-core filter kernel."""
+        import torch
+        if Y is None:
+            Y = torch.empty_like(X)
+        return gft_filter_tune(self._h, dtype, X, Y, X.shape[0], reps, stream,
+                               GFT_TUNE_GEOMETRY if geometry else 0)
 
     def kernel_name(self, dtype="f32"):
         return gft_filter_kernel_name(self._h, dtype)

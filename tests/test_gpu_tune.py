@@ -88,3 +88,19 @@ def test_tune_geometry_bit_identical():
     torch.cuda.synchronize()
     assert torch.equal(Y0, Y1)
     plan.close()
+
+
+def test_filter_tune_bit_identical():
+    cfg = workloads.config("cfg4")
+    plan = gft.Plan.from_config(cfg, dtypes=("f32",))
+    import numpy as np
+    filt = gft.Filter(plan, np.exp(-plan.eigenvalues()), dtypes=("f32",))
+    X = torch.randn(1 << 18, cfg.n, device="cuda")
+    Y0 = filt.apply(X)
+    ch = filt.tune(X, geometry=True, reps=2)
+    assert ch is not None and ch[3] in CAND
+    Y1 = filt.apply(X)
+    torch.cuda.synchronize()
+    assert torch.equal(Y0, Y1)
+    filt.close()
+    plan.close()
