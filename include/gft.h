@@ -257,6 +257,17 @@ GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kin
 GFT_API gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, uint32_t flags,
                                  const void* X, void* Y, int64_t batch, int32_t reps, gft_stream stream,
                                  int32_t* choice_out);
+/* Tuning records ("wisdom"): the FMA-skeleton geometry of one kernel of a plan,
+ * cfg4 = {R rows per thread, stages, warps, pace_ns}, so a tuned choice can be stored next to
+ * the serialised plan and re-applied after gft_plan_deserialize without re-measuring.
+ * get: -1s for a tensor-core kernel.  set: regenerates the kernel (compiled at its next
+ * launch or gft_plan_compile); GFT_ERR_UNSUPPORTED for a tensor-core kernel,
+ * GFT_ERR_INVALID_ARG for values outside R in {1,2,4,8}, stages 2..8, warps 1..16,
+ * pace 0..100000 or a geometry whose shared memory does not fit.  Needs no GPU.  Not
+ * thread-safe with respect to concurrent calls on the same plan. */
+GFT_API gft_status gft_plan_tuning_get(gft_plan plan, gft_dtype dtype, int32_t kind, int32_t* cfg4);
+GFT_API gft_status gft_plan_tuning_set(gft_plan plan, gft_dtype dtype, int32_t kind, const int32_t* cfg4);
+
 /* The same measured tuning for a filter's kernel (gft_filter_apply): X, Y, batch, reps,
  * flags, stream as above; choice_out: NULL or int32_t[4] = {R, stages, warps, pace_ns}
  * (-1s for a tensor-core filter kernel). */

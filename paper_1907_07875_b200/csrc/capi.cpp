@@ -501,6 +501,42 @@ gft_status gft_filter_tune(gft_filter f, gft_dtype dtype, uint32_t flags, const 
   });
 }
 
+gft_status gft_plan_tuning_get(gft_plan plan, gft_dtype dtype, int32_t kind, int32_t* cfg4) {
+  return guard([&] {
+    if (!cfg4) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
+    const gft::Kernel& k = kernel_of(plan, kind, dtype);
+    if (k.cfg.tc) {
+      for (int i = 0; i < 4; ++i) cfg4[i] = -1;
+      return;
+    }
+    cfg4[0] = k.cfg.R;
+    cfg4[1] = k.cfg.stages;
+    cfg4[2] = k.cfg.warps;
+    cfg4[3] = k.cfg.pace_ns;
+  });
+}
+
+gft_status gft_plan_tuning_set(gft_plan plan, gft_dtype dtype, int32_t kind, const int32_t* cfg4) {
+  return guard([&] {
+    if (!cfg4) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
+    gft::Kernel& cur = kernel_of(plan, kind, dtype);
+    if (cur.cfg.tc) gft::fail(GFT_ERR_UNSUPPORTED, "tensor-core kernel: no FMA-skeleton geometry to set");
+    const int R = cfg4[0], S = cfg4[1], W = cfg4[2], pace = cfg4[3];
+    if (!(R == 1 || R == 2 || R == 4 || R == 8) || S < 2 || S > 8 || W < 1 || W > 16 || pace < 0 ||
+        pace > 100000)
+      gft::fail(GFT_ERR_INVALID_ARG, "tuning: R in {1,2,4,8}, stages 2..8, warps 1..16, pace 0..100000 ns");
+    const gft::CfgOverride ov{R, S, W, pace};
+    std::unique_ptr<gft::Kernel> k(new gft::Kernel);
+    gft::generate_kernel(plan->P, kind, dtype, *k, !(plan->flags & GFT_FLAG_NO_TENSOR_CORES),
+                         (plan->flags & GFT_FLAG_DENSE_TC) != 0, &ov);
+    if (k->cfg.tc || k->cfg.R != R || k->cfg.stages != S || k->cfg.warps != W)
+      gft::fail(GFT_ERR_INVALID_ARG, "tuning: geometry not realisable for this kernel (tile / shared-memory limits)");
+    if (k->name == cur.name) return;
+    gft::unload_kernel(cur);
+    plan->k[dtype][kind] = std::move(k);
+  });
+}
+
 gft_status gft_plan_info_get(gft_plan plan, gft_plan_info* info) {
   return guard([&] {
     if (!plan || !info) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");

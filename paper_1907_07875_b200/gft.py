@@ -40,7 +40,8 @@ EXPORTS = ["gft_plan_opts_default", "gft_plan_create", "gft_plan_destroy", "gft_
            "gft_plan_launch_config", "gft_laplacian", "gft_decompose", "gft_find_involution",
            "gft_status_str", "gft_last_error", "gft_abi_version", "gft_filter_create",
            "gft_filter_apply", "gft_filter_kernel_name", "gft_filter_kernel_source", "gft_filter_destroy",
-           "gft_plan_serialize", "gft_plan_deserialize", "gft_plan_tune", "gft_filter_tune"]
+           "gft_plan_serialize", "gft_plan_deserialize", "gft_plan_tune", "gft_filter_tune",
+           "gft_plan_tuning_get", "gft_plan_tuning_set"]
 
 
 class GFTError(RuntimeError):
@@ -98,6 +99,8 @@ def lib():
         "gft_plan_compile": (c_int32, [P, c_int32, c_uint32]),
         "gft_plan_tune": (c_int32, [P, c_int32, c_uint32, c_uint32, P, P, c_int64, c_int32, P, P]),
         "gft_filter_tune": (c_int32, [P, c_int32, c_uint32, P, P, c_int64, c_int32, P, P]),
+        "gft_plan_tuning_get": (c_int32, [P, c_int32, c_int32, P]),
+        "gft_plan_tuning_set": (c_int32, [P, c_int32, c_int32, P]),
         "gft_plan_info_get": (c_int32, [P, POINTER(gft_plan_info)]),
         "gft_plan_eigenvalues": (c_int32, [P, P]),
         "gft_plan_basis": (c_int32, [P, P]),
@@ -292,6 +295,18 @@ def gft_filter_tune(f, dtype, X, Y, batch, reps=0, stream=None, flags=0):
     _check(lib().gft_filter_tune(f, _dtype_code(dtype), int(flags), _dev_ptr(X), _dev_ptr(Y),
                                  int(batch), int(reps), _stream_handle(stream), out))
     return tuple(out) if out[0] >= 0 else None
+
+
+def gft_plan_tuning_get(h, dtype, kind):
+    """(R, stages, warps, pace_ns) of the kernel, or None for a tensor-core kernel."""
+    out = (ctypes.c_int32 * 4)()
+    _check(lib().gft_plan_tuning_get(h, _dtype_code(dtype), int(kind), out))
+    return tuple(out) if out[0] >= 0 else None
+
+
+def gft_plan_tuning_set(h, dtype, kind, cfg4):
+    arr = (ctypes.c_int32 * 4)(*[int(v) for v in cfg4])
+    _check(lib().gft_plan_tuning_set(h, _dtype_code(dtype), int(kind), arr))
 
 
 def gft_plan_info_get(h):
@@ -574,6 +589,16 @@ class Plan:
             raise ValueError("X, Y: [batch, %d] tensors of the tuned dtype" % self.n)
         return gft_plan_tune(self._h, dtype, sum(1 << k for k in kinds), X, Y, X.shape[0], reps, stream,
                              GFT_TUNE_GEOMETRY if geometry else 0)
+
+    def tuning(self, dtype="f32", kinds=(0, 1, 2, 3)):
+        """Tuning record {kind: (R, stages, warps, pace_ns)} of the FMA-skeleton kernels."""
+        rec = {k: gft_plan_tuning_get(self._h, dtype, k) for k in kinds}
+        return {k: v for k, v in rec.items() if v is not None}
+
+    def set_tuning(self, record, dtype="f32"):
+        """Re-apply a record from tuning() (e.g. after Plan.load), without re-measuring."""
+        for k, cfg4 in record.items():
+            gft_plan_tuning_set(self._h, dtype, int(k), cfg4)
 
     def info(self):
         return gft_plan_info_get(self._h).as_dict()

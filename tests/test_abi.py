@@ -146,3 +146,36 @@ def test_nvrtc_compiles_generated_kernels_on_cpu():
     p = G.Plan.from_config(cfg, no_cubin_cache=True, dtypes=("f32",))
     p.compile("f32")
     assert p.info()["kernels_ready"] & 1
+
+
+def test_tuning_record_get_set_on_cpu():
+    """gft_plan_tuning_get / _set (no GPU): the record reflects the kernel's geometry, a set
+    regenerates the kernel with it (source prelude), survives a save/load round trip when
+    re-applied, and invalid or unrealisable records are rejected."""
+    cfg = workloads.config("cfg3")
+    p = G.Plan.from_config(cfg, dtypes=("f32",))
+    rec = p.tuning("f32", kinds=(0, 1))
+    assert rec[0] == (3, 3, 4, 400)          # tuning.tsv: fma 25 f32 3 3 4 pace=400
+    name0 = p.kernel_name(0, "f32")
+    p.set_tuning({0: (2, 2, 8, 150)}, "f32")
+    src = p.kernel_source(0, "f32")
+    for line in ("#define GFT_R 2", "#define GFT_STAGES 2", "#define GFT_WARPS 8", "#define GFT_PACE_NS 150"):
+        assert line in src
+    assert p.kernel_name(0, "f32") != name0 and p.tuning("f32", (0,))[0] == (2, 2, 8, 150)
+    p.set_tuning({0: (2, 2, 8, 0)}, "f32")
+    assert "#define GFT_PACE_NS" not in p.kernel_source(0, "f32")
+    # wisdom round trip: plan bytes + record -> identical kernel
+    p.set_tuning({0: (1, 3, 8, 300)}, "f32")
+    q = G.Plan.load(p.save(), dtypes=("f32",))
+    q.set_tuning(p.tuning("f32", (0,)), "f32")
+    assert q.kernel_name(0, "f32") == p.kernel_name(0, "f32")
+    for bad in ((3, 2, 4, 0), (1, 1, 4, 0), (1, 2, 0, 0), (1, 2, 4, -1), (8, 8, 16, 0)):
+        with pytest.raises(G.GFTError) as ei:
+            p.set_tuning({0: bad}, "f32")
+        assert ei.value.name == "GFT_ERR_INVALID_ARG"
+    # tensor-core kernels have no FMA-skeleton record
+    t = G.Plan.from_config(workloads.config("cfg5b"), dtypes=("f32",))
+    assert 0 not in t.tuning("f32", (0,))
+    with pytest.raises(G.GFTError) as ei:
+        t.set_tuning({0: (1, 2, 4, 0)}, "f32")
+    assert ei.value.name == "GFT_ERR_UNSUPPORTED"

@@ -104,3 +104,20 @@ def test_filter_tune_bit_identical():
     assert torch.equal(Y0, Y1)
     filt.close()
     plan.close()
+
+
+def test_tuning_record_replay_bit_identical():
+    """A tuning record applied to a reloaded plan (the wisdom path) runs and computes the same
+    bits as the default kernel."""
+    cfg = workloads.config("cfg2")
+    plan = gft.Plan.from_config(cfg, dtypes=("f32",))
+    X = torch.randn(100_001, cfg.n, device="cuda")
+    Y0 = plan.forward(X)
+    q = gft.Plan.load(plan.save(), dtypes=("f32",))
+    q.set_tuning({0: (2, 3, 12, 300), 1: (8, 2, 4, 150)}, "f32")
+    Y1 = q.forward(X)
+    Z1 = q.inverse(Y1)
+    torch.cuda.synchronize()
+    assert torch.equal(Y0, Y1) and torch.equal(Z1, plan.inverse(Y0))
+    q.close()
+    plan.close()
