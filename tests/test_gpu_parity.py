@@ -127,22 +127,29 @@ def test_dense_tensor_core_kernel_vs_oracle(name):
 
 
 @pytest.mark.parametrize("batch", [0, 1, 31, 32, 33, 127, 128, 129, 1000])
-@pytest.mark.parametrize("name", ["cfg3", "cfg5a"])   # bulk (odd n) and TMA layouts
+@pytest.mark.parametrize("name", ["cfg1", "cfg3", "cfg5a", "cfg5b"])   # packed, bulk (odd n), TMA, tcgen05 pair
 def test_small_and_ragged_batches(name, batch):
     plan = plan_for(name, "f32")
     cfg = workloads.config(name)
     lam_o, U_o = oracle_basis(name)
     X = workloads.signals(cfg, batch=max(batch, 1), dtype="f32")[:batch].contiguous()
     Xd = X.cuda()
-    guard = torch.full((batch + 64, cfg.n), 7.0, device="cuda")
-    Yd = guard[:batch]
+    # sentinel rows before and after Y (16 rows keep Y 16-byte aligned)
+    guard = torch.full((batch + 80, cfg.n), 7.0, device="cuda")
+    Yd = guard[16:16 + batch]
     if batch == 0:
         plan.forward(Xd, Yd)
         return
     plan.forward(Xd, Yd)
     torch.cuda.synchronize()
-    assert torch.all(guard[batch:] == 7.0), "kernel wrote past the end of Y"
+    assert torch.all(guard[16 + batch:] == 7.0), "kernel wrote past the end of Y"
+    assert torch.all(guard[:16] == 7.0), "kernel wrote before the start of Y"
     check_forward(Yd.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
+    Zd = guard[16:16 + batch]
+    plan.inverse(Yd.clone(), Zd)
+    torch.cuda.synchronize()
+    assert torch.all(guard[16 + batch:] == 7.0) and torch.all(guard[:16] == 7.0)
+    assert oracle.relative_error(Zd.cpu().numpy(), X.numpy()).max() <= 2e-5
 
 
 @pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5b"])
