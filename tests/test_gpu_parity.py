@@ -584,3 +584,30 @@ def test_packed_view_mode(monkeypatch, n, dtype, force, batch):
     torch.cuda.synchronize()
     check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), TOL[dtype])
     assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL[dtype]
+
+
+@pytest.mark.parametrize("which", ["ws_tc3", "f64"])
+@pytest.mark.parametrize("batch", [1, 129, 1000])
+def test_guard_regions_ws_and_f64(which, batch):
+    """Sentinel rows around Y for the warp-specialised tcgen05 kernel (right-Haar 32|32,
+    n = 64) and the fp64 FMA kernel (cfg4): nothing written outside Y, Y = X U_f."""
+    if which == "ws_tc3":
+        n, s_, d_, w_, loops, norm = workloads.right_haar_bench_graph(workloads.RIGHT_HAAR_BENCH_CASES[0])
+        plan = G.Plan(n, s_, d_, w_, loops, dtypes=("f32",), normalized=norm)
+        assert "tc3" in plan.kernel_name(0, "f32")
+        tdt, tol, dt = torch.float32, 1e-5, "f32"
+    else:
+        cfg = workloads.config("cfg4")
+        n = cfg.n
+        plan = G.Plan.from_config(cfg, dtypes=("f64",))
+        tdt, tol, dt = torch.float64, 1e-12, "f64"
+    X = torch.randn(batch, n, generator=torch.Generator().manual_seed(batch), dtype=tdt)
+    guard = torch.full((batch + 80, n), 7.0, device="cuda", dtype=tdt)
+    Yd = guard[16:16 + batch]
+    plan.forward(X.cuda(), Yd)
+    torch.cuda.synchronize()
+    assert torch.all(guard[:16] == 7.0) and torch.all(guard[16 + batch:] == 7.0)
+    ref = X.double().numpy() @ plan.basis()
+    err = np.linalg.norm(Yd.cpu().double().numpy() - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    assert err.max() <= tol
+    plan.close()
