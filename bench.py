@@ -632,7 +632,9 @@ def main():
 
     table = None
     rh_table = ap_table = None
-    if rank == 0 and not args.no_table:
+    # the side tables are single-GPU diagnostics; in a multi-rank run the other ranks would
+    # only wait for them at the final barrier
+    if rank == 0 and not args.no_table and ws == 1:
         table = config_table(args, stream, hbm, device)
         rh_table = right_haar_table(args, stream, hbm, device)
         ap_table = approx_table(args, stream, hbm, device)
