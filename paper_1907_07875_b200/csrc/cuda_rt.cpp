@@ -233,6 +233,18 @@ constexpr int kMapCacheWays = 4;
 thread_local MapCacheEntry t_map_cache[kMapCacheWays];
 thread_local int t_map_next = 0;
 
+// L2 sector promotion of the signal tensor maps (256 B default; GFT_L2PROMO=0/64/128/256
+// for experiments)
+CUtensorMapL2promotion l2_promotion() {
+  static const CUtensorMapL2promotion p = [] {
+    const char* e = getenv("GFT_L2PROMO");
+    const int v = (e && *e) ? atoi(e) : 256;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+           : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
+  return p;
+}
+
 void encode_map(CUtensorMap* m, const Kernel& k, const void* ptr, int64_t rows) {
   Driver& d = need_driver();
   const KernelCfg& c = k.cfg;
@@ -248,7 +260,7 @@ void encode_map(CUtensorMap* m, const Kernel& k, const void* ptr, int64_t rows) 
                                             : CU_TENSOR_MAP_SWIZZLE_NONE;
   ck(d.cuTensorMapEncodeTiled(m, c.elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                               2, const_cast<void*>(ptr), dims, strides, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, l2_promotion(),
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
      "cuTensorMapEncodeTiled");
 }
