@@ -248,6 +248,49 @@ def config_table(args, stream, hbm, device):
     return rows
 
 
+def mixed_cfg5_row(args, stream, hbm, device):
+    """configs[4] as one mixed batch: the cycle C64 (cfg5a) and the bipartite 128-node graph
+    (cfg5b), 2^20 signals each, forward of both per step -- back to back on one stream
+    (programmatic dependent launch overlaps the tails) and concurrently on two streams --
+    with the dense kernels of both timed alongside."""
+    import torch
+    import workloads
+    from paper_1907_07875_b200 import gft
+    ca, cb = workloads.config("cfg5a"), workloads.config("cfg5b")
+    pa, pb = gft.Plan.from_config(ca, dtypes=("f32",)), gft.Plan.from_config(cb, dtypes=("f32",))
+    g = torch.Generator(device=device).manual_seed(ca.seed)
+    Xa = torch.randn(ca.batch, ca.n, generator=g, device=device)
+    Xb = torch.randn(cb.batch, cb.n, generator=g, device=device)
+    Ya, Yb = torch.empty_like(Xa), torch.empty_like(Xb)
+    nbytes = 2 * 4 * (ca.batch * ca.n + cb.batch * cb.n)
+    sig = ca.batch + cb.batch
+    row = {"config": "cfg5 mixed (cfg5a + cfg5b)", "batch": sig}
+
+    def rec(ms):
+        return {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1), "frac": round(nbytes / ms / 1e6 / hbm, 4),
+                "signals_per_s": sig / ms * 1e3}
+
+    row["fast_fwd_one_stream"] = rec(time_kernel(lambda: (pa.forward(Xa, Ya, stream), pb.forward(Xb, Yb, stream)),
+                                                 stream, 3, args.table_iters))
+    s2 = torch.cuda.Stream(device)
+
+    def two_streams():
+        s2.wait_stream(stream)
+        pa.forward(Xa, Ya, stream)
+        with torch.cuda.stream(s2):
+            pb.forward(Xb, Yb, s2)
+        stream.wait_stream(s2)
+
+    row["fast_fwd_two_streams"] = rec(time_kernel(two_streams, stream, 3, args.table_iters))
+    row["dense_fwd_one_stream"] = rec(time_kernel(lambda: (pa.dense_forward(Xa, Ya, stream),
+                                                           pb.dense_forward(Xb, Yb, stream)),
+                                                  stream, 3, args.table_iters))
+    row["fast_vs_dense"] = round(row["dense_fwd_one_stream"]["ms"] / row["fast_fwd_one_stream"]["ms"], 3)
+    pa.close()
+    pb.close()
+    return row
+
+
 def right_haar_table(args, stream, hbm, device):
     """Right Haar stages: plans with / without them on bipartite graphs
     whose Laplacian diagonal is constant, device-resident N(0,1), 2^20 signals."""
@@ -636,6 +679,7 @@ def main():
     # only wait for them at the final barrier
     if rank == 0 and not args.no_table and ws == 1:
         table = config_table(args, stream, hbm, device)
+        table.append(mixed_cfg5_row(args, stream, hbm, device))
         rh_table = right_haar_table(args, stream, hbm, device)
         ap_table = approx_table(args, stream, hbm, device)
 
