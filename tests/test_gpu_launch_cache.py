@@ -37,3 +37,24 @@ def test_map_cache_cycles(name):
             ref_plan.inverse(X, Y)
             assert torch.equal(Y, yi)
     ref_plan.close()
+
+
+def test_mixed_cfg5_two_streams_bit_identical():
+    """configs[4]'s mixed batch: cfg5a (FMA kernel) and cfg5b (tcgen05 pair kernel) launched
+    concurrently on two streams give the same bits as one at a time."""
+    ca, cb = workloads.config("cfg5a"), workloads.config("cfg5b")
+    pa, pb = gft.Plan.from_config(ca, dtypes=("f32",)), gft.Plan.from_config(cb, dtypes=("f32",))
+    g = torch.Generator(device="cuda").manual_seed(4)
+    Xa = torch.randn(200_000, ca.n, generator=g, device="cuda")
+    Xb = torch.randn(200_000, cb.n, generator=g, device="cuda")
+    ra, rb = pa.forward(Xa), pb.forward(Xb)
+    torch.cuda.synchronize()
+    Ya, Yb = torch.empty_like(ra), torch.empty_like(rb)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        pa.forward(Xa, Ya, s1)
+        pb.forward(Xb, Yb, s2)
+    torch.cuda.synchronize()
+    assert torch.equal(Ya, ra) and torch.equal(Yb, rb)
+    pa.close()
+    pb.close()
