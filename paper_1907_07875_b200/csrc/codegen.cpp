@@ -33,7 +33,7 @@ static const char* kSkeletonTC3 =
 #include "skeleton_tc3_inc.h"
     ;
 
-KernelCfg choose_cfg(int n, int dtype, int64_t work, const CfgOverride* ov) {
+KernelCfg choose_cfg(int n, int dtype, int64_t work, const CfgOverride* ov, int kind) {
   KernelCfg c;
   c.n = n;
   c.elem = dtype == GFT_F64 ? 8 : 4;
@@ -80,7 +80,7 @@ KernelCfg choose_cfg(int n, int dtype, int64_t work, const CfgOverride* ov) {
   c.warps = std::max(2, std::min(12, (150 * 1024) / (c.stages * c.tile_bytes())));
   // measured geometry for this (n, dtype) if the tuning table has one (tools/gpu_autotune.py)
   int tR, tS, tW, tP;
-  if (tuned_geometry(n, dtype, work, tR, tS, tW, tP)) {
+  if (tuned_geometry(n, dtype, work, kind, tR, tS, tW, tP)) {
     c.R = tR;
     c.stages = tS;
     c.warps = tW;
@@ -758,7 +758,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
   k.kind = kind;
   k.dtype = dtype;
   k.cfg = choose_cfg(P.n, dtype, (kind == K_DENSE_FWD || kind == K_DENSE_INV) ? (int64_t)P.n * P.n : P.sum_k2,
-                     ov);
+                     ov, kind);
   static const char* kKindNameTC[] = {"fwdtc", "invtc", "", "", "filttc"};
   const Dir dir = kind == K_FAST_INV ? DIR_INV : kind == K_FILTER ? DIR_FILTER : DIR_FWD;
   if (allow_tc && (kind == K_FAST_FWD || kind == K_FAST_INV || kind == K_FILTER)) {

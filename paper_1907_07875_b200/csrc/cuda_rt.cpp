@@ -279,11 +279,12 @@ constexpr int64_t kMaxRowsPerLaunch = (int64_t)1 << 30;
 
 }  // namespace
 
-bool tuned_geometry(int n, int dtype, int64_t work, int& R, int& S, int& W, int& pace_ns) {
-  // lines: "fma <n> <f32|f64> <R> <S> <W> [work=<FMAs per signal>] [pace=<ns>]"; an entry with
-  // a work key applies only to kernels with exactly that much leaf work (plan-specific
-  // measurement); pace = per-tile __nanosleep of the FMA skeleton (0 = none)
-  struct Entry { int n, dt, R, S, W, pace; int64_t work; };
+bool tuned_geometry(int n, int dtype, int64_t work, int kind, int& R, int& S, int& W, int& pace_ns) {
+  // lines: "fma <n> <f32|f64> <R> <S> <W> [work=<FMAs per signal>] [kind=fwd|inv|dfwd|dinv|filter]
+  // [pace=<ns>]"; an entry with a work / kind key applies only to kernels with exactly that
+  // leaf work / of that kind (plan-specific measurements); the most specific match wins
+  // (work and kind > work > kind > plain).  pace = per-tile __nanosleep of the FMA skeleton.
+  struct Entry { int n, dt, R, S, W, pace, kind; int64_t work; };
   static const std::vector<Entry> table = [] {
     std::vector<Entry> t;
     const char* e = getenv("GFT_TUNING_FILE");
@@ -291,6 +292,7 @@ bool tuned_geometry(int n, int dtype, int64_t work, int& R, int& S, int& W, int&
     if (path == "none") return t;
     std::ifstream f(path);
     std::string line;
+    static const char* kKinds[] = {"fwd", "inv", "dfwd", "dinv", "filter"};
     while (std::getline(f, line)) {
       std::istringstream ss(line);
       std::string mode, dt, extra;
@@ -299,20 +301,27 @@ bool tuned_geometry(int n, int dtype, int64_t work, int& R, int& S, int& W, int&
       x.dt = dt == "f64" ? GFT_F64 : GFT_F32;
       x.work = -1;
       x.pace = 0;
+      x.kind = -1;
       while ((ss >> extra) && extra[0] != '#') {
         if (extra.rfind("work=", 0) == 0) x.work = std::atoll(extra.c_str() + 5);
         else if (extra.rfind("pace=", 0) == 0) x.pace = std::atoi(extra.c_str() + 5);
+        else if (extra.rfind("kind=", 0) == 0)
+          for (int k = 0; k < 5; ++k)
+            if (extra.substr(5) == kKinds[k]) x.kind = k;
       }
       t.push_back(x);
     }
     return t;
   }();
   const Entry* hit = nullptr;
-  for (const Entry& x : table)
-    if (x.n == n && x.dt == dtype && (x.work == work || (x.work < 0 && !hit))) {
-      hit = &x;
-      if (x.work == work) break;
-    }
+  int best = -1;
+  for (const Entry& x : table) {
+    if (x.n != n || x.dt != dtype) continue;
+    if (x.work >= 0 && x.work != work) continue;
+    if (x.kind >= 0 && x.kind != kind) continue;
+    const int score = (x.work >= 0 ? 2 : 0) + (x.kind >= 0 ? 1 : 0);
+    if (score > best) { best = score; hit = &x; }
+  }
   if (!hit) return false;
   R = hit->R; S = hit->S; W = hit->W; pace_ns = hit->pace;
   return true;

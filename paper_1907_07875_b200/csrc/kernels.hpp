@@ -48,7 +48,7 @@ struct KernelCfg {
 // work = FMAs per signal of the kernel body (selects plan-specific tuning entries)
 // Geometry / pacing overrides of the FMA skeleton (gft_plan_tune candidates); -1 = keep.
 struct CfgOverride { int R = -1, stages = -1, warps = -1, pace_ns = -1; };
-KernelCfg choose_cfg(int n, int dtype, int64_t work = -1, const CfgOverride* ov = nullptr);
+KernelCfg choose_cfg(int n, int dtype, int64_t work = -1, const CfgOverride* ov = nullptr, int kind = -1);
 
 struct LoadedFn {
   void* module = nullptr;   // CUmodule
@@ -99,6 +99,6 @@ std::string cubin_cache_dir();
 // Measured geometry table (paper_1907_07875_b200/tuning.tsv, written by
 // tools/gpu_autotune.py on a B200): lines "fma <n> <f32|f64> <R> <S> <W>".  Returns false
 // if (n, dtype) has no entry.  GFT_TUNING_FILE overrides the path ("none" disables).
-bool tuned_geometry(int n, int dtype, int64_t work, int& R, int& S, int& W, int& pace_ns);
+bool tuned_geometry(int n, int dtype, int64_t work, int kind, int& R, int& S, int& W, int& pace_ns);
 
 }  // namespace gft

@@ -179,3 +179,24 @@ def test_tuning_record_get_set_on_cpu():
     with pytest.raises(G.GFTError) as ei:
         t.set_tuning({0: (1, 2, 4, 0)}, "f32")
     assert ei.value.name == "GFT_ERR_UNSUPPORTED"
+
+
+def test_tuning_table_kind_and_work_keys():
+    """tuning.tsv entries keyed by kind= and work= reach only their kernels (most specific
+    match wins): cfg4's fused filter and cfg1's inverse have their own measured geometry."""
+    def geo(src):
+        return tuple(int(re.search(r"#define %s (\d+)" % k, src).group(1)) for k in ("GFT_R", "GFT_STAGES", "GFT_WARPS"))
+
+    def pace(src):
+        m = re.search(r"#define GFT_PACE_NS (\d+)", src)
+        return int(m.group(1)) if m else 0
+
+    c4 = G.Plan.from_config(workloads.config("cfg4"), dtypes=("f32",))
+    assert geo(c4.kernel_source(0, "f32")) == (2, 2, 4) and pace(c4.kernel_source(0, "f32")) == 0
+    f4 = G.Filter(c4, np.ones(64), dtypes=("f32",))
+    assert geo(f4.kernel_source("f32")) == (1, 2, 8) and pace(f4.kernel_source("f32")) == 150
+    c1 = G.Plan.from_config(workloads.config("cfg1"), dtypes=("f32",))
+    assert geo(c1.kernel_source(0, "f32")) == (8, 3, 4) and pace(c1.kernel_source(0, "f32")) == 0
+    assert geo(c1.kernel_source(1, "f32")) == (8, 2, 8) and pace(c1.kernel_source(1, "f32")) == 150
+    # the dense kernels of cfg1 take the plain n = 8 entry
+    assert geo(c1.kernel_source(2, "f32")) == (8, 3, 4)
