@@ -164,7 +164,12 @@ GFT_API gft_status gft_plan_destroy(gft_plan plan);   /* caller must have synchr
  * GFT_ERR_INVALID_ARG on malformed input, GFT_ERR_UNSUPPORTED on another format version);
  * opts supplies only dtypes and flags for kernel generation (the planning options are part
  * of the serialized plan).  Kernels are regenerated deterministically, so they carry the same
- * names as the original plan's and reuse its AOT / NVRTC cubins. */
+ * names as the original plan's and reuse its AOT / NVRTC cubins.
+ * Tuning: kernels whose FMA-skeleton geometry differs from the generator's own choice
+ * (measured by gft_plan_tune or set by gft_plan_tuning_set) are
+ * recorded in an optional trailer ({dtype, kind, R, stages, warps, pace_ns} per kernel) and
+ * re-applied on load, so a tuned plan needs no re-measuring; a malformed trailer is
+ * GFT_ERR_INVALID_ARG.  Records for a dtype not prepared on load are ignored. */
 GFT_API gft_status gft_plan_serialize(gft_plan plan, void* buf, size_t cap, size_t* size_out);
 GFT_API gft_status gft_plan_deserialize(gft_plan* out, const void* buf, size_t size,
                                         const gft_plan_opts* opts);
@@ -250,7 +255,7 @@ GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kin
  * choice_out: NULL or int32_t[16]; for kind k, choice_out[4k..4k+3] = {R, stages, warps,
  *   pace_ns} of the kernel kept (-1s: kind not tuned / tensor-core kernel).
  * Synchronous on `stream`.  Not thread-safe with respect to concurrent calls on the same plan
- * (it replaces kernels); the choice is per process (not serialised with the plan).
+ * (it replaces kernels); gft_plan_serialize records the choice (tuning trailer).
  * Errors: GFT_ERR_INVALID_ARG (NULL / bad sizes / unknown flags), GFT_ERR_ALIGNMENT,
  * GFT_ERR_UNSUPPORTED (dtype not prepared), GFT_ERR_COMPILE, GFT_ERR_NO_DEVICE / GFT_ERR_CUDA. */
 #define GFT_TUNE_GEOMETRY 1u
@@ -259,7 +264,7 @@ GFT_API gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_
                                  int32_t* choice_out);
 /* Tuning records ("wisdom"): the FMA-skeleton geometry of one kernel of a plan,
  * cfg4 = {R rows per thread, stages, warps, pace_ns}, so a tuned choice can be stored next to
- * the serialised plan and re-applied after gft_plan_deserialize without re-measuring.
+ * the serialised plan (gft_plan_serialize does so itself) and re-applied after load.
  * get: -1s for a tensor-core kernel.  set: regenerates the kernel (compiled at its next
  * launch or gft_plan_compile); GFT_ERR_UNSUPPORTED for a tensor-core kernel,
  * GFT_ERR_INVALID_ARG for values outside R in {1,2,4,8}, stages 2..8, warps 1..16,

@@ -97,10 +97,43 @@ void make_kernels(gft_plan_s& p, const gft_plan_opts& o) {
 
 extern "C" {
 
+namespace {
+// Tuning trailer of a serialised plan: "GFTTUNE1", u32 count, then count x {i32 dtype, kind,
+// R, stages, warps, pace_ns} -- the FMA-skeleton kernels whose geometry differs from what the
+// generator would choose by itself (i.e. measured by gft_plan_tune or set by
+// gft_plan_tuning_set), re-applied by gft_plan_deserialize.
+constexpr char kTuneMagic[8] = {'G', 'F', 'T', 'T', 'U', 'N', 'E', '1'};
+
+std::vector<uint8_t> tuning_trailer(gft_plan plan) {
+  std::vector<int32_t> recs;
+  for (int dt = 0; dt < 2; ++dt)
+    for (int kind = 0; kind < gft::K_NUM; ++kind) {
+      const auto& k = plan->k[dt][kind];
+      if (!k || k->cfg.tc) continue;
+      gft::Kernel def;
+      gft::generate_kernel(plan->P, kind, dt, def, !(plan->flags & GFT_FLAG_NO_TENSOR_CORES),
+                           (plan->flags & GFT_FLAG_DENSE_TC) != 0);
+      if (def.name == k->name) continue;
+      recs.insert(recs.end(), {dt, kind, k->cfg.R, k->cfg.stages, k->cfg.warps, k->cfg.pace_ns});
+    }
+  std::vector<uint8_t> b;
+  if (recs.empty()) return b;
+  b.insert(b.end(), kTuneMagic, kTuneMagic + 8);
+  const uint32_t cnt = (uint32_t)(recs.size() / 6);
+  const uint8_t* pc = reinterpret_cast<const uint8_t*>(&cnt);
+  b.insert(b.end(), pc, pc + 4);
+  const uint8_t* pr = reinterpret_cast<const uint8_t*>(recs.data());
+  b.insert(b.end(), pr, pr + recs.size() * 4);
+  return b;
+}
+}  // namespace
+
 gft_status gft_plan_serialize(gft_plan plan, void* buf, size_t cap, size_t* size_out) {
   return guard([&] {
     if (!plan || !size_out) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
-    const std::vector<uint8_t> b = gft::serialize_plan(plan->P);
+    std::vector<uint8_t> b = gft::serialize_plan(plan->P);
+    const std::vector<uint8_t> t = tuning_trailer(plan);
+    b.insert(b.end(), t.begin(), t.end());
     *size_out = b.size();
     if (!buf) return;   // size query
     if (cap < b.size()) gft::fail(GFT_ERR_INVALID_ARG, "buffer too small (see *size_out)");
@@ -117,8 +150,32 @@ gft_status gft_plan_deserialize(gft_plan* out, const void* buf, size_t size, con
     if (opts) o = *opts;
     if (o.dtypes & ~3u) gft::fail(GFT_ERR_UNSUPPORTED, "unknown dtype bits");
     std::unique_ptr<gft_plan_s> p(new gft_plan_s);
-    p->P = gft::deserialize_plan(static_cast<const uint8_t*>(buf), size);
+    const uint8_t* bytes = static_cast<const uint8_t*>(buf);
+    size_t used = 0;
+    p->P = gft::deserialize_plan(bytes, size, &used);
+    // optional tuning trailer (validated as strictly as the plan itself)
+    std::vector<int32_t> recs;
+    if (used != size) {
+      const size_t rest = size - used;
+      if (rest < 12 || std::memcmp(bytes + used, kTuneMagic, 8) != 0)
+        gft::fail(GFT_ERR_INVALID_ARG, "serialized plan: trailing bytes");
+      uint32_t cnt;
+      std::memcpy(&cnt, bytes + used + 8, 4);
+      if (cnt > 2 * gft::K_NUM || rest != 12 + (size_t)cnt * 24)
+        gft::fail(GFT_ERR_INVALID_ARG, "serialized plan: bad tuning trailer");
+      recs.resize((size_t)cnt * 6);
+      std::memcpy(recs.data(), bytes + used + 12, recs.size() * 4);
+    }
     make_kernels(*p, o);
+    gft_plan plan = p.get();
+    for (size_t i = 0; i + 6 <= recs.size(); i += 6) {
+      const int dt = recs[i], kind = recs[i + 1];
+      if (dt < 0 || dt > 1 || kind < 0 || kind >= gft::K_NUM)
+        gft::fail(GFT_ERR_INVALID_ARG, "serialized plan: bad tuning record");
+      if (!plan->k[dt][kind]) continue;   // dtype not prepared in this process
+      const gft_status st = gft_plan_tuning_set(plan, (gft_dtype)dt, kind, &recs[i + 2]);
+      if (st != GFT_OK) gft::fail(st, std::string("serialized plan: tuning record: ") + gft_last_error());
+    }
     *out = p.release();
   });
 }

@@ -179,6 +179,7 @@ Plan build_plan(const SubGraph& g, const int32_t* user_phi, const PlanOptions& o
 // Plan persistence (serialize.cpp): a versioned byte string of the whole factorisation;
 // deserialize validates every index and size and throws GFT_ERR_INVALID_ARG on malformed input.
 std::vector<uint8_t> serialize_plan(const Plan& P);
-Plan deserialize_plan(const uint8_t* buf, size_t size);
+// consumed (optional): bytes of `buf` the plan occupies; without it, trailing bytes are an error
+Plan deserialize_plan(const uint8_t* buf, size_t size, size_t* consumed = nullptr);
 
 }  // namespace gft

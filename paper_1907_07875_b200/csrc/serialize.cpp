@@ -125,7 +125,7 @@ std::vector<uint8_t> serialize_plan(const Plan& P) {
   return w.b;
 }
 
-Plan deserialize_plan(const uint8_t* buf, size_t size) {
+Plan deserialize_plan(const uint8_t* buf, size_t size, size_t* consumed) {
   Reader r{buf, size};
   if (size < 12 || std::memcmp(buf, kMagic, 8) != 0) fail(GFT_ERR_INVALID_ARG, "not a serialized gft plan");
   r.off = 8;
@@ -254,7 +254,8 @@ Plan deserialize_plan(const uint8_t* buf, size_t size) {
   P.sum_kk1 = r.pod<int64_t>();
   P.residual = r.pod<double>();
   P.orth_error = r.pod<double>();
-  if (r.off != size) fail(GFT_ERR_INVALID_ARG, "serialized plan: trailing bytes");
+  if (consumed) *consumed = r.off;
+  else if (r.off != size) fail(GFT_ERR_INVALID_ARG, "serialized plan: trailing bytes");
   return P;
 }
 

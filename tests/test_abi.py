@@ -169,6 +169,17 @@ def test_tuning_record_get_set_on_cpu():
     q = G.Plan.load(p.save(), dtypes=("f32",))
     q.set_tuning(p.tuning("f32", (0,)), "f32")
     assert q.kernel_name(0, "f32") == p.kernel_name(0, "f32")
+    # the serialised plan carries the non-default records itself (tuning trailer)
+    blob = p.save()
+    r = G.Plan.load(blob, dtypes=("f32",))
+    assert r.kernel_name(0, "f32") == p.kernel_name(0, "f32")
+    assert r.kernel_name(1, "f32") == p.kernel_name(1, "f32")          # untouched kind: default
+    untuned = G.Plan.from_config(cfg, dtypes=("f32",))
+    assert len(untuned.save()) < len(blob)                                # no trailer when untuned
+    for bad in (blob + b"x", blob[:-1], blob[:-24] + b"\x00" * 24):
+        with pytest.raises(G.GFTError) as ei:
+            G.Plan.load(bad, dtypes=("f32",))
+        assert ei.value.name == "GFT_ERR_INVALID_ARG"
     for bad in ((3, 2, 4, 0), (1, 1, 4, 0), (1, 2, 0, 0), (1, 2, 4, -1), (8, 8, 16, 0)):
         with pytest.raises(G.GFTError) as ei:
             p.set_tuning({0: bad}, "f32")

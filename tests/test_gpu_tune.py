@@ -121,3 +121,21 @@ def test_tuning_record_replay_bit_identical():
     assert torch.equal(Y0, Y1) and torch.equal(Z1, plan.inverse(Y0))
     q.close()
     plan.close()
+
+
+def test_tuned_plan_round_trips_through_serialize():
+    """A plan tuned on the device serialises its tuning: the reloaded plan has the same
+    kernels (names) and computes the same bits, with no re-measuring."""
+    cfg = workloads.config("cfg1")
+    cfg.batch = 1 << 20
+    plan = gft.Plan.from_config(cfg, dtypes=("f32",))
+    plan.set_tuning({0: (4, 2, 12, 300)}, "f32")        # force a non-default record
+    plan.tune("f32", (1,), batch=1 << 18, reps=2, geometry=True)
+    q = gft.Plan.load(plan.save(), dtypes=("f32",))
+    for k in (0, 1):
+        assert q.kernel_name(k, "f32") == plan.kernel_name(k, "f32")
+    X = torch.randn(70_001, cfg.n, device="cuda")
+    torch.cuda.synchronize()
+    assert torch.equal(q.forward(X), plan.forward(X)) and torch.equal(q.inverse(X), plan.inverse(X))
+    q.close()
+    plan.close()
