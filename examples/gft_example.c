@@ -85,6 +85,14 @@ int main(int argc, char** argv) {
   CHECK_GFT(gft_inverse(plan, dy, dx, batch, GFT_F32, NULL));   /* back into dx */
   CHECK_CUDA(cudaMemcpy(hz, dx, sizeof(float) * count, cudaMemcpyDeviceToHost));
 
+  /* measured tuning of the forward kernel (geometry + request pacing, timed on dx -> dy);
+   * the arithmetic is unchanged, so the reloaded plan below must still reproduce hy bit for
+   * bit -- and it carries the tuning in its serialised bytes */
+  int32_t choice[16];
+  CHECK_GFT(gft_plan_tune(plan, GFT_F32, 1u, GFT_TUNE_GEOMETRY, dx, dy, batch, 3, NULL, choice));
+  printf("tuned forward kernel: R %d, stages %d, warps %d, pace %d ns\n", choice[0], choice[1], choice[2],
+         choice[3]);
+
   /* plan persistence: serialise (size query first), reload, and the reloaded plan's
    * forward must be bit-identical (same decomposition -> same generated kernel) */
   size_t blob_size = 0;
