@@ -381,12 +381,15 @@ def approx_table(args, stream, hbm, device):
         else:
             Uh = plan.basis()
             row.update(delta=round(delta(Uh, exact[label]), 5), epsilon=round(eps(Uh, exact[label]), 5))
-        # measured pacing (gft_plan_tune) for FMA-skeleton kernels, then re-timed
+        # measured tuning (gft_plan_tune: pacing of FMA-skeleton kernels, the kernel variant of
+        # tcgen05 plans), then re-timed
+        name0 = plan.kernel_name(0, "f32")
         paces = plan.tune("f32", (0,), X, Y, stream=stream)
-        if 0 in paces:
+        if 0 in paces or plan.kernel_name(0, "f32") != name0:
             ms = time_kernel(lambda: plan.forward(X, Y, stream), stream, 3, args.table_iters)
             row["fast_fwd_tuned"] = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
-                                     "frac": round(nbytes / ms / 1e6 / hbm, 4), "geometry_pace": paces[0]}
+                                     "frac": round(nbytes / ms / 1e6 / hbm, 4), "geometry_pace": paces.get(0),
+                                     "kernel": plan.kernel_name(0, "f32")}
         rows.append(row)
         plan.close()
     return rows

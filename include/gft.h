@@ -246,14 +246,18 @@ GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kin
  *   2. the kernel is regenerated with each per-tile pacing in {0, 150, 300, 450} ns;
  * candidates are compiled in parallel (NVRTC) and timed twice over `reps` back-to-back
  * launches (after 2 untimed ones) on X -> Y with driver events on `stream`; the fastest
- * replaces the plan's kernel if it beats the current one by more than 1%.  Tensor-core
- * kernels are left as they are.  The arithmetic is unchanged, so every candidate computes
- * bit-identical outputs.
+ * replaces the plan's kernel if it beats the current one by more than 1%.  For a kernel on
+ * the tensor cores the candidates are instead the tcgen05 kernel variants that apply (plain
+ * CTA pair, pair with two compute warpgroups, warp-specialised pair, single CTA), same rule;
+ * their choice is not part of the tuning records / serialised trailer.  FMA-skeleton
+ * candidates change no arithmetic, so they compute bit-identical outputs; tcgen05 variants
+ * compute the same 3xTF32 products (fp32-accurate, not guaranteed bit-identical).
  * X, Y: caller-owned device buffers of >= batch x n elements of `dtype` (16-byte aligned,
  *   distinct); X is read, Y is overwritten.  batch should exceed L2 (e.g. >= 256 MiB of rows)
  *   for the timing to reflect HBM streaming.  reps <= 0 selects 10.
  * choice_out: NULL or int32_t[16]; for kind k, choice_out[4k..4k+3] = {R, stages, warps,
- *   pace_ns} of the kernel kept (-1s: kind not tuned / tensor-core kernel).
+ *   pace_ns} of the kernel kept (-1s: kind not tuned / tensor-core kernel, whose variant is
+ *   visible in gft_plan_kernel_name: tc / tc2 / tc2w / tc3).
  * Synchronous on `stream`.  Not thread-safe with respect to concurrent calls on the same plan
  * (it replaces kernels); gft_plan_serialize records the choice (tuning trailer).
  * Errors: GFT_ERR_INVALID_ARG (NULL / bad sizes / unknown flags), GFT_ERR_ALIGNMENT,

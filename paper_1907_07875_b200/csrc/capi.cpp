@@ -455,8 +455,35 @@ void tune_slot(const gft::Plan& P, std::unique_ptr<gft::Kernel>& slot, int kind,
                int reps, gft_stream stream, int32_t* out4) {
   static const int kPace[] = {0, 150, 300, 450};
   gft::Kernel& cur = *slot;
-  if (cur.cfg.tc) return;
   const double t_cur = gft::time_kernel_ms(cur, X, Y, batch, stream, 2, reps, cache);
+  if (cur.cfg.tc) {
+    // tensor-core plan: measure the kernel variants (plain pair / two-warpgroup pair /
+    // warp-specialised / single CTA) that apply, keep the fastest if > 1% better
+    std::set<std::string> seen{cur.name};
+    std::vector<TuneCand> cs;
+    for (int v = 0; v < 4; ++v) {
+      TuneCand c;
+      c.ov.tc_variant = v;
+      c.k.reset(new gft::Kernel);
+      gft::generate_kernel(P, kind, dtype, *c.k, allow_tc, dense_tc, &c.ov);
+      if (!c.k->cfg.tc || !seen.insert(c.k->name).second) continue;
+      cs.push_back(std::move(c));
+    }
+    compile_parallel(cs, cache);
+    TuneCand* b = nullptr;
+    for (int round = 0; round < 2; ++round)
+      for (auto& c : cs) {
+        c.ms = std::min(c.ms, gft::time_kernel_ms(*c.k, X, Y, batch, stream, 2, reps, cache));
+        if (round == 1 && (!b || c.ms < b->ms)) b = &c;
+      }
+    if (b && b->ms < 0.99 * t_cur) {
+      gft::unload_kernel(cur);
+      slot = std::move(b->k);
+    }
+    for (auto& c : cs)
+      if (c.k) gft::unload_kernel(*c.k);
+    return;
+  }
   std::set<std::string> seen{cur.name};
   std::vector<TuneCand> pool;   // every timed candidate (the winner is moved out of it)
   // candidates -> generated (deduplicated by kernel name) -> compiled -> timed twice

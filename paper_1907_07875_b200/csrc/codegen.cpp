@@ -774,7 +774,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
     const char* pst = getenv("GFT_TC_PAIR_MAXSTAGES");
     for (int st = (pst && *pst) ? atoi(pst) : 4; st >= 2 && !ok; --st)
       if (plan_tc(P, dtype, st, true, T, tmem_cols, b_bytes) && (int)T.size() == nbig &&
-          getenv("GFT_NO_CTA_PAIR") == nullptr) {
+          getenv("GFT_NO_CTA_PAIR") == nullptr && !(ov && ov->tc_variant == 3)) {
         ok = pair = true;
         stages = st;
       }
@@ -788,7 +788,9 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
     // and n <= 80 qualify (measured: +4-5% at n = 64 with two 32-leaves, -6% with an FMA
     // leaf beside them; tools/tc_vs_fma.py)
     int wgs = 1, wg_cols = 0;
-    if (ok && pair && P.n <= 80 && T.size() == P.leaves.size() && getenv("GFT_NO_TC_2WG") == nullptr) {
+    const bool no_2wg = getenv("GFT_NO_TC_2WG") != nullptr || (ov && ov->tc_variant == 0);
+    const bool no_ws = getenv("GFT_NO_TC_WS") != nullptr || (ov && (ov->tc_variant == 0 || ov->tc_variant == 1));
+    if (ok && pair && P.n <= 80 && T.size() == P.leaves.size() && !no_2wg) {
       for (const auto& t : T) wg_cols = std::max(wg_cols, t.d_col + ru(t.np, 32));
       if (2 * wg_cols <= 512) {
         std::vector<TcLeaf> T2;
@@ -812,7 +814,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
     bool ws = false;
     int ws_a = 0, ws_d = 0, ws_tmem = 0;
     std::vector<TcLeaf> Tws;
-    if (ok && pair && P.n <= 64 && getenv("GFT_NO_TC_WS") == nullptr) {
+    if (ok && pair && P.n <= 64 && !no_ws) {
       Tws = T;
       if (ws_layout(Tws, ws_a, ws_d, ws_tmem)) {
         const int tile = 128 * ((P.n + 31) / 32 * 32) * 4;

@@ -47,7 +47,9 @@ struct KernelCfg {
 
 // work = FMAs per signal of the kernel body (selects plan-specific tuning entries)
 // Geometry / pacing overrides of the FMA skeleton (gft_plan_tune candidates); -1 = keep.
-struct CfgOverride { int R = -1, stages = -1, warps = -1, pace_ns = -1; };
+// tc_variant (tensor-core plans): -1 rule-based default, 0 plain CTA pair, 1 CTA pair with two
+// compute warpgroups, 2 warp-specialised pair, 3 single CTA (each where it applies).
+struct CfgOverride { int R = -1, stages = -1, warps = -1, pace_ns = -1, tc_variant = -1; };
 KernelCfg choose_cfg(int n, int dtype, int64_t work = -1, const CfgOverride* ov = nullptr, int kind = -1);
 
 struct LoadedFn {

@@ -30,13 +30,20 @@ def test_tune_bit_identical(name, dtype):
     plan.close()
 
 
-def test_tune_skips_tensor_core_kernels():
+def test_tune_tensor_core_variants():
+    """On a tcgen05 plan the tuner measures the kernel variants (no FMA record is returned);
+    whichever it keeps is a tensor-core kernel computing the transform to fp32 accuracy."""
     cfg = workloads.config("cfg5b")
     plan = gft.Plan.from_config(cfg, dtypes=("f32",))
     assert "tc" in plan.kernel_name(0, "f32")
-    name = plan.kernel_name(0, "f32")
-    paces = plan.tune("f32", (0, 1), batch=1 << 12, reps=1)
-    assert paces == {} and plan.kernel_name(0, "f32") == name
+    X = torch.randn(1 << 18, cfg.n, device="cuda")
+    Y0 = plan.forward(X)
+    paces = plan.tune("f32", (0, 1), X=X, reps=2)
+    assert paces == {} and "tc" in plan.kernel_name(0, "f32") and "tc" in plan.kernel_name(1, "f32")
+    Y1 = plan.forward(X)
+    torch.cuda.synchronize()
+    rel = ((Y1 - Y0).double().norm(dim=1) / Y0.double().norm(dim=1)).max().item()
+    assert rel <= 1e-6
     plan.close()
 
 
