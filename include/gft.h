@@ -165,9 +165,9 @@ GFT_API gft_status gft_plan_destroy(gft_plan plan);   /* caller must have synchr
  * opts supplies only dtypes and flags for kernel generation (the planning options are part
  * of the serialized plan).  Kernels are regenerated deterministically, so they carry the same
  * names as the original plan's and reuse its AOT / NVRTC cubins.
- * Tuning: kernels whose FMA-skeleton geometry differs from the generator's own choice
- * (measured by gft_plan_tune or set by gft_plan_tuning_set) are
- * recorded in an optional trailer ({dtype, kind, R, stages, warps, pace_ns} per kernel) and
+ * Tuning: kernels that differ from the generator's own choice (measured by gft_plan_tune or
+ * set by gft_plan_tuning_set) are recorded in an optional trailer ({dtype, kind, rec5} per
+ * kernel, see gft_plan_tuning_get) and
  * re-applied on load, so a tuned plan needs no re-measuring; a malformed trailer is
  * GFT_ERR_INVALID_ARG.  Records for a dtype not prepared on load are ignored. */
 GFT_API gft_status gft_plan_serialize(gft_plan plan, void* buf, size_t cap, size_t* size_out);
@@ -249,7 +249,7 @@ GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kin
  * replaces the plan's kernel if it beats the current one by more than 1%.  For a kernel on
  * the tensor cores the candidates are instead the tcgen05 kernel variants that apply (plain
  * CTA pair, pair with two compute warpgroups, warp-specialised pair, single CTA), same rule;
- * their choice is not part of the tuning records / serialised trailer.  FMA-skeleton
+ * the choice is recorded like a geometry (gft_plan_tuning_get).  FMA-skeleton
  * candidates change no arithmetic, so they compute bit-identical outputs; tcgen05 variants
  * compute the same 3xTF32 products (fp32-accurate, not guaranteed bit-identical).
  * X, Y: caller-owned device buffers of >= batch x n elements of `dtype` (16-byte aligned,
@@ -266,16 +266,19 @@ GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kin
 GFT_API gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, uint32_t flags,
                                  const void* X, void* Y, int64_t batch, int32_t reps, gft_stream stream,
                                  int32_t* choice_out);
-/* Tuning records ("wisdom"): the FMA-skeleton geometry of one kernel of a plan,
- * cfg4 = {R rows per thread, stages, warps, pace_ns}, so a tuned choice can be stored next to
- * the serialised plan (gft_plan_serialize does so itself) and re-applied after load.
- * get: -1s for a tensor-core kernel.  set: regenerates the kernel (compiled at its next
- * launch or gft_plan_compile); GFT_ERR_UNSUPPORTED for a tensor-core kernel,
+/* Tuning records ("wisdom") of one kernel of a plan: rec5 = {R rows per thread, stages,
+ * warps, pace_ns, tc_variant}.  An FMA-skeleton kernel has tc_variant -1; a tcgen05 kernel
+ * has -1 in the first four and its variant (0 plain CTA pair, 1 pair with two compute
+ * warpgroups, 2 warp-specialised pair, 3 single CTA; -1 for the opt-in IO-split kernel).
+ * gft_plan_serialize stores the records of every kernel that differs from the generator's own
+ * choice and gft_plan_deserialize re-applies them; set can also apply one by hand.
+ * set: regenerates the kernel (compiled at its next launch or gft_plan_compile);
  * GFT_ERR_INVALID_ARG for values outside R in {1,2,4,8}, stages 2..8, warps 1..16,
- * pace 0..100000 or a geometry whose shared memory does not fit.  Needs no GPU.  Not
- * thread-safe with respect to concurrent calls on the same plan. */
-GFT_API gft_status gft_plan_tuning_get(gft_plan plan, gft_dtype dtype, int32_t kind, int32_t* cfg4);
-GFT_API gft_status gft_plan_tuning_set(gft_plan plan, gft_dtype dtype, int32_t kind, const int32_t* cfg4);
+ * pace 0..100000 (FMA kernels, tc_variant -1), tc_variant outside 0..3 (tcgen05 kernels), or
+ * a record the kernel cannot realise (shared memory, variant not applicable).  Needs no GPU.
+ * Not thread-safe with respect to concurrent calls on the same plan. */
+GFT_API gft_status gft_plan_tuning_get(gft_plan plan, gft_dtype dtype, int32_t kind, int32_t* rec5);
+GFT_API gft_status gft_plan_tuning_set(gft_plan plan, gft_dtype dtype, int32_t kind, const int32_t* rec5);
 
 /* The same measured tuning for a filter's kernel (gft_filter_apply): X, Y, batch, reps,
  * flags, stream as above; choice_out: NULL or int32_t[4] = {R, stages, warps, pace_ns}

@@ -98,28 +98,46 @@ void make_kernels(gft_plan_s& p, const gft_plan_opts& o) {
 extern "C" {
 
 namespace {
-// Tuning trailer of a serialised plan: "GFTTUNE1", u32 count, then count x {i32 dtype, kind,
-// R, stages, warps, pace_ns} -- the FMA-skeleton kernels whose geometry differs from what the
-// generator would choose by itself (i.e. measured by gft_plan_tune or set by
-// gft_plan_tuning_set), re-applied by gft_plan_deserialize.
-constexpr char kTuneMagic[8] = {'G', 'F', 'T', 'T', 'U', 'N', 'E', '1'};
+// Tuning trailer of a serialised plan: "GFTTUNE2", u32 count, then count x {i32 dtype, kind,
+// R, stages, warps, pace_ns, tc_variant} -- the kernels that differ from what the generator
+// would choose by itself (measured by gft_plan_tune or set by gft_plan_tuning_set),
+// re-applied by gft_plan_deserialize.
+constexpr char kTuneMagic[8] = {'G', 'F', 'T', 'T', 'U', 'N', 'E', '2'};
+
+// {R, stages, warps, pace_ns, tc_variant} of a kernel: the FMA-skeleton geometry (variant -1),
+// or -1s and the tcgen05 variant (0 plain pair, 1 two-warpgroup pair, 2 warp-specialised,
+// 3 single CTA; -1 for the opt-in IO-split kernel)
+void tuning_record(const gft::Kernel& k, int32_t* r5) {
+  if (!k.cfg.tc) {
+    r5[0] = k.cfg.R;
+    r5[1] = k.cfg.stages;
+    r5[2] = k.cfg.warps;
+    r5[3] = k.cfg.pace_ns;
+    r5[4] = -1;
+    return;
+  }
+  r5[0] = r5[1] = r5[2] = r5[3] = -1;
+  r5[4] = !k.cfg.tc_pair ? 3 : k.cfg.tc_io_split ? -1 : k.cfg.tc_ws ? 2 : k.cfg.tc_wgs == 2 ? 1 : 0;
+}
 
 std::vector<uint8_t> tuning_trailer(gft_plan plan) {
   std::vector<int32_t> recs;
   for (int dt = 0; dt < 2; ++dt)
     for (int kind = 0; kind < gft::K_NUM; ++kind) {
       const auto& k = plan->k[dt][kind];
-      if (!k || k->cfg.tc) continue;
+      if (!k) continue;
       gft::Kernel def;
       gft::generate_kernel(plan->P, kind, dt, def, !(plan->flags & GFT_FLAG_NO_TENSOR_CORES),
                            (plan->flags & GFT_FLAG_DENSE_TC) != 0);
       if (def.name == k->name) continue;
-      recs.insert(recs.end(), {dt, kind, k->cfg.R, k->cfg.stages, k->cfg.warps, k->cfg.pace_ns});
+      int32_t r5[5];
+      tuning_record(*k, r5);
+      recs.insert(recs.end(), {dt, kind, r5[0], r5[1], r5[2], r5[3], r5[4]});
     }
   std::vector<uint8_t> b;
   if (recs.empty()) return b;
   b.insert(b.end(), kTuneMagic, kTuneMagic + 8);
-  const uint32_t cnt = (uint32_t)(recs.size() / 6);
+  const uint32_t cnt = (uint32_t)(recs.size() / 7);
   const uint8_t* pc = reinterpret_cast<const uint8_t*>(&cnt);
   b.insert(b.end(), pc, pc + 4);
   const uint8_t* pr = reinterpret_cast<const uint8_t*>(recs.data());
@@ -161,14 +179,14 @@ gft_status gft_plan_deserialize(gft_plan* out, const void* buf, size_t size, con
         gft::fail(GFT_ERR_INVALID_ARG, "serialized plan: trailing bytes");
       uint32_t cnt;
       std::memcpy(&cnt, bytes + used + 8, 4);
-      if (cnt > 2 * gft::K_NUM || rest != 12 + (size_t)cnt * 24)
+      if (cnt > 2 * gft::K_NUM || rest != 12 + (size_t)cnt * 28)
         gft::fail(GFT_ERR_INVALID_ARG, "serialized plan: bad tuning trailer");
-      recs.resize((size_t)cnt * 6);
+      recs.resize((size_t)cnt * 7);
       std::memcpy(recs.data(), bytes + used + 12, recs.size() * 4);
     }
     make_kernels(*p, o);
     gft_plan plan = p.get();
-    for (size_t i = 0; i + 6 <= recs.size(); i += 6) {
+    for (size_t i = 0; i + 7 <= recs.size(); i += 7) {
       const int dt = recs[i], kind = recs[i + 1];
       if (dt < 0 || dt > 1 || kind < 0 || kind >= gft::K_NUM)
         gft::fail(GFT_ERR_INVALID_ARG, "serialized plan: bad tuning record");
@@ -585,36 +603,38 @@ gft_status gft_filter_tune(gft_filter f, gft_dtype dtype, uint32_t flags, const 
   });
 }
 
-gft_status gft_plan_tuning_get(gft_plan plan, gft_dtype dtype, int32_t kind, int32_t* cfg4) {
+gft_status gft_plan_tuning_get(gft_plan plan, gft_dtype dtype, int32_t kind, int32_t* rec5) {
   return guard([&] {
-    if (!cfg4) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
-    const gft::Kernel& k = kernel_of(plan, kind, dtype);
-    if (k.cfg.tc) {
-      for (int i = 0; i < 4; ++i) cfg4[i] = -1;
-      return;
-    }
-    cfg4[0] = k.cfg.R;
-    cfg4[1] = k.cfg.stages;
-    cfg4[2] = k.cfg.warps;
-    cfg4[3] = k.cfg.pace_ns;
+    if (!rec5) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
+    tuning_record(kernel_of(plan, kind, dtype), rec5);
   });
 }
 
-gft_status gft_plan_tuning_set(gft_plan plan, gft_dtype dtype, int32_t kind, const int32_t* cfg4) {
+gft_status gft_plan_tuning_set(gft_plan plan, gft_dtype dtype, int32_t kind, const int32_t* rec5) {
   return guard([&] {
-    if (!cfg4) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
+    if (!rec5) gft::fail(GFT_ERR_INVALID_ARG, "NULL argument");
     gft::Kernel& cur = kernel_of(plan, kind, dtype);
-    if (cur.cfg.tc) gft::fail(GFT_ERR_UNSUPPORTED, "tensor-core kernel: no FMA-skeleton geometry to set");
-    const int R = cfg4[0], S = cfg4[1], W = cfg4[2], pace = cfg4[3];
-    if (!(R == 1 || R == 2 || R == 4 || R == 8) || S < 2 || S > 8 || W < 1 || W > 16 || pace < 0 ||
-        pace > 100000)
-      gft::fail(GFT_ERR_INVALID_ARG, "tuning: R in {1,2,4,8}, stages 2..8, warps 1..16, pace 0..100000 ns");
-    const gft::CfgOverride ov{R, S, W, pace};
+    gft::CfgOverride ov;
+    if (cur.cfg.tc) {
+      if (rec5[4] < 0 || rec5[4] > 3)
+        gft::fail(GFT_ERR_INVALID_ARG, "tuning: tensor-core kernel, tc_variant must be 0..3");
+      ov.tc_variant = rec5[4];
+    } else {
+      const int R = rec5[0], S = rec5[1], W = rec5[2], pace = rec5[3];
+      if (!(R == 1 || R == 2 || R == 4 || R == 8) || S < 2 || S > 8 || W < 1 || W > 16 || pace < 0 ||
+          pace > 100000 || rec5[4] != -1)
+        gft::fail(GFT_ERR_INVALID_ARG,
+                  "tuning: R in {1,2,4,8}, stages 2..8, warps 1..16, pace 0..100000 ns, tc_variant -1");
+      ov = gft::CfgOverride{R, S, W, pace, -1};
+    }
     std::unique_ptr<gft::Kernel> k(new gft::Kernel);
     gft::generate_kernel(plan->P, kind, dtype, *k, !(plan->flags & GFT_FLAG_NO_TENSOR_CORES),
                          (plan->flags & GFT_FLAG_DENSE_TC) != 0, &ov);
-    if (k->cfg.tc || k->cfg.R != R || k->cfg.stages != S || k->cfg.warps != W)
-      gft::fail(GFT_ERR_INVALID_ARG, "tuning: geometry not realisable for this kernel (tile / shared-memory limits)");
+    int32_t got[5];
+    tuning_record(*k, got);
+    if ((bool)k->cfg.tc != (bool)cur.cfg.tc || (cur.cfg.tc ? got[4] != rec5[4]
+                                                         : (got[0] != rec5[0] || got[1] != rec5[1] || got[2] != rec5[2])))
+      gft::fail(GFT_ERR_INVALID_ARG, "tuning: not realisable for this kernel (variant / tile / shared-memory limits)");
     if (k->name == cur.name) return;
     gft::unload_kernel(cur);
     plan->k[dtype][kind] = std::move(k);

@@ -298,15 +298,16 @@ def gft_filter_tune(f, dtype, X, Y, batch, reps=0, stream=None, flags=0):
 
 
 def gft_plan_tuning_get(h, dtype, kind):
-    """(R, stages, warps, pace_ns) of the kernel, or None for a tensor-core kernel."""
-    out = (ctypes.c_int32 * 4)()
+    """(R, stages, warps, pace_ns, tc_variant) of the kernel (see include/gft.h)."""
+    out = (ctypes.c_int32 * 5)()
     _check(lib().gft_plan_tuning_get(h, _dtype_code(dtype), int(kind), out))
-    return tuple(out) if out[0] >= 0 else None
+    return tuple(out)
 
 
-def gft_plan_tuning_set(h, dtype, kind, cfg4):
-    arr = (ctypes.c_int32 * 4)(*[int(v) for v in cfg4])
-    _check(lib().gft_plan_tuning_set(h, _dtype_code(dtype), int(kind), arr))
+def gft_plan_tuning_set(h, dtype, kind, rec):
+    """rec: (R, stages, warps, pace_ns[, tc_variant]) -- a 4-tuple means tc_variant -1."""
+    vals = [int(v) for v in rec] + ([-1] if len(rec) == 4 else [])
+    _check(lib().gft_plan_tuning_set(h, _dtype_code(dtype), int(kind), (ctypes.c_int32 * 5)(*vals)))
 
 
 def gft_plan_info_get(h):
@@ -591,14 +592,13 @@ class Plan:
                              GFT_TUNE_GEOMETRY if geometry else 0)
 
     def tuning(self, dtype="f32", kinds=(0, 1, 2, 3)):
-        """Tuning record {kind: (R, stages, warps, pace_ns)} of the FMA-skeleton kernels."""
-        rec = {k: gft_plan_tuning_get(self._h, dtype, k) for k in kinds}
-        return {k: v for k, v in rec.items() if v is not None}
+        """Tuning records {kind: (R, stages, warps, pace_ns, tc_variant)}."""
+        return {k: gft_plan_tuning_get(self._h, dtype, k) for k in kinds}
 
     def set_tuning(self, record, dtype="f32"):
-        """Re-apply a record from tuning() (e.g. after Plan.load), without re-measuring."""
-        for k, cfg4 in record.items():
-            gft_plan_tuning_set(self._h, dtype, int(k), cfg4)
+        """Re-apply records from tuning() (4-tuples: FMA geometry with tc_variant -1)."""
+        for k, rec in record.items():
+            gft_plan_tuning_set(self._h, dtype, int(k), rec)
 
     def info(self):
         return gft_plan_info_get(self._h).as_dict()

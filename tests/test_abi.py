@@ -155,13 +155,13 @@ def test_tuning_record_get_set_on_cpu():
     cfg = workloads.config("cfg3")
     p = G.Plan.from_config(cfg, dtypes=("f32",))
     rec = p.tuning("f32", kinds=(0, 1))
-    assert rec[0] == (3, 3, 4, 400)          # tuning.tsv: fma 25 f32 3 3 4 pace=400
+    assert rec[0] == (3, 3, 4, 400, -1)      # tuning.tsv: fma 25 f32 3 3 4 pace=400
     name0 = p.kernel_name(0, "f32")
     p.set_tuning({0: (2, 2, 8, 150)}, "f32")
     src = p.kernel_source(0, "f32")
     for line in ("#define GFT_R 2", "#define GFT_STAGES 2", "#define GFT_WARPS 8", "#define GFT_PACE_NS 150"):
         assert line in src
-    assert p.kernel_name(0, "f32") != name0 and p.tuning("f32", (0,))[0] == (2, 2, 8, 150)
+    assert p.kernel_name(0, "f32") != name0 and p.tuning("f32", (0,))[0] == (2, 2, 8, 150, -1)
     p.set_tuning({0: (2, 2, 8, 0)}, "f32")
     assert "#define GFT_PACE_NS" not in p.kernel_source(0, "f32")
     # wisdom round trip: plan bytes + record -> identical kernel
@@ -184,12 +184,21 @@ def test_tuning_record_get_set_on_cpu():
         with pytest.raises(G.GFTError) as ei:
             p.set_tuning({0: bad}, "f32")
         assert ei.value.name == "GFT_ERR_INVALID_ARG"
-    # tensor-core kernels have no FMA-skeleton record
+    for bad in ((2, 2, 8, 0, 1),):                         # FMA kernel with a tc_variant
+        with pytest.raises(G.GFTError) as ei:
+            p.set_tuning({0: bad}, "f32")
+        assert ei.value.name == "GFT_ERR_INVALID_ARG"
+    # tensor-core kernels: the record is the tcgen05 variant; it round-trips through the bytes
     t = G.Plan.from_config(workloads.config("cfg5b"), dtypes=("f32",))
-    assert 0 not in t.tuning("f32", (0,))
-    with pytest.raises(G.GFTError) as ei:
-        t.set_tuning({0: (1, 2, 4, 0)}, "f32")
-    assert ei.value.name == "GFT_ERR_UNSUPPORTED"
+    assert t.tuning("f32", (0,))[0] == (-1, -1, -1, -1, 0)          # plain CTA pair (n = 128)
+    t.set_tuning({0: (-1, -1, -1, -1, 3)}, "f32")                    # single CTA
+    assert "fwdtc_" in t.kernel_name(0, "f32") and t.tuning("f32", (0,))[0][4] == 3
+    u = G.Plan.load(t.save(), dtypes=("f32",))
+    assert u.kernel_name(0, "f32") == t.kernel_name(0, "f32")
+    for bad in ((1, 2, 4, 0), (-1, -1, -1, -1, 7)):
+        with pytest.raises(G.GFTError) as ei:
+            t.set_tuning({0: bad}, "f32")
+        assert ei.value.name == "GFT_ERR_INVALID_ARG"
 
 
 def test_tuning_table_kind_and_work_keys():
