@@ -33,7 +33,8 @@ ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
 SKELETONS = {"kernel_skeleton.cuh": "skeleton_inc.h", "kernel_tc_skeleton.cuh": "skeleton_tc_inc.h",
-             "kernel_tc2_skeleton.cuh": "skeleton_tc2_inc.h", "kernel_tc3_skeleton.cuh": "skeleton_tc3_inc.h"}
+             "kernel_tc2_skeleton.cuh": "skeleton_tc2_inc.h", "kernel_tc3_skeleton.cuh": "skeleton_tc3_inc.h",
+             "kernel_dense_skeleton.cuh": "skeleton_dense_inc.h"}
 
 
 def _write_skeleton_inc():
@@ -180,6 +181,29 @@ def build_aot_cubins(jobs=8, verbose=True):
     return sorted(todo)
 
 
+PEAKS_LIB = os.path.join(LIBDIR, "libgftpeaks.so")
+
+
+def build_peaks(verbose=True):
+    """csrc/peaks.cu -> _lib/libgftpeaks.so: the same-run FFMA / DFMA / tcgen05-TF32 peak
+    microbenchmarks bench.py divides by (a measurement tool, not the GFT product path)."""
+    src = os.path.join(CSRC, "peaks.cu")
+    with open(src, "rb") as f:
+        stamp = hashlib.sha256(f.read()).hexdigest()
+    sf = PEAKS_LIB + ".stamp"
+    if os.path.exists(PEAKS_LIB) and os.path.exists(sf) and open(sf).read() == stamp:
+        return PEAKS_LIB
+    nvcc = os.path.join(CUDA_HOME, "bin", "nvcc")
+    cmd = [nvcc, "-shared", "-Xcompiler", "-fPIC", ARCH, "-lineinfo", "-O3", "-o", PEAKS_LIB + ".tmp", src]
+    subprocess.check_call(cmd)
+    os.replace(PEAKS_LIB + ".tmp", PEAKS_LIB)
+    with open(sf, "w") as f:
+        f.write(stamp)
+    if verbose:
+        print("built", PEAKS_LIB)
+    return PEAKS_LIB
+
+
 def build_c_example(verbose=True):
     """examples/gft_example.c: a plain-C consumer of the C ABI (libgft + CUDA runtime)."""
     exe = os.path.join(LIBDIR, "gft_example")
@@ -200,6 +224,7 @@ def main(argv=None):
     a = ap.parse_args(argv)
     build_library(force=a.force)
     build_c_example()
+    build_peaks()
     if not a.no_aot:
         build_aot_cubins()
 

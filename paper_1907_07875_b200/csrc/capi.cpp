@@ -191,6 +191,11 @@ gft_status gft_plan_deserialize(gft_plan* out, const void* buf, size_t size, con
       if (dt < 0 || dt > 1 || kind < 0 || kind >= gft::K_NUM)
         gft::fail(GFT_ERR_INVALID_ARG, "serialized plan: bad tuning record");
       if (!plan->k[dt][kind]) continue;   // dtype not prepared in this process
+      // a record applies only to the kernel family it was measured on: the load-time flags
+      // (e.g. GFT_FLAG_NO_TENSOR_CORES) may regenerate a different family -- skip it then
+      const gft::KernelCfg& kc = plan->k[dt][kind]->cfg;
+      const bool rec_tc = recs[i + 2] == -1;
+      if (kc.dgemm || rec_tc != (bool)kc.tc) continue;
       const gft_status st = gft_plan_tuning_set(plan, (gft_dtype)dt, kind, &recs[i + 2]);
       if (st != GFT_OK) gft::fail(st, std::string("serialized plan: tuning record: ") + gft_last_error());
     }
@@ -443,10 +448,18 @@ gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask)
 
 namespace {
 // one tuning candidate: an FMA-skeleton kernel regenerated with geometry / pacing overrides
+// (or a tcgen05 variant); its loaded modules are released when it goes out of scope unless
+// it was moved into the plan
 struct TuneCand {
   gft::CfgOverride ov;
   std::unique_ptr<gft::Kernel> k;
   double ms = 1e30;
+  TuneCand() = default;
+  TuneCand(TuneCand&&) = default;
+  TuneCand& operator=(TuneCand&&) = default;
+  ~TuneCand() {
+    if (k) gft::unload_kernel(*k);
+  }
 };
 
 void compile_parallel(std::vector<TuneCand>& cs, bool cache) {
@@ -473,7 +486,15 @@ void tune_slot(const gft::Plan& P, std::unique_ptr<gft::Kernel>& slot, int kind,
                int reps, gft_stream stream, int32_t* out4) {
   static const int kPace[] = {0, 150, 300, 450};
   gft::Kernel& cur = *slot;
-  const double t_cur = gft::time_kernel_ms(cur, X, Y, batch, stream, 2, reps, cache);
+  if (cur.cfg.dgemm) {   // the dense comparison GEMM has a fixed geometry
+    if (out4)
+      for (int i = 0; i < 4; ++i) out4[i] = -1;
+    return;
+  }
+  // the current kernel is timed in the same rounds as the candidates (min of two passes each),
+  // so timing noise does not bias the choice towards switching
+  double t_cur = 1e30;
+  auto time_cur = [&] { t_cur = std::min(t_cur, gft::time_kernel_ms(cur, X, Y, batch, stream, 2, reps, cache)); };
   if (cur.cfg.tc) {
     // tensor-core plan: measure the kernel variants (plain pair / two-warpgroup pair /
     // warp-specialised / single CTA) that apply, keep the fastest if > 1% better
@@ -489,17 +510,17 @@ void tune_slot(const gft::Plan& P, std::unique_ptr<gft::Kernel>& slot, int kind,
     }
     compile_parallel(cs, cache);
     TuneCand* b = nullptr;
-    for (int round = 0; round < 2; ++round)
+    for (int round = 0; round < 2; ++round) {
+      time_cur();
       for (auto& c : cs) {
         c.ms = std::min(c.ms, gft::time_kernel_ms(*c.k, X, Y, batch, stream, 2, reps, cache));
         if (round == 1 && (!b || c.ms < b->ms)) b = &c;
       }
+    }
     if (b && b->ms < 0.99 * t_cur) {
       gft::unload_kernel(cur);
       slot = std::move(b->k);
     }
-    for (auto& c : cs)
-      if (c.k) gft::unload_kernel(*c.k);
     return;
   }
   std::set<std::string> seen{cur.name};
@@ -516,9 +537,11 @@ void tune_slot(const gft::Plan& P, std::unique_ptr<gft::Kernel>& slot, int kind,
       cs.push_back(std::move(c));
     }
     compile_parallel(cs, cache);
-    for (int round = 0; round < 2; ++round)
+    for (int round = 0; round < 2; ++round) {
+      time_cur();
       for (auto& c : cs)
         c.ms = std::min(c.ms, gft::time_kernel_ms(*c.k, X, Y, batch, stream, 2, reps, cache));
+    }
     for (auto& c : cs) pool.push_back(std::move(c));
   };
   auto best_of_pool = [&]() -> TuneCand* {
@@ -550,8 +573,6 @@ void tune_slot(const gft::Plan& P, std::unique_ptr<gft::Kernel>& slot, int kind,
     gft::unload_kernel(cur);
     slot = std::move(b->k);
   }
-  for (auto& c : pool)
-    if (c.k) gft::unload_kernel(*c.k);
   if (out4) {
     out4[0] = slot->cfg.R;
     out4[1] = slot->cfg.stages;

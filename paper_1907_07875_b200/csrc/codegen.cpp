@@ -32,6 +32,9 @@ static const char* kSkeletonTC2 =
 static const char* kSkeletonTC3 =
 #include "skeleton_tc3_inc.h"
     ;
+static const char* kSkeletonDense =
+#include "skeleton_dense_inc.h"
+    ;
 
 KernelCfg choose_cfg(int n, int dtype, int64_t work, const CfgOverride* ov, int kind) {
   KernelCfg c;
@@ -729,6 +732,73 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
   o << "}\n";
 }
 
+// Dense comparison kernel Y = X W (H7) as a register-tiled GEMM with W in SMEM
+// (kernel_dense_skeleton.cuh), for n = 64 / 128 when a tile ring of >= 2 buffers fits beside
+// W.  Thread tile GFT_TM x 8 (TM = 8 fp32, 4 fp64), 256 compute threads: GFT_BM = 256 TM 8 / n.
+bool dense_gemm_geometry(int n, int dtype, KernelCfg& c) {
+  if (n != 64 && n != 128) return false;
+  if (const char* e = getenv("GFT_NO_DENSE_GEMM")) if (e[0] == '1') return false;   // ablation
+  auto env_int = [](const char* k, int v) { const char* e = getenv(k); return (e && *e) ? atoi(e) : v; };
+  const int elem = dtype == GFT_F64 ? 8 : 4;
+  const int tm = env_int("GFT_DG_TM", dtype == GFT_F64 ? 4 : 8), tn = env_int("GFT_DG_TN", 8);
+  const int threads = env_int("GFT_DG_THREADS", 256);
+  if (tm < 1 || tn < 16 / elem || tn % (16 / elem) || n % tn || (threads != 128 && threads != 256)) return false;
+  const int bm = threads * tm * tn / n;
+  if (bm > 256 || bm % 8 || (bm / tm) < 8 || (bm / tm) * (n / tn) != threads) return false;
+  KernelCfg g;
+  g.n = n;
+  g.elem = elem;
+  g.dgemm = 1;
+  g.bm = bm;
+  g.R = tm;       // thread tile rows
+  g.pack = tn;    // thread tile columns
+  g.warps = threads / 32;
+  g.mode = 0;
+  g.boxc = 128 / elem;
+  g.swz_mask = 7;
+  g.vec = 16 / elem;
+  for (g.stages = 4; g.stages >= 2 && g.smem_bytes() > 227 * 1024; --g.stages) {}
+  if (g.stages < 2) return false;
+  c = g;
+  return true;
+}
+
+void generate_dense_gemm(const Plan& P, int kind, int dtype, Kernel& k) {
+  const KernelCfg& c = k.cfg;
+  const int n = P.n;
+  std::ostringstream gen;
+  gen << "__device__ __align__(16) const elem_t gft_W[" << n * n << "] = {\n";
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      // forward y_j = sum_i x_i U[i][j]; inverse x_j = sum_i y_i U[j][i]
+      const double v = kind == K_DENSE_FWD ? P.U[(size_t)i * n + j] : P.U[(size_t)j * n + i];
+      char buf[48];
+      if (dtype == GFT_F64) std::snprintf(buf, sizeof buf, "%a,", v);
+      else std::snprintf(buf, sizeof buf, "%af,", (double)(float)v);
+      gen << buf << ((j % 8 == 7) ? "\n" : "");
+    }
+  gen << "};\n";
+  std::ostringstream pre;
+  pre << "#define GFT_ELEM " << (dtype == GFT_F64 ? "double" : "float") << "\n";
+  if (dtype == GFT_F64) pre << "#define GFT_ELEM_IS_DOUBLE 1\n";
+  pre << "#define GFT_N " << n << "\n#define GFT_BM " << c.bm << "\n#define GFT_TM " << c.R << "\n#define GFT_TN " << c.pack
+      << "\n#define GFT_THREADS " << 32 * c.warps << "\n#define GFT_STAGES " << c.stages << "\n";
+  if (const char* e = getenv("GFT_DG_PREFETCH")) pre << "#define GFT_DG_PREFETCH " << atoi(e) << "\n";   // experiment
+  const std::string skel(kSkeletonDense);
+  const std::string marker = "// @@GFT_GENERATED@@";
+  const size_t at = skel.find(marker);
+  if (at == std::string::npos) fail(GFT_ERR_COMPILE, "dense skeleton marker missing");
+  const std::string key = pre.str() + gen.str() + skel;
+  char hbuf[32];
+  std::snprintf(hbuf, sizeof hbuf, "%016llx", (unsigned long long)fnv1a(key));
+  k.name = std::string("gft_") + (kind == K_DENSE_FWD ? "dgfwd" : "dginv") + "_" + (dtype == GFT_F64 ? "f64" : "f32") +
+           "_n" + std::to_string(n) + "_" + hbuf;
+  std::ostringstream src;
+  src << "// generated by paper_1907_07875_b200 codegen.cpp — dense comparison GEMM (W in SMEM)\n"
+      << pre.str() << "#define GFT_KNAME " << k.name << "\n" << skel.substr(0, at) << gen.str() << skel.substr(at);
+  k.source = src.str();
+}
+
 }  // namespace
 
 void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_tc, bool dense_tc,
@@ -757,6 +827,10 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
   }
   k.kind = kind;
   k.dtype = dtype;
+  if ((kind == K_DENSE_FWD || kind == K_DENSE_INV) && dense_gemm_geometry(P.n, dtype, k.cfg)) {
+    generate_dense_gemm(P, kind, dtype, k);
+    return;
+  }
   k.cfg = choose_cfg(P.n, dtype, (kind == K_DENSE_FWD || kind == K_DENSE_INV) ? (int64_t)P.n * P.n : P.sum_k2,
                      ov, kind);
   static const char* kKindNameTC[] = {"fwdtc", "invtc", "", "", "filttc"};

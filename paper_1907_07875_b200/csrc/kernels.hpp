@@ -33,12 +33,19 @@ struct KernelCfg {
   int tc_wgs = 1;               // compute warpgroups of the CTA-pair kernel (1 or 2)
   int tc_ws = 0;                // warp-specialised pair kernel (kernel_tc3_skeleton.cuh, 384 threads)
   int tc_io_split = 0;          // ... with separate input ring and one output buffer
-  int tile_rows() const { return tc ? 128 : 32 * R; }
+  // dense comparison GEMM (kernel_dense_skeleton.cuh): tiles of `bm` rows, 32*warps compute
+  // threads + 1 TMA warp, thread tile R x pack outputs, W = U or U^T resident in SMEM
+  int dgemm = 0;
+  int bm = 0;
+  int tile_rows() const { return dgemm ? bm : tc ? 128 : 32 * R; }
   // tensor-core tiles pad each row to whole 32-float TMA boxes (kernel_tc*_skeleton.cuh)
   int tile_bytes() const { return tile_rows() * (tc ? (n + 31) / 32 * 32 : n) * elem; }
-  int threads() const { return tc ? (tc_ws ? 384 : tc_pair ? 32 * (4 * tc_wgs + 2) : 160) : warps * 32; }
-  int tiles_per_cta() const { return tc ? 1 : warps; }   // tiles processed concurrently per CTA
+  int threads() const {
+    return dgemm ? 32 * warps + 32 : tc ? (tc_ws ? 384 : tc_pair ? 32 * (4 * tc_wgs + 2) : 160) : warps * 32;
+  }
+  int tiles_per_cta() const { return (tc || dgemm) ? 1 : warps; }   // tiles processed concurrently per CTA
   int smem_bytes() const {
+    if (dgemm) return stages * tile_bytes() + n * n * elem + 2 * stages * 8 + 1024;
     if (tc) return (stages + tc_io_split) * tile_bytes() + tc_b_bytes + (3 * stages + 24) * 8 + 16 + 1024;
     return warps * stages * tile_bytes() + warps * stages * 8 + 1024;
   }

@@ -198,6 +198,17 @@ Plan deserialize_plan(const uint8_t* buf, size_t size, size_t* consumed) {
     P.leaves.push_back(std::move(lf));
   }
   if (covered != n) fail(GFT_ERR_INVALID_ARG, "serialized plan: leaves do not cover the positions");
+  // every position is read by exactly one leaf and every coefficient slot written by exactly
+  // one: the sizes summing to n is not enough (a duplicate would compile into a kernel that
+  // reads one position twice and leaves another coefficient unwritten)
+  {
+    std::vector<char> seen_pos(n, 0), seen_slot(n, 0);
+    for (const Leaf& lf : P.leaves)
+      for (int i = 0; i < lf.k; ++i) {
+        if (seen_pos[lf.pos[i]]++) fail(GFT_ERR_INVALID_ARG, "serialized plan: position read by two leaves");
+        if (seen_slot[lf.slot[i]]++) fail(GFT_ERR_INVALID_ARG, "serialized plan: coefficient slot written twice");
+      }
+  }
   for (const Leaf& lf : P.leaves)
     for (int v : lf.pair)
       if (v < -1 || v >= lf.k) fail(GFT_ERR_INVALID_ARG, "serialized plan: bad right-stage pair index");

@@ -22,4 +22,5 @@ def test_reference_arm_json_line():
     assert d["value"] > 0 and d["unit"] == "signals/s"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
-    assert d["config"]["workload"].startswith("cfg2:")
+    assert d["config"]["workload"].startswith("cfg5 mixed")
+    assert len(lines[0].encode()) <= 2048

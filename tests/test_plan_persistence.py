@@ -76,3 +76,79 @@ def test_loaded_plan_bit_identical_on_gpu(name):
     Yp, Yq = p.forward(X), q.forward(X)
     assert torch.equal(Yp, Yq)
     assert torch.equal(p.inverse(Yp), q.inverse(Yq))
+
+
+def _leaf_arrays(data):
+    """Offsets of every leaf's pos / slot arrays in a serialised plan (format: serialize.cpp)."""
+    import struct
+    off = 8 + 4 + 4                                  # magic, version, n
+    nops = struct.unpack_from("<Q", data, off)[0]
+    off += 8 + 20 * nops
+    nleaves = struct.unpack_from("<Q", data, off)[0]
+    off += 8
+    out = []
+    for _ in range(nleaves):
+        k = struct.unpack_from("<i", data, off)[0]
+        off += 4
+        pos_off = off + 8
+        off = pos_off + 4 * k
+        slot_off = off + 8
+        off = slot_off + 4 * k
+        out.append((k, pos_off, slot_off))
+        for elem in (8, 8, 8):                       # lam, V, M (f64 arrays)
+            c = struct.unpack_from("<Q", data, off)[0]
+            off += 8 + elem * c
+        off += 12                                    # level, right, side
+        c = struct.unpack_from("<Q", data, off)[0]   # pair
+        off += 8 + 4 * c
+        off += 4                                     # approx
+        nl = struct.unpack_from("<Q", data, off)[0]
+        off += 8
+        for _ in range(nl):
+            nr = struct.unpack_from("<Q", data, off)[0]
+            off += 8 + 24 * nr
+        c = struct.unpack_from("<Q", data, off)[0]   # perm
+        off += 8 + 4 * c
+        c = struct.unpack_from("<Q", data, off)[0]   # scale
+        off += 8 + 8 * c
+    return out
+
+
+@pytest.mark.parametrize("which", ["pos", "slot"])
+def test_duplicate_leaf_index_rejected(which):
+    """Leaf sizes summing to n is not enough: a position read by two leaves (or a coefficient
+    slot written twice) is rejected (serialize.cpp cover check)."""
+    p = G.Plan.from_config(workloads.config("cfg1"), max_depth=1, host_only=True)
+    data = bytearray(p.save())
+    (k0, p0, s0), (k1, p1, s1) = _leaf_arrays(bytes(data))[:2]
+    assert k0 == k1 == 4
+    G.Plan.load(bytes(data), host_only=True)         # the parse above is right: intact loads
+    src, dst = (p0, p1) if which == "pos" else (s0, s1)
+    data[dst:dst + 4] = data[src:src + 4]            # leaf 1's first index := leaf 0's first
+    with pytest.raises(G.GFTError) as e:
+        G.Plan.load(bytes(data), host_only=True)
+    assert e.value.name == "GFT_ERR_INVALID_ARG"
+    assert ("two leaves" if which == "pos" else "written twice") in G.gft_last_error()
+
+
+def test_tuning_trailer_of_other_kernel_family_is_skipped():
+    """A tuned plan loads whatever the load-time flags: a tcgen05-variant record is skipped
+    when the plan is regenerated without tensor cores, and an FMA-geometry record when it is
+    regenerated with them (capi.cpp deserialize)."""
+    cfg = workloads.config("cfg5b")
+    p = G.Plan.from_config(cfg, dtypes=("f32",))
+    rec = p.tuning("f32", kinds=(0,))[0]
+    assert rec[0] == -1 and rec[4] in (0, 1, 2, 3)          # cfg5b forward: a tcgen05 kernel
+    alt = 3 if rec[4] != 3 else 0
+    p.set_tuning({0: (-1, -1, -1, -1, alt)})
+    blob = p.save()
+    q = G.Plan.load(blob, dtypes=("f32",))
+    assert q.tuning("f32", kinds=(0,))[0][4] == alt
+    r = G.Plan.load(blob, dtypes=("f32",), no_tensor_cores=True)
+    assert r.tuning("f32", kinds=(0,))[0][4] == -1          # FMA kernel, record skipped
+    f = G.Plan.from_config(cfg, dtypes=("f32",), no_tensor_cores=True)
+    rf = f.tuning("f32", kinds=(0,))[0]
+    f.set_tuning({0: (rf[0], rf[1], rf[2], 150 if rf[3] != 150 else 300, -1)})
+    blob = f.save()
+    s = G.Plan.load(blob, dtypes=("f32",))  # tensor cores allowed again
+    assert s.tuning("f32", kinds=(0,))[0][4] in (0, 1, 2, 3)
