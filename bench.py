@@ -487,30 +487,6 @@ def main():
                 "event_bracketed_ms": round(per[dom], 5),
                 "tensor_frac": round(tc_flops / (dom_ms * 1e-3) / (peaks["tf32_tflops"] * 1e12), 4)}
 
-    # ---- sustained load: >= sustain_s seconds of back-to-back steps at the power cap ------
-    sustained = None
-    if args.sustain_s > 0:
-        chunk = max(1, int(200.0 / ms_step))   # ~0.2 s of steps per event pair
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        tot_ms, nsteps = 0.0, 0
-        s0 = time.perf_counter()
-        a.record(stream)
-        while tot_ms < args.sustain_s * 1e3:
-            for _ in range(chunk):
-                step()
-            nsteps += chunk
-            b.record(stream)
-            b.synchronize()
-            tot_ms = a.elapsed_time(b)
-        s1 = time.perf_counter()
-        sms = max_over_ranks(tot_ms / nsteps, device)
-        sc = sampler.summary(s0, s1)
-        sustained = {"seconds": round(tot_ms / 1e3, 2), "ms_per_step": round(sms, 5),
-                     "value": B * ws / (sms * 1e-3),
-                     "dominant_frac": round(nbytes[di] / (sms * share[dom] * 1e-3) / 1e9 / hbm, 4),
-                     "clocks": {k: sc[k] for k in ("sm_mhz", "reasons", "power_w")}}
-    sampler.stop()
-
     # ---- the in-run dense U^T x comparisons (same inputs, fwd + inv of both per step) ------
     def dense_step_ms(fwd, inv):
         def f():
@@ -542,6 +518,40 @@ def main():
     for p in dplans:
         p.close()
 
+    # ---- side tables (file only) ----------------------------------------------------------
+    if args.tables and rank == 0 and ws == 1:
+        tables = {"hbm_peak_gbs": hbm, "compute_peaks": peaks,
+                  "configs": config_table(args, stream, hbm, device, peaks),
+                  "right_haar": right_haar_table(args, stream, hbm, device)}
+        os.makedirs(os.path.dirname(os.path.abspath(args.tables)), exist_ok=True)
+        with open(args.tables, "w") as f:
+            json.dump(tables, f, indent=1)
+
+    # ---- sustained load: >= sustain_s seconds of back-to-back steps at the power cap (after
+    # the dense comparisons: a hot GPU sits at a capped clock for a while) ------------------
+    sustained = None
+    if args.sustain_s > 0:
+        chunk = max(1, int(200.0 / ms_step))   # ~0.2 s of steps per event pair
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot_ms, nsteps = 0.0, 0
+        s0 = time.perf_counter()
+        a.record(stream)
+        while tot_ms < args.sustain_s * 1e3:
+            for _ in range(chunk):
+                step()
+            nsteps += chunk
+            b.record(stream)
+            b.synchronize()
+            tot_ms = a.elapsed_time(b)
+        s1 = time.perf_counter()
+        sms = max_over_ranks(tot_ms / nsteps, device)
+        sc = sampler.summary(s0, s1)
+        sustained = {"seconds": round(tot_ms / 1e3, 2), "ms_per_step": round(sms, 5),
+                     "value": B * ws / (sms * 1e-3),
+                     "dominant_frac": round(nbytes[di] / (sms * share[dom] * 1e-3) / 1e9 / hbm, 4),
+                     "clocks": {k: sc[k] for k in ("sm_mhz", "reasons", "power_w")}}
+    sampler.stop()
+
     # ---- end to end through the C ABI with pinned HOST buffers (H2D + kernels + D2H timed) ---
     Xh = [x.pin_memory() for x in Xc]
     Yh = [torch.empty_like(x).pin_memory() for x in Xh]
@@ -571,15 +581,6 @@ def main():
            "d2h_bytes_per_step": step_bytes, "ms_per_step": round(e2e_ms, 4), "roundtrip_max_rel_err": rt_err,
            "pcie_bidir_each_gbs": pcie_roof(device),
            "achieved_each_dir_gbs": round(step_bytes / (e2e_ms * 1e6), 1)}
-
-    # ---- side tables (file only) ----------------------------------------------------------
-    if args.tables and rank == 0 and ws == 1:
-        tables = {"hbm_peak_gbs": hbm, "compute_peaks": peaks,
-                  "configs": config_table(args, stream, hbm, device, peaks),
-                  "right_haar": right_haar_table(args, stream, hbm, device)}
-        os.makedirs(os.path.dirname(os.path.abspath(args.tables)), exist_ok=True)
-        with open(args.tables, "w") as f:
-            json.dump(tables, f, indent=1)
 
     cpu = None
     if rank == 0:

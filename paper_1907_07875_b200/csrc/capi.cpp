@@ -105,8 +105,8 @@ namespace {
 constexpr char kTuneMagic[8] = {'G', 'F', 'T', 'T', 'U', 'N', 'E', '2'};
 
 // {R, stages, warps, pace_ns, tc_variant} of a kernel: the FMA-skeleton geometry (variant -1),
-// or -1s and the tcgen05 variant (0 plain pair, 1 two-warpgroup pair, 2 warp-specialised,
-// 3 single CTA; -1 for the opt-in IO-split kernel)
+// or -1s and the tcgen05 variant (0 plain pair, 1 two-warpgroup pair, 2 warp-specialised --
+// in place for n <= 64, IO-split above --, 3 single CTA)
 void tuning_record(const gft::Kernel& k, int32_t* r5) {
   if (!k.cfg.tc) {
     r5[0] = k.cfg.R;
@@ -117,7 +117,7 @@ void tuning_record(const gft::Kernel& k, int32_t* r5) {
     return;
   }
   r5[0] = r5[1] = r5[2] = r5[3] = -1;
-  r5[4] = !k.cfg.tc_pair ? 3 : k.cfg.tc_io_split ? -1 : k.cfg.tc_ws ? 2 : k.cfg.tc_wgs == 2 ? 1 : 0;
+  r5[4] = !k.cfg.tc_pair ? 3 : k.cfg.tc_ws ? 2 : k.cfg.tc_wgs == 2 ? 1 : 0;
 }
 
 std::vector<uint8_t> tuning_trailer(gft_plan plan) {

@@ -62,11 +62,10 @@ KernelCfg choose_cfg(int n, int dtype, int64_t work, const CfgOverride* ov, int 
       c.swz_mask = 7;
     }
   } else {
-    // unaligned row pitch: 1-D bulk copies of whole tiles.  Opt-in (GFT_SUPERROW=1): TMA
-    // tensor copies of the 4-signal super-row view (4n <= 256) -- parity-tested but 3% slower
-    // on cfg3 (5.79 vs 5.95 TB/s back to back, tools/gpu_superrow_cmp.sh)
-    c.mode = (4 * n <= 256 && getenv("GFT_SUPERROW") != nullptr) ? 2 : 1;
-    c.pack = c.mode == 2 ? 4 : 1;
+    // unaligned row pitch: 1-D bulk copies of whole tiles (TMA copies of a 4-signal super-row
+    // view were measured 3% slower on cfg3 in round 1 and removed)
+    c.mode = 1;
+    c.pack = 1;
     c.boxc = n;
     c.swz_mask = 0;
     // odd row pitch in vector units makes thread-per-row accesses conflict-free
@@ -406,6 +405,25 @@ void emit_tmem_ld(std::ostringstream& o, const std::string& arr, int col0, int c
   }
 }
 
+// hi/lo split of a 3xTF32 A operand (x = hi + lo exactly).  Default: hi = x with its 13 low
+// mantissa bits cleared (one LOP3; the tensor core reads only the TF32 bits of the container
+// anyway), lo = x - hi.  cvt.rna.tf32.f32 compiles to FSETP + IADD3 + SEL + LOP3 -- four ALU
+// instructions per element on the staging critical path; the truncated hi leaves |lo| <= 2^-10
+// |x| instead of 2^-11 (lo keeps 11 of its <= 13 bits: ~2^-21 |x| per element, well inside
+// the 1e-5 per-signal bound).  GFT_TC_SPLIT=rna restores the rounded split (ablation).
+std::string split_line(int i, const std::string& src) {
+  static const bool rna = [] {
+    const char* e = getenv("GFT_TC_SPLIT");
+    return e && std::strcmp(e, "rna") == 0;
+  }();
+  const std::string h = "h[" + std::to_string(i) + "]", l = "l[" + std::to_string(i) + "]";
+  if (rna)
+    return "  " + h + " = tf32_rna(" + src + "); " + l + " = __float_as_uint(" + src + " - __uint_as_float(" + h +
+           "));\n";
+  return "  " + h + " = __float_as_uint(" + src + ") & 0xffffe000u; " + l + " = __float_as_uint(" + src +
+         " - __uint_as_float(" + h + "));\n";
+}
+
 void emit_units(std::ostringstream& o, const Plan& P, const char* arr, bool reverse, int dtype) {
   o << "  { float a_, b_;\n";
   auto one = [&](const Op& op) {
@@ -487,8 +505,7 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, bool pair, 
       for (int c = c0; c < c0 + w; ++c) {
         if (c < t.k) {
           const int src = in_idx(lf, d, c);
-          o << "  h[" << c - c0 << "] = tf32_rna(x[" << src << "]); l[" << c - c0 << "] = __float_as_uint(x["
-            << src << "] - __uint_as_float(h[" << c - c0 << "]));\n";
+          o << split_line(c - c0, "x[" + std::to_string(src) + "]");
         } else {
           o << "  h[" << c - c0 << "] = 0u; l[" << c - c0 << "] = 0u;\n";
         }
@@ -585,16 +602,6 @@ void generate_tc(const Plan& P, Dir d, const std::vector<TcLeaf>& T, bool pair, 
 // stager (front butterflies, hi/lo -> TMEM A, small leaves -> SMEM row) and a drainer
 // (TMEM D -> registers, back / coefficient butterflies); D double-buffered in TMEM.
 // Returns false if the TMEM layout (A + 2 D) does not fit in 512 columns.
-// Opt-in (GFT_TC_WS_A2=1): A (the staged hi/lo operand) double-buffered in TMEM when it fits
-// beside the two D buffers -- the stager of tile t+1 then waits for MMA(t-1), not MMA(t).
-// Measured back to back at n = 64 (tools/gpu_ws_a2_cmp.sh): +1.5-2% with one 64-leaf, -3%
-// with two 32-leaves, a tie on G_z -- staging is not what bounds these kernels, so one A
-// buffer stays the default.
-int ws_a_bufs(int a_cols, int d_cols) {
-  if (getenv("GFT_TC_WS_A2") == nullptr) return 1;
-  return 2 * a_cols + 2 * d_cols <= 512 ? 2 : 1;
-}
-
 bool ws_layout(std::vector<TcLeaf>& T, int& a_cols, int& d_cols, int& tmem_cols) {
   a_cols = d_cols = 0;
   for (auto& t : T) {
@@ -608,7 +615,7 @@ bool ws_layout(std::vector<TcLeaf>& T, int& a_cols, int& d_cols, int& tmem_cols)
   }
   if (a_cols + 2 * d_cols > 512) return false;
   tmem_cols = 32;
-  while (tmem_cols < ws_a_bufs(a_cols, d_cols) * a_cols + 2 * d_cols) tmem_cols *= 2;
+  while (tmem_cols < a_cols + 2 * d_cols) tmem_cols *= 2;
   return true;
 }
 
@@ -634,9 +641,10 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
             }
     }
   const size_t per_cta = B.size() / 2;
-  const int abufs = ws_a_bufs(a_cols, d_cols);
-  o << "#define GFT_B_FLOATS " << per_cta << "\n#define GFT_A_COLS " << a_cols << "\n#define GFT_A_BUFS " << abufs
-    << "\n#define GFT_D_BASE " << abufs * a_cols << "\n#define GFT_D_COLS " << d_cols << "\n#define GFT_SMALL "
+  int nch = 0;   // 32-column A chunks over all tensor-core leaves (staged / released one by one)
+  for (const TcLeaf& t : T) nch += (t.kp8 + 31) / 32;
+  o << "#define GFT_B_FLOATS " << per_cta << "\n#define GFT_A_COLS " << a_cols << "\n#define GFT_NCH " << nch
+    << "\n#define GFT_D_BASE " << a_cols << "\n#define GFT_D_COLS " << d_cols << "\n#define GFT_SMALL "
     << (T.size() < P.leaves.size() ? 1 : 0) << "\n";
   o << "__device__ __align__(16) const float gft_tcB[2][" << per_cta << "] = {\n";
   for (size_t i = 0; i < B.size(); ++i) {
@@ -649,23 +657,24 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
        "  *reinterpret_cast<float*>(buf + tile_off(row, col)) = v;\n}\n"
        "static __device__ __forceinline__ float ld_elem(const unsigned char* buf, int row, int col) {\n"
        "  return *reinterpret_cast<const float*>(buf + tile_off(row, col));\n}\n";
-  // ---- stager ----
+  // ---- stager: per 32-column A chunk c, wait until the MMAs of the previous tile on it are
+  // done (a_free[c]), write hi/lo, signal staged[c] on the leader ----
   o << "static __device__ __forceinline__ void gft_stage(float (&x)[GFT_N], u32 tm, u32 staged0,\n"
-       "    unsigned char* buf, int row, u32 abar, u32 apar, bool await_a) {\n";
+       "    unsigned char* buf, int row, u32 afree, u32 apar, bool await_a) {\n";
   if (d != DIR_INV) emit_units(o, P, "x", false, dtype);
   if (d == DIR_FILTER && !P.post.empty()) fail(GFT_ERR_COMPILE, "filter plan with right Haar stages");
   if (d == DIR_INV) emit_post_units(o, P, "x", true, "float");
-  o << "  if (await_a) { mbar_wait(abar, apar); tc_fence_after(); }   // the MMAs that last read this A buffer are done\n";
+  int ch = 0;
   for (const TcLeaf& t : T) {
     const Leaf& lf = P.leaves[t.leaf];
-    for (int c0 = 0; c0 < t.kp8; c0 += 32) {
+    for (int c0 = 0; c0 < t.kp8; c0 += 32, ++ch) {
       const int w = std::min(32, t.kp8 - c0);
+      o << "  if (await_a) { mbar_wait(afree + " << 8 * ch << "u, apar); tc_fence_after(); }\n";
       o << "  { u32 h[" << w << "], l[" << w << "];\n";
       for (int c = c0; c < c0 + w; ++c) {
         if (c < t.k) {
           const int src = in_idx(lf, d, c);
-          o << "  h[" << c - c0 << "] = tf32_rna(x[" << src << "]); l[" << c - c0 << "] = __float_as_uint(x["
-            << src << "] - __uint_as_float(h[" << c - c0 << "]));\n";
+          o << split_line(c - c0, "x[" + std::to_string(src) + "]");
         } else {
           o << "  h[" << c - c0 << "] = 0u; l[" << c - c0 << "] = 0u;\n";
         }
@@ -673,9 +682,9 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
       emit_tmem_st(o, "h", t.hi_col + c0, w);
       emit_tmem_st(o, "l", t.lo_col + c0, w);
       o << "  }\n";
+      o << "  signal_staged(staged0 + " << 8 * ch << "u);\n";
     }
   }
-  o << "  signal_staged(staged0);\n";
   if (T.size() < P.leaves.size()) {
     o << "  { float y[GFT_N];\n";
     for (size_t l = 0; l < P.leaves.size(); ++l)
@@ -713,20 +722,26 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
   if (d == DIR_FWD) emit_post_units(o, P, "y", false, "float");
   if (d != DIR_FWD) emit_units(o, P, "y", true, dtype);
   o << "}\n";
-  // ---- issuer ----
-  o << "static __device__ __forceinline__ void gft_issue_ws(u32 tA, u32 tD, u32 bsm) {\n";
+  // ---- issuer: chunk by chunk (all three passes of the chunk's k-steps), each chunk's MMAs
+  // committed to a_free[c] so the stager can refill it ----
+  o << "static __device__ __forceinline__ void gft_issue_ws(u32 tA, u32 tD, u32 bsm, u32 staged, u32 spar, u32 afree) {\n";
+  ch = 0;
   for (const TcLeaf& t : T) {
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(t.np >> 3) << 17) | (16u << 24);
-    const int ksteps = t.kp8 / 8;
     const int atom_bytes = (t.np / 2) * 128;
-    for (int pass = 0; pass < 3; ++pass) {
-      const int acol = pass == 2 ? t.lo_col : t.hi_col;
-      const int boff = pass == 1 ? t.blo_off : t.bhi_off;
-      for (int j = 0; j < ksteps; ++j) {
-        const int bo = boff + (j / 4) * atom_bytes + (j % 4) * 32;
-        o << "  mma_ts2(tD + " << t.d_col << "u, tA + " << (acol + 8 * j) << "u, smem_desc_sw128(bsm + " << bo
-          << "u), " << idesc << "u, " << ((pass == 0 && j == 0) ? 0 : 1) << "u);\n";
+    for (int c0 = 0; c0 < t.kp8; c0 += 32, ++ch) {
+      const int w = std::min(32, t.kp8 - c0);
+      o << "  mbar_wait_acq_cluster(staged + " << 8 * ch << "u, spar); tc_fence_after();\n";
+      for (int pass = 0; pass < 3; ++pass) {
+        const int acol = pass == 2 ? t.lo_col : t.hi_col;
+        const int boff = pass == 1 ? t.blo_off : t.bhi_off;
+        for (int j = c0 / 8; j < (c0 + w) / 8; ++j) {
+          const int bo = boff + (j / 4) * atom_bytes + (j % 4) * 32;
+          o << "  mma_ts2(tD + " << t.d_col << "u, tA + " << (acol + 8 * j) << "u, smem_desc_sw128(bsm + " << bo
+            << "u), " << idesc << "u, " << ((pass == 0 && j == 0) ? 0 : 1) << "u);\n";
+        }
       }
+      o << "  tc_commit_pair(afree + " << 8 * ch << "u);\n";
     }
   }
   o << "}\n";
@@ -903,13 +918,15 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
         }
       }
     }
-    // experiment (opt-in, GFT_TC_IOSPLIT=1): for n > 64 split input / output buffers -- 2
-    // input buffers released by the stager right after reading its rows, one output buffer
-    // drained by a storer warp (plans without CUDA-core leaves).  Faster than the pair kernel
-    // in isolation under ncu (cfg5b 183 vs 188 us) but 9% slower back to back (5.55 vs 6.08
-    // TB/s, with or without PDL; tools/gpu_iosplit_cmp.sh, gpu_pdl_ws.sh), so not the default.
+    // n > 64 (tiles too big for four in-place buffers): the IO-split warp-specialised kernel --
+    // two input buffers released by the stager right after reading its rows, one output buffer
+    // written and stored box by box (plans without CUDA-core leaves).  With load pacing and
+    // per-chunk A release it beats the plain pair kernel in a burst (cfg5b forward 6.30 vs
+    // 6.13 TB/s) and under sustained load (6.00 vs 5.25 TB/s at the power-capped clock,
+    // tools/r02/gpu_tc_probe7.sh).  GFT_TC_IOSPLIT=0 keeps the plain pair kernel (ablation).
     bool io_split = false;
-    if (ok && pair && !ws && P.n > 64 && T.size() == P.leaves.size() && getenv("GFT_TC_IOSPLIT") != nullptr) {
+    const char* eio = getenv("GFT_TC_IOSPLIT");
+    if (ok && pair && !ws && !no_ws && P.n > 64 && T.size() == P.leaves.size() && !(eio && eio[0] == '0')) {
       Tws = T;
       if (ws_layout(Tws, ws_a, ws_d, ws_tmem)) {
         const int tile = 128 * ((P.n + 31) / 32 * 32) * 4;
@@ -945,6 +962,15 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
           << tmem_cols << "\n";
       if (wgs == 2) pre << "#define GFT_WGS 2\n#define GFT_WG_COLS " << wg_cols << "\n";
       if (io_split) pre << "#define GFT_IO_SPLIT 1\n";
+      if (const char* e = getenv("GFT_TC_TRACE")) if (e[0] == '1') pre << "#define GFT_TRACE 1\n";   // experiments
+      if (ws) {
+        // load pacing (kernel_tc3_skeleton.cuh pace_load): 0.9 x the CTA's fair share of HBM
+        // time per tile (read + write of its 128 rows at 6455 GB/s over 148 SMs, the measured
+        // copy roof); GFT_TC_LOAD_PACE_NS overrides (0 disables)
+        int pace = (int)(0.9 * 2.0 * c.tile_bytes() / (6455.0 / 148.0));
+        if (const char* lp = getenv("GFT_TC_LOAD_PACE_NS")) pace = atoi(lp);
+        if (pace > 0) pre << "#define GFT_LOAD_PACE_NS " << pace << "\n";
+      }
       const std::string skel(ws ? kSkeletonTC3 : pair ? kSkeletonTC2 : kSkeletonTC);
       const std::string marker = "// @@GFT_GENERATED@@";
       const size_t at = skel.find(marker);

@@ -15,14 +15,15 @@
 //                             D[t % 2] -> one multicast commit on mma_done[t % 2];
 //   warps 10-11      idle (a full third warpgroup so that setmaxnreg can move registers:
 //                             WG2 drops to 56, the stager rises to 248, the drainer to 200).
-// The stager of tile t+1 only waits for MMA(t) to have READ the A columns (mma_done(t)),
-// so staging t+1, the MMAs of t and the drain of t-1 run concurrently.
-// With GFT_A_BUFS == 2 the A columns are double-buffered too (tile t uses A[t % 2]) and the
-// stager of tile t+1 only waits for MMA(t-1).
-// TMEM: A = all leaves' hi/lo columns (x GFT_A_BUFS), D = all leaves' D columns x 2.
+// The A columns are staged and released per 32-column chunk (GFT_NCH chunks over all
+// tensor-core leaves): the issuer waits for chunk c of tile t to be staged (both CTAs), issues
+// its MMAs (all three 3xTF32 passes of its k-steps) and commits them to a_free[c]; the stager
+// of tile t+1 overwrites chunk c as soon as a_free[c] fires.  So staging tile t+1 runs under
+// the MMAs of tile t (one A buffer suffices), and the drain of tile t-1 beside both.
+// TMEM: A = all leaves' hi/lo columns, D = all leaves' D columns x 2.
 // Generated part: GFT_N, GFT_STAGES, GFT_TMEM_COLS, GFT_B_FLOATS, GFT_KNAME, gft_tcB[2][],
-// GFT_A_COLS (per A buffer), GFT_A_BUFS, GFT_D_BASE (D buffer 0 base), GFT_D_COLS (per
-// buffer), GFT_SMALL (1 if CUDA-core leaves exist), gft_stage(), gft_drain(), gft_issue_ws().
+// GFT_A_COLS, GFT_NCH, GFT_D_BASE (D buffer 0 base), GFT_D_COLS (per buffer), GFT_SMALL (1 if
+// CUDA-core leaves exist), gft_stage(), gft_drain(), gft_finish(), gft_issue_ws().
 typedef unsigned int u32;
 typedef unsigned long long u64;
 typedef float elem_t;
@@ -100,6 +101,31 @@ static __device__ __forceinline__ void tma_load_2d(u32 dst, const TmaDesc* desc,
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       :: "r"(dst), "l"((u64)desc), "r"(c0), "r"(c1), "r"(bar) : "memory");
 }
+template <int N_>
+static __device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N_) : "memory");
+}
+static __device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Load pacing: consecutive tile loads of a CTA at least GFT_LOAD_PACE_NS apart (codegen sets
+// it to 0.9 x this CTA's fair share of HBM time per tile, i.e. a cap ~10% above the roof).
+// Without it, at the full SM clock the CTAs issue their refills in synchronised bursts and
+// the kernels move 5.5 TB/s instead of 6.3-6.45 (cfg5b IO-split, tools/r02/gpu_tc_probe7.sh);
+// under sustained load (capped clock) the cap never binds.
+#ifndef GFT_LOAD_PACE_NS
+#define GFT_LOAD_PACE_NS 0
+#endif
+static __device__ __forceinline__ void pace_load(unsigned long long& t_last, long long it) {
+  if (GFT_LOAD_PACE_NS > 0) {
+    unsigned long long now = globaltimer_ns();
+    if (it > 0)
+      while (now - t_last < (unsigned long long)GFT_LOAD_PACE_NS) { __nanosleep(64); now = globaltimer_ns(); }
+    t_last = now;
+  }
+}
 static __device__ __forceinline__ void tma_store_2d(const TmaDesc* desc, int c0, int c1, u32 src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
                :: "l"((u64)desc), "r"(c0), "r"(c1), "r"(src) : "memory");
@@ -154,6 +180,19 @@ static __device__ __forceinline__ void signal_staged(u32 staged_cluster_addr) {
 }
 
 
+// Phase trace (experiments only: GFT_TC_TRACE=1 adds `#define GFT_TRACE 1`): clock64 stamps of
+// each role per tile for CTAs 0..7, printed by CTA 0 and 1 at exit.  Events: 0 load issued,
+// 1 stager: tile landed, 2 rows in registers, 3 staged; 4 issuer: waits done, 5 committed;
+// 6 drainer: MMAs done, 7 rows written; 8 storer: output ready, 9 store has read the buffer.
+#ifdef GFT_TRACE
+#define GFT_TR_EV 10
+#define GFT_TR_TILES 48
+__device__ unsigned long long gft_trace_buf[8][GFT_TR_TILES][GFT_TR_EV];
+#define TR(ev, itv) do { if (blockIdx.x < 8 && (itv) < GFT_TR_TILES) gft_trace_buf[blockIdx.x][(itv)][(ev)] = clock64(); } while (0)
+#else
+#define TR(ev, itv) do { } while (0)
+#endif
+
 // @@GFT_GENERATED@@  (codegen.cpp inserts gft_tcB[][], gft_stage(), gft_drain(), gft_issue_ws())
 
 // register split of the 12 warps (65536 = 32 x 4 x (248 + 200 + 56)): the stager holds a row
@@ -172,23 +211,29 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
 #define GFT_IO_SPLIT 0
 #endif
   // GFT_IO_SPLIT: input ring of GFT_STAGES buffers released by the stager as soon as its rows
-  // are in registers, plus ONE output buffer the drainer fills and a storer warp drains
+  // are in registers, plus ONE output buffer the drainer fills box by box and a storer warp
+  // drains box by box
   unsigned char* stages = smem;
   unsigned char* outbuf = smem + GFT_STAGES * GFT_TILE_BYTES;
   unsigned char* bsm = smem + (GFT_STAGES + GFT_IO_SPLIT) * GFT_TILE_BYTES;   // this CTA's half of B
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(bsm + GFT_B_FLOATS * 4);
-  // bars: full[S], done[S] (= input free when IO-split), rows[S], staged[2], mma_done[2],
-  // d_free[2], out_ready, out_free (staged alternates per tile, so a stager running a tile
-  // ahead -- two A buffers -- can never complete a phase the issuer has not yet observed)
+  // bars: full[S], done[S] (= input free when IO-split), rows[S], then the ones below
+  // (staged alternates per tile parity, so a stager a tile ahead can never complete a phase
+  // the issuer has not yet observed)
   unsigned long long* b_full = bars;
   unsigned long long* b_done = bars + GFT_STAGES;
   unsigned long long* b_rows = bars + 2 * GFT_STAGES;
-  unsigned long long* b_staged = bars + 3 * GFT_STAGES;
-  unsigned long long* b_mma = bars + 3 * GFT_STAGES + 2;
-  unsigned long long* b_dfree = bars + 3 * GFT_STAGES + 4;
-  unsigned long long* b_outrdy = bars + 3 * GFT_STAGES + 6;
-  unsigned long long* b_outfree = bars + 3 * GFT_STAGES + 7;
-  u32* tmem_slot = reinterpret_cast<u32*>(bars + 3 * GFT_STAGES + 8);
+  unsigned long long* b_mma = bars + 3 * GFT_STAGES;           // [2]: tile's MMAs done (D[t%2] full)
+  unsigned long long* b_dfree = bars + 3 * GFT_STAGES + 2;     // [2]: D[t%2] drained
+  // IO-split output ring at TMA-box granularity: box b of the output buffer is written by the
+  // drainer (box_ready[b], 4 warps) and released once its store has read it (box_free[b])
+  unsigned long long* b_boxrdy = bars + 3 * GFT_STAGES + 4;
+  unsigned long long* b_boxfree = bars + 3 * GFT_STAGES + 4 + GFT_NBOX;
+  // per A chunk: staged[t%2][c] (leader; 8 stager warps of the pair), a_free[c] (MMAs of the
+  // chunk done, multicast commit)
+  unsigned long long* b_staged = bars + 3 * GFT_STAGES + 4 + 2 * GFT_NBOX;
+  unsigned long long* b_afree = b_staged + 2 * GFT_NCH;
+  u32* tmem_slot = reinterpret_cast<u32*>(b_afree + GFT_NCH);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const u32 rank = cluster_rank();
   const long long npairs = (batch + 2 * GFT_TILE_ROWS - 1) / (2 * GFT_TILE_ROWS);
@@ -209,12 +254,15 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       mbar_init(smem_u32(&b_rows[s]), 4);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(smem_u32(&b_staged[b]), 8);
       mbar_init(smem_u32(&b_mma[b]), 1);
       mbar_init(smem_u32(&b_dfree[b]), 8);
     }
-    mbar_init(smem_u32(b_outrdy), 4);
-    mbar_init(smem_u32(b_outfree), 1);
+    for (int c = 0; c < 2 * GFT_NCH; ++c) mbar_init(smem_u32(&b_staged[c]), 8);
+    for (int c = 0; c < GFT_NCH; ++c) mbar_init(smem_u32(&b_afree[c]), 1);
+    for (int b = 0; b < GFT_NBOX; ++b) {
+      mbar_init(smem_u32(&b_boxrdy[b]), 4);
+      mbar_init(smem_u32(&b_boxfree[b]), 1);
+    }
     fence_mbar_init();
   }
   const float4* bsrc = reinterpret_cast<const float4*>(gft_tcB[rank]);
@@ -234,12 +282,15 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
 #if GFT_IO_SPLIT
     if (warp == 8 && lane == 0) {
       // ---------------- loader: input ring, refilled as soon as the stager has read a tile ----
+      unsigned long long t_last = 0;
       for (long long it = 0;; ++it) {
         const long long p = pid0 + it * npid;
         if (p >= npairs) break;
         const long long row0 = p * 2 * GFT_TILE_ROWS + rank * GFT_TILE_ROWS;
         const int s = (int)(it % GFT_STAGES);
         if (it >= GFT_STAGES) mbar_wait(smem_u32(&b_done[s]), (u32)(((it / GFT_STAGES) - 1) & 1));
+        pace_load(t_last, it);
+        TR(0, it);
         const u32 bar = smem_u32(&b_full[s]);
         const u32 dst = smem_u32(stages + s * GFT_TILE_BYTES);
         mbar_expect_tx(bar, GFT_TILE_BYTES);
@@ -247,24 +298,33 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
           tma_load_2d(dst + b * GFT_BOX_BYTES, &tin, b * GFT_BOXC, (int)row0, bar);
       }
     } else if (warp == 10 && lane == 0) {
-      // ---------------- storer: the output buffer -> HBM, then hand it back to the drainer ----
+      // ---------------- storer: output boxes -> HBM as soon as each is written; a box slot is
+      // handed back to the drainer once the store that read it has finished reading (the
+      // store of the NEXT box is already in flight then: one store group outstanding)
+      int prev = -1;
       for (long long it = 0;; ++it) {
         const long long p = pid0 + it * npid;
         if (p >= npairs) break;
         const long long row0 = p * 2 * GFT_TILE_ROWS + rank * GFT_TILE_ROWS;
-        mbar_wait(smem_u32(b_outrdy), (u32)(it & 1));
-        const u32 src = smem_u32(outbuf);
-        for (int b = 0; b < GFT_NBOX; ++b)
-          tma_store_2d(&tout, b * GFT_BOXC, (int)row0, src + b * GFT_BOX_BYTES);
-        bulk_commit();
-        bulk_wait_read0();
-        mbar_arrive(smem_u32(b_outfree));
+        for (int b = 0; b < GFT_NBOX; ++b) {
+          mbar_wait(smem_u32(&b_boxrdy[b]), (u32)(it & 1));
+          if (b == 0) TR(8, it);
+          tma_store_2d(&tout, b * GFT_BOXC, (int)row0, smem_u32(outbuf) + b * GFT_BOX_BYTES);
+          bulk_commit();
+          if (prev >= 0) {
+            bulk_wait_read<1>();
+            mbar_arrive(smem_u32(&b_boxfree[prev]));
+          }
+          prev = b;
+        }
+        TR(9, it);
       }
       bulk_wait_all();
     } else
 #endif
     if (warp == 8 && lane == 0) {
       // ---------------- producer / storer of this CTA's 128 rows per pair tile ----------------
+      unsigned long long t_last = 0;
       long long it = 0;
       for (;; ++it) {
         const long long p = pid0 + it * npid;
@@ -280,6 +340,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
           bulk_commit();
           bulk_wait_read0();
         }
+        pace_load(t_last, it);
         const u32 bar = smem_u32(&b_full[s]);
         const u32 dst = smem_u32(stages + s * GFT_TILE_BYTES);
         mbar_expect_tx(bar, GFT_TILE_BYTES);
@@ -303,42 +364,42 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       for (long long it = 0;; ++it) {
         if (pid0 + it * npid >= npairs) break;
         const int b = (int)(it & 1);
-        mbar_wait_acq_cluster(smem_u32(&b_staged[b]), (u32)((it >> 1) & 1));
         if (it >= 2) mbar_wait_acq_cluster(smem_u32(&b_dfree[b]), (u32)(((it >> 1) - 1) & 1));
-        tc_fence_after();
+        TR(4, it);
         // re-materialise the B base each tile so the ~100 MMA descriptors are not hoisted
         // out of the loop into registers (this warpgroup runs with 56 registers)
         u32 bs;
         asm volatile("mov.b32 %0, %1;" : "=r"(bs) : "r"(bsm_s));
-        gft_issue_ws(tmem + (u32)((GFT_A_BUFS == 2 ? b : 0) * GFT_A_COLS), tmem + (u32)(GFT_D_BASE + b * GFT_D_COLS), bs);
+        gft_issue_ws(tmem, tmem + (u32)(GFT_D_BASE + b * GFT_D_COLS), bs, smem_u32(&b_staged[b * GFT_NCH]),
+                     (u32)((it >> 1) & 1), smem_u32(b_afree));
         tc_commit_pair(smem_u32(&b_mma[b]));
+        TR(5, it);
       }
     }
   } else if (warp < 4) {
     // ---------------- stager (row = TMEM lane = tid) ----------------
     reg_stager();
     const u32 tm_a = tmem + ((u32)(warp * 32) << 16);
-    const u32 staged0[2] = {map_to_cta(smem_u32(&b_staged[0]), 0), map_to_cta(smem_u32(&b_staged[1]), 0)};
+    const u32 staged0[2] = {map_to_cta(smem_u32(&b_staged[0]), 0), map_to_cta(smem_u32(&b_staged[GFT_NCH]), 0)};
     for (long long it = 0;; ++it) {
       const long long p = pid0 + it * npid;
       if (p >= npairs) break;
       const int s = (int)(it % GFT_STAGES);
       mbar_wait(smem_u32(&b_full[s]), (u32)((it / GFT_STAGES) & 1));
+      if (tid == 0) TR(1, it);
       unsigned char* buf = stages + s * GFT_TILE_BYTES;
       float x[GFT_N];
       load_row(buf, tid, x);
+      if (tid == 0) TR(2, it);
 #if GFT_IO_SPLIT
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&b_done[s]));   // input rows consumed: refill
 #endif
       // before writing the A columns: the MMAs that last read this A buffer (tile t-1, or
       // t-2 with two buffers) are done
-#if GFT_A_BUFS == 2
-      gft_stage(x, tm_a + (u32)((it & 1) * GFT_A_COLS), staged0[it & 1], buf, tid, smem_u32(&b_mma[it & 1]),
-                (u32)(((it - 2) >> 1) & 1), it >= 2);
-#else
-      gft_stage(x, tm_a, staged0[it & 1], buf, tid, smem_u32(&b_mma[(it - 1) & 1]), (u32)(((it - 1) >> 1) & 1), it >= 1);
-#endif
+      // chunk c of A is rewritten once the MMAs of tile it-1 on it are done (a_free[c])
+      gft_stage(x, tm_a, staged0[it & 1], buf, tid, smem_u32(b_afree), (u32)((it - 1) & 1), it >= 1);
+      if (tid == 0) TR(3, it);
 #if GFT_SMALL
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&b_rows[s]));   // release: small-leaf outputs in SMEM
@@ -356,12 +417,12 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       const int b = (int)(it & 1);
       mbar_wait(smem_u32(&b_mma[b]), (u32)((it >> 1) & 1));
       tc_fence_after();
+      if (row == 0) TR(6, it);
 #if GFT_SMALL
       mbar_wait(smem_u32(&b_rows[s]), (u32)((it / GFT_STAGES) & 1));
 #endif
 #if GFT_IO_SPLIT
       unsigned char* buf = outbuf;
-      if (it >= 1) mbar_wait(smem_u32(b_outfree), (u32)((it - 1) & 1));   // store has read it
 #else
       unsigned char* buf = stages + s * GFT_TILE_BYTES;
 #endif
@@ -372,18 +433,41 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(map_to_cta(smem_u32(&b_dfree[b]), 0));
       gft_finish(y);
+#if GFT_IO_SPLIT
+#pragma unroll
+      for (int b = 0; b < GFT_NBOX; ++b) {
+        if (it >= 1) mbar_wait(smem_u32(&b_boxfree[b]), (u32)((it - 1) & 1));   // its last store has read it
+#pragma unroll
+        for (int c = 32 * b; c < 32 * b + 32 && c < GFT_N; c += 4)
+          *reinterpret_cast<float4*>(buf + tile_off(row, c)) = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&b_boxrdy[b]));
+      }
+      if (row == 0) TR(7, it);
+#else
       store_row(buf, row, y);
       fence_proxy_async();
       __syncwarp();
-#if GFT_IO_SPLIT
-      if (lane == 0) mbar_arrive(smem_u32(b_outrdy));
-#else
       if (lane == 0) mbar_arrive(smem_u32(&b_done[s]));
 #endif
     }
   }
   tc_fence_before();
   __syncthreads();
+#ifdef GFT_TRACE
+  if (blockIdx.x < 2 && tid == 0) {
+    const long long nt = (npairs - pid0 + npid - 1) / npid;
+    for (int i = 0; i < GFT_TR_TILES && i < nt; ++i) {
+      const unsigned long long* e = gft_trace_buf[blockIdx.x][i];
+      const unsigned long long b0 = gft_trace_buf[blockIdx.x][0][0];
+      printf("TRACE cta %d tile %d: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", (int)blockIdx.x, i,
+             (long long)(e[0] - b0), (long long)(e[1] - b0), (long long)(e[2] - b0), (long long)(e[3] - b0),
+             (long long)(e[4] - b0), (long long)(e[5] - b0), (long long)(e[6] - b0), (long long)(e[7] - b0),
+             (long long)(e[8] - b0), (long long)(e[9] - b0));
+    }
+  }
+#endif
   cluster_sync();   // the peer may still be reading our B half / arriving on our barriers
   if (warp == 0) {
     tc_fence_after();

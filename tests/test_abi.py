@@ -190,7 +190,9 @@ def test_tuning_record_get_set_on_cpu():
         assert ei.value.name == "GFT_ERR_INVALID_ARG"
     # tensor-core kernels: the record is the tcgen05 variant; it round-trips through the bytes
     t = G.Plan.from_config(workloads.config("cfg5b"), dtypes=("f32",))
-    assert t.tuning("f32", (0,))[0] == (-1, -1, -1, -1, 0)          # plain CTA pair (n = 128)
+    assert t.tuning("f32", (0,))[0] == (-1, -1, -1, -1, 2)          # IO-split warp-specialised (n = 128)
+    t.set_tuning({0: (-1, -1, -1, -1, 0)}, "f32")                    # plain CTA pair
+    assert "fwdtc2_" in t.kernel_name(0, "f32") and t.tuning("f32", (0,))[0][4] == 0
     t.set_tuning({0: (-1, -1, -1, -1, 3)}, "f32")                    # single CTA
     assert "fwdtc_" in t.kernel_name(0, "f32") and t.tuning("f32", (0,))[0][4] == 3
     u = G.Plan.load(t.save(), dtypes=("f32",))

@@ -204,24 +204,31 @@ def test_random_symmetric_graphs_on_gpu():
 
 
 def test_tensor_core_single_cta_and_pair_variants_agree(monkeypatch):
-    """cfg5b through both tcgen05 variants: the CTA-pair (cta_group::2, default) kernel and
-    the single-CTA kernel (GFT_NO_CTA_PAIR=1) against the oracle and each other."""
+    """cfg5b through the three tcgen05 variants that apply at n = 128: the IO-split
+    warp-specialised pair kernel (default), the plain CTA-pair kernel (GFT_TC_IOSPLIT=0) and
+    the single-CTA kernel (GFT_NO_CTA_PAIR=1) -- against the oracle and each other."""
     cfg = workloads.config("cfg5b")
+    ws = G.Plan.from_config(cfg, dtypes=("f32",), no_cubin_cache=True)
+    monkeypatch.setenv("GFT_TC_IOSPLIT", "0")
     pair = G.Plan.from_config(cfg, dtypes=("f32",), no_cubin_cache=True)
+    monkeypatch.delenv("GFT_TC_IOSPLIT")
     monkeypatch.setenv("GFT_NO_CTA_PAIR", "1")
     single = G.Plan.from_config(cfg, dtypes=("f32",), no_cubin_cache=True)
     monkeypatch.delenv("GFT_NO_CTA_PAIR")
+    assert "tc3s_" in ws.kernel_name(G.K_FAST_FWD)
     assert "tc2_" in pair.kernel_name(G.K_FAST_FWD) and "tc_" in single.kernel_name(G.K_FAST_FWD)
     lam_o, U_o = oracle_basis("cfg5b")
     X = workloads.signals(cfg, batch=1000, dtype="f32")   # ragged: 1000 = 3 pair tiles + 232 rows
     Xd = X.cuda()
-    for plan in (pair, single):
+    for plan in (ws, pair, single):
         Y = plan.forward(Xd)
         Xr = plan.inverse(Y)
         torch.cuda.synchronize()
         check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
         assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
-    assert oracle.relative_error(pair.forward(Xd).cpu().numpy(), single.forward(Xd).cpu().numpy()).max() < 1e-6
+    ref = single.forward(Xd).cpu().numpy()
+    for plan in (ws, pair):
+        assert oracle.relative_error(plan.forward(Xd).cpu().numpy(), ref).max() < 1e-6
 
 
 @pytest.mark.parametrize("inverse_small_leaf", [False, True])
@@ -425,14 +432,32 @@ def test_two_sparse_eigenvector_graphs_on_gpu(kind, n, dtype):
     assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL[dtype]
 
 
-def test_tensor_core_io_split_experiment(monkeypatch):
-    """The opt-in IO-split warp-specialised kernel (GFT_TC_IOSPLIT=1, n > 64, all leaves on
-    the tensor core) stays correct: cfg5b forward / inverse vs the oracle."""
+@pytest.mark.parametrize("batch", [1, 255, 257, 1000, 70001])
+def test_tensor_core_io_split_kernel(batch):
+    """The IO-split warp-specialised kernel (default for n > 64 with every leaf on the tensor
+    core: two input buffers, box-granular output ring, per-chunk A release, load pacing):
+    cfg5b forward / inverse vs the oracle over one, several and a ragged number of pair tiles."""
     cfg = workloads.config("cfg5b")
-    monkeypatch.setenv("GFT_TC_IOSPLIT", "1")
+    plan = G.Plan.from_config(cfg, dtypes=("f32",))
+    assert "tc3s_" in plan.kernel_name(G.K_FAST_FWD) and "tc3s_" in plan.kernel_name(G.K_FAST_INV)
+    src = plan.kernel_source(G.K_FAST_FWD, "f32")
+    assert "#define GFT_IO_SPLIT 1" in src and "#define GFT_LOAD_PACE_NS" in src and "#define GFT_NCH 4" in src
+    lam_o, U_o = oracle_basis("cfg5b")
+    X = workloads.signals(cfg, batch=batch, dtype="f32")
+    Y = plan.forward(X.cuda())
+    Xr = plan.inverse(Y)
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
+
+
+def test_tensor_core_plain_pair_ablation(monkeypatch):
+    """GFT_TC_IOSPLIT=0 keeps the plain CTA-pair kernel for cfg5b; it stays correct."""
+    cfg = workloads.config("cfg5b")
+    monkeypatch.setenv("GFT_TC_IOSPLIT", "0")
     plan = G.Plan.from_config(cfg, dtypes=("f32",), no_cubin_cache=True)
     monkeypatch.delenv("GFT_TC_IOSPLIT")
-    assert "tc3s_" in plan.kernel_name(G.K_FAST_FWD)
+    assert "tc2_" in plan.kernel_name(G.K_FAST_FWD)
     lam_o, U_o = oracle_basis("cfg5b")
     X = workloads.signals(cfg, batch=1000, dtype="f32")
     Y = plan.forward(X.cuda())
@@ -443,10 +468,10 @@ def test_tensor_core_io_split_experiment(monkeypatch):
 
 
 @pytest.mark.parametrize("leaves", [1, 2])
-def test_tensor_core_ws_double_a_experiment(monkeypatch, leaves):
-    """Opt-in double-buffered A operand of the warp-specialised kernel (GFT_TC_WS_A2=1): a
-    64-node graph with one 64-leaf (no symmetry: random weights) or a mirror-symmetric one
-    with two 32-leaves, forward / inverse vs the oracle over several tiles + a ragged tail."""
+def test_tensor_core_ws_chunked_staging(leaves):
+    """The in-place warp-specialised kernel (n <= 64) stages and releases A per 32-column
+    chunk: a 64-node graph with one 64-leaf (no symmetry: random weights) or a mirror-symmetric
+    one with two 32-leaves, forward / inverse vs the oracle over several tiles + a ragged tail."""
     rng = np.random.default_rng(7 + leaves)
     n = 64
     if leaves == 1:
@@ -459,32 +484,12 @@ def test_tensor_core_ws_double_a_experiment(monkeypatch, leaves):
         w = np.concatenate([wh, wh, np.full(32, 0.7)])
     s = np.array([p[0] for p in pairs], np.int32)
     d = np.array([p[1] for p in pairs], np.int32)
-    monkeypatch.setenv("GFT_TC_WS_A2", "1")
-    plan = G.Plan(n, s, d, w, dtypes=("f32",), no_cubin_cache=True)
-    monkeypatch.delenv("GFT_TC_WS_A2")
+    plan = G.Plan(n, s, d, w, dtypes=("f32",))
     src = plan.kernel_source(G.K_FAST_FWD, "f32")
-    assert "tc3_" in plan.kernel_name(G.K_FAST_FWD) and "#define GFT_A_BUFS 2" in src
+    assert "tc3_" in plan.kernel_name(G.K_FAST_FWD) and "#define GFT_NCH 2" in src
     assert plan.leaf_sizes() == ([64] if leaves == 1 else [32, 32])
     lam_o, U_o = oracle.gft_basis(oracle.laplacian(n, s, d, w))
     X = torch.randn(5000, n, generator=torch.Generator().manual_seed(leaves))
-    Y = plan.forward(X.cuda())
-    Xr = plan.inverse(Y)
-    torch.cuda.synchronize()
-    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
-    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
-
-
-@pytest.mark.parametrize("batch", [1, 3, 4, 130, 1001])
-def test_superrow_tma_mode_experiment(monkeypatch, batch):
-    """Opt-in super-row TMA mode for odd row pitch (GFT_SUPERROW=1): cfg3 with batches
-    that are / are not multiples of 4 (the batch % 4 tail takes the direct path)."""
-    cfg = workloads.config("cfg3")
-    monkeypatch.setenv("GFT_SUPERROW", "1")
-    plan = G.Plan.from_config(cfg, dtypes=("f32",), no_cubin_cache=True)
-    monkeypatch.delenv("GFT_SUPERROW")
-    assert "#define GFT_MODE 2" in plan.kernel_source(G.K_FAST_FWD, "f32")
-    lam_o, U_o = oracle_basis("cfg3")
-    X = workloads.signals(cfg, batch=batch, dtype="f32")
     Y = plan.forward(X.cuda())
     Xr = plan.inverse(Y)
     torch.cuda.synchronize()

@@ -1,0 +1,6 @@
+out=gpurun_out/r02_tc_probe7.log
+: > $out
+for v in "GFT_TC_IOSPLIT=1 GFT_TC_LOAD_PACE_NS=2700" "GFT_TC_IOSPLIT=1 GFT_TC_LOAD_PACE_NS=2900" "GFT_TC_IOSPLIT=1 GFT_TC_LOAD_PACE_NS=3100" "GFT_TC_IOSPLIT=1 GFT_TC_SPLIT=rna"; do
+  env $v timeout 300 python tools/r02/tc_probe.py cfg5b >> $out 2>&1
+  sleep 5
+done
