@@ -660,7 +660,7 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
   // ---- stager: per 32-column A chunk c, wait until the MMAs of the previous tile on it are
   // done (a_free[c]), write hi/lo, signal staged[c] on the leader ----
   o << "static __device__ __forceinline__ void gft_stage(float (&x)[GFT_N], u32 tm, u32 staged0,\n"
-       "    unsigned char* buf, int row, u32 afree, u32 apar, bool await_a) {\n";
+       "    unsigned char* buf, int row, u32 afree, u32 apar, bool await_a, long long it) {\n";
   if (d != DIR_INV) emit_units(o, P, "x", false, dtype);
   if (d == DIR_FILTER && !P.post.empty()) fail(GFT_ERR_COMPILE, "filter plan with right Haar stages");
   if (d == DIR_INV) emit_post_units(o, P, "x", true, "float");
@@ -670,6 +670,7 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
     for (int c0 = 0; c0 < t.kp8; c0 += 32, ++ch) {
       const int w = std::min(32, t.kp8 - c0);
       o << "  if (await_a) { mbar_wait(afree + " << 8 * ch << "u, apar); tc_fence_after(); }\n";
+      o << "  if (row == 0) TR(" << 14 + std::min(ch, 3) << ", it);\n";
       o << "  { u32 h[" << w << "], l[" << w << "];\n";
       for (int c = c0; c < c0 + w; ++c) {
         if (c < t.k) {
@@ -724,7 +725,8 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
   o << "}\n";
   // ---- issuer: chunk by chunk (all three passes of the chunk's k-steps), each chunk's MMAs
   // committed to a_free[c] so the stager can refill it ----
-  o << "static __device__ __forceinline__ void gft_issue_ws(u32 tA, u32 tD, u32 bsm, u32 staged, u32 spar, u32 afree) {\n";
+  o << "static __device__ __forceinline__ void gft_issue_ws(u32 tA, u32 tD, u32 bsm, u32 staged, u32 spar, u32 afree,\n"
+       "    long long it) {\n";
   ch = 0;
   for (const TcLeaf& t : T) {
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(t.np >> 3) << 17) | (16u << 24);
@@ -732,6 +734,7 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
     for (int c0 = 0; c0 < t.kp8; c0 += 32, ++ch) {
       const int w = std::min(32, t.kp8 - c0);
       o << "  mbar_wait_acq_cluster(staged + " << 8 * ch << "u, spar); tc_fence_after();\n";
+      o << "  TR(" << 10 + std::min(ch, 3) << ", it);\n";
       for (int pass = 0; pass < 3; ++pass) {
         const int acol = pass == 2 ? t.lo_col : t.hi_col;
         const int boff = pass == 1 ? t.blo_off : t.bhi_off;

@@ -183,9 +183,10 @@ static __device__ __forceinline__ void signal_staged(u32 staged_cluster_addr) {
 // Phase trace (experiments only: GFT_TC_TRACE=1 adds `#define GFT_TRACE 1`): clock64 stamps of
 // each role per tile for CTAs 0..7, printed by CTA 0 and 1 at exit.  Events: 0 load issued,
 // 1 stager: tile landed, 2 rows in registers, 3 staged; 4 issuer: waits done, 5 committed;
-// 6 drainer: MMAs done, 7 rows written; 8 storer: output ready, 9 store has read the buffer.
+// 6 drainer: MMAs done, 7 rows written; 8 storer: output ready, 9 store has read the buffer;
+// 10-13 issuer: chunk 0..3 staged; 14-17 stager: chunk 0..3 free (A columns).
 #ifdef GFT_TRACE
-#define GFT_TR_EV 10
+#define GFT_TR_EV 18
 #define GFT_TR_TILES 48
 __device__ unsigned long long gft_trace_buf[8][GFT_TR_TILES][GFT_TR_EV];
 #define TR(ev, itv) do { if (blockIdx.x < 8 && (itv) < GFT_TR_TILES) gft_trace_buf[blockIdx.x][(itv)][(ev)] = clock64(); } while (0)
@@ -371,7 +372,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
         u32 bs;
         asm volatile("mov.b32 %0, %1;" : "=r"(bs) : "r"(bsm_s));
         gft_issue_ws(tmem, tmem + (u32)(GFT_D_BASE + b * GFT_D_COLS), bs, smem_u32(&b_staged[b * GFT_NCH]),
-                     (u32)((it >> 1) & 1), smem_u32(b_afree));
+                     (u32)((it >> 1) & 1), smem_u32(b_afree), it);
         tc_commit_pair(smem_u32(&b_mma[b]));
         TR(5, it);
       }
@@ -398,7 +399,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       // before writing the A columns: the MMAs that last read this A buffer (tile t-1, or
       // t-2 with two buffers) are done
       // chunk c of A is rewritten once the MMAs of tile it-1 on it are done (a_free[c])
-      gft_stage(x, tm_a, staged0[it & 1], buf, tid, smem_u32(b_afree), (u32)((it - 1) & 1), it >= 1);
+      gft_stage(x, tm_a, staged0[it & 1], buf, tid, smem_u32(b_afree), (u32)((it - 1) & 1), it >= 1, it);
       if (tid == 0) TR(3, it);
 #if GFT_SMALL
       __syncwarp();
@@ -461,10 +462,13 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
     for (int i = 0; i < GFT_TR_TILES && i < nt; ++i) {
       const unsigned long long* e = gft_trace_buf[blockIdx.x][i];
       const unsigned long long b0 = gft_trace_buf[blockIdx.x][0][0];
-      printf("TRACE cta %d tile %d: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", (int)blockIdx.x, i,
+      printf("TRACE cta %d tile %d: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n",
+             (int)blockIdx.x, i,
              (long long)(e[0] - b0), (long long)(e[1] - b0), (long long)(e[2] - b0), (long long)(e[3] - b0),
              (long long)(e[4] - b0), (long long)(e[5] - b0), (long long)(e[6] - b0), (long long)(e[7] - b0),
-             (long long)(e[8] - b0), (long long)(e[9] - b0));
+             (long long)(e[8] - b0), (long long)(e[9] - b0), (long long)(e[10] - b0), (long long)(e[11] - b0),
+             (long long)(e[12] - b0), (long long)(e[13] - b0), (long long)(e[14] - b0), (long long)(e[15] - b0),
+             (long long)(e[16] - b0), (long long)(e[17] - b0));
     }
   }
 #endif
