@@ -556,7 +556,7 @@ void tune_slot(const gft::Plan& P, std::unique_ptr<gft::Kernel>& slot, int kind,
     const int row = g.n * g.elem;
     for (int R : {1, 2, 4, 8})
       for (int S : {2, 3, 4})
-        for (int W : {4, 8, 12}) {
+        for (int W : {1, 2, 3, 4, 8, 12}) {
           const int tile = 32 * R * row;
           if (tile < 1024 || tile > 32768 || W * S * (tile + 8) + 1024 > 227 * 1024) continue;
           ovs.push_back(gft::CfgOverride{R, S, W, 0});

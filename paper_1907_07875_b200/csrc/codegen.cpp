@@ -81,12 +81,13 @@ KernelCfg choose_cfg(int n, int dtype, int64_t work, const CfgOverride* ov, int 
   c.stages = 2;
   c.warps = std::max(2, std::min(12, (150 * 1024) / (c.stages * c.tile_bytes())));
   // measured geometry for this (n, dtype) if the tuning table has one (tools/gpu_autotune.py)
-  int tR, tS, tW, tP;
-  if (tuned_geometry(n, dtype, work, kind, tR, tS, tW, tP)) {
+  int tR, tS, tW, tP, tO;
+  if (tuned_geometry(n, dtype, work, kind, tR, tS, tW, tP, tO)) {
     c.R = tR;
     c.stages = tS;
     c.warps = tW;
     c.pace_ns = tP;
+    c.obuf = tO;
   }
   // tuning knobs for experiments (GFT_TUNE_R / _STAGES / _WARPS); defaults above
   auto env_int = [](const char* k, int v) { const char* e = getenv(k); return (e && *e) ? atoi(e) : v; };
@@ -94,6 +95,7 @@ KernelCfg choose_cfg(int n, int dtype, int64_t work, const CfgOverride* ov, int 
   c.stages = std::max(2, std::min(8, env_int("GFT_TUNE_STAGES", c.stages)));
   c.warps = std::max(1, std::min(16, env_int("GFT_TUNE_WARPS", c.warps)));
   c.pace_ns = std::max(0, std::min(100000, env_int("GFT_PACE_NS", c.pace_ns)));
+  c.obuf = std::max(0, std::min(2, env_int("GFT_FMA_OBUF", c.obuf)));   // experiments
   if (ov) {
     if (ov->R > 0) c.R = std::min(8, ov->R);
     if (ov->stages > 0) c.stages = std::max(2, std::min(8, ov->stages));
@@ -102,6 +104,7 @@ KernelCfg choose_cfg(int n, int dtype, int64_t work, const CfgOverride* ov, int 
   }
   // the 128B swizzle atom needs 1024-byte aligned tile buffers; TMA boxes hold <= 256 rows
   while (c.mode == 2 && c.swz_mask && c.tile_bytes() % 1024 != 0 && c.R < 8) c.R *= 2;
+  if (c.smem_bytes() > 227 * 1024) c.obuf = 0;
   if (c.smem_bytes() > 227 * 1024) c.stages = 2;
   if (c.smem_bytes() > 227 * 1024) c.warps = 2;
   return c;
@@ -1027,6 +1030,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
       << "\n#define GFT_STAGES " << c.stages << "\n#define GFT_MODE " << c.mode << "\n#define GFT_BOXC "
       << c.boxc << "\n#define GFT_SWZ_MASK " << c.swz_mask << "\n#define GFT_VEC " << c.vec << "\n#define GFT_PACK " << c.pack << "\n";
   if (c.pace_ns > 0) pre << "#define GFT_PACE_NS " << c.pace_ns << "\n";
+  if (c.obuf > 0) pre << "#define GFT_OBUF " << c.obuf << "\n";
   // name = kind/dtype/n + hash of everything that determines the code
   std::string key = pre.str() + body.str() + kSkeleton;
   char hbuf[32];

@@ -279,12 +279,13 @@ constexpr int64_t kMaxRowsPerLaunch = (int64_t)1 << 30;
 
 }  // namespace
 
-bool tuned_geometry(int n, int dtype, int64_t work, int kind, int& R, int& S, int& W, int& pace_ns) {
+bool tuned_geometry(int n, int dtype, int64_t work, int kind, int& R, int& S, int& W, int& pace_ns, int& obuf) {
   // lines: "fma <n> <f32|f64> <R> <S> <W> [work=<FMAs per signal>] [kind=fwd|inv|dfwd|dinv|filter]
-  // [pace=<ns>]"; an entry with a work / kind key applies only to kernels with exactly that
-  // leaf work / of that kind (plan-specific measurements); the most specific match wins
-  // (work and kind > work > kind > plain).  pace = per-tile __nanosleep of the FMA skeleton.
-  struct Entry { int n, dt, R, S, W, pace, kind; int64_t work; };
+  // [pace=<ns>] [obuf=<0|1|2>]"; an entry with a work / kind key applies only to kernels with
+  // exactly that leaf work / of that kind (plan-specific measurements); the most specific match
+  // wins (work and kind > work > kind > plain).  pace = per-tile __nanosleep of the FMA
+  // skeleton; obuf = output tiles per warp (IO split, kernel_skeleton.cuh).
+  struct Entry { int n, dt, R, S, W, pace, kind, obuf; int64_t work; };
   static const std::vector<Entry> table = [] {
     std::vector<Entry> t;
     const char* e = getenv("GFT_TUNING_FILE");
@@ -302,9 +303,11 @@ bool tuned_geometry(int n, int dtype, int64_t work, int kind, int& R, int& S, in
       x.work = -1;
       x.pace = 0;
       x.kind = -1;
+      x.obuf = 0;
       while ((ss >> extra) && extra[0] != '#') {
         if (extra.rfind("work=", 0) == 0) x.work = std::atoll(extra.c_str() + 5);
         else if (extra.rfind("pace=", 0) == 0) x.pace = std::atoi(extra.c_str() + 5);
+        else if (extra.rfind("obuf=", 0) == 0) x.obuf = std::atoi(extra.c_str() + 5);
         else if (extra.rfind("kind=", 0) == 0)
           for (int k = 0; k < 5; ++k)
             if (extra.substr(5) == kKinds[k]) x.kind = k;
@@ -323,7 +326,7 @@ bool tuned_geometry(int n, int dtype, int64_t work, int kind, int& R, int& S, in
     if (score > best) { best = score; hit = &x; }
   }
   if (!hit) return false;
-  R = hit->R; S = hit->S; W = hit->W; pace_ns = hit->pace;
+  R = hit->R; S = hit->S; W = hit->W; pace_ns = hit->pace; obuf = hit->obuf;
   return true;
 }
 

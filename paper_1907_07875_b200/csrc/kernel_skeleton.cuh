@@ -31,6 +31,9 @@
 typedef unsigned int u32;
 typedef unsigned long long u64;
 typedef GFT_ELEM elem_t;
+#ifndef GFT_OBUF
+#define GFT_OBUF 0   // output tiles per warp (IO split); 0 = outputs in place in the input tile
+#endif
 
 struct __align__(64) TmaDesc { u64 d[16]; };
 
@@ -145,10 +148,13 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   const u32 raw_s = smem_u32(smem_raw);
   unsigned char* smem = smem_raw + ((1024u - (raw_s & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbuf = smem + (size_t)warp * (GFT_STAGES * GFT_TILE_BYTES);
+  // per warp: GFT_STAGES input tiles, then (GFT_OBUF > 0) GFT_OBUF output tiles
+  unsigned char* wbuf = smem + (size_t)warp * ((GFT_STAGES + GFT_OBUF) * GFT_TILE_BYTES);
+  unsigned char* obase = wbuf + GFT_STAGES * GFT_TILE_BYTES;
   unsigned long long* bars =
-      reinterpret_cast<unsigned long long*>(smem + (size_t)GFT_WARPS * GFT_STAGES * GFT_TILE_BYTES) +
+      reinterpret_cast<unsigned long long*>(smem + (size_t)GFT_WARPS * (GFT_STAGES + GFT_OBUF) * GFT_TILE_BYTES) +
       warp * GFT_STAGES;
+  (void)obase;
   const long long ntiles = (batch + GFT_TILE_ROWS - 1) / GFT_TILE_ROWS;
   const long long gw = (long long)blockIdx.x * GFT_WARPS + warp;
   const long long nw = (long long)gridDim.x * GFT_WARPS;
@@ -185,8 +191,8 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
               GFT_TILE_BYTES, bar);
 #endif
   };
-  auto issue_store = [&](long long t, int s) {
-    const u32 src = smem_u32(wbuf + s * GFT_TILE_BYTES);
+  auto issue_store = [&](long long t, const unsigned char* tbuf) {
+    const u32 src = smem_u32(tbuf);
 #if GFT_MODE == 0
 #pragma unroll
     for (int b = 0; b < GFT_NBOX; ++b)
@@ -219,18 +225,45 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
     if (!is_direct(t)) {
       mbar_wait(smem_u32(&bars[s]), (u32)((it / GFT_STAGES) & 1));
       unsigned char* buf = wbuf + s * GFT_TILE_BYTES;
+#if GFT_OBUF > 0
+      // IO split: outputs go to one of GFT_OBUF output tiles; the input tile is refilled with
+      // tile it + GFT_STAGES as soon as the last row has been read (not after the compute and
+      // the store), so GFT_STAGES - 1 .. GFT_STAGES loads stay in flight while a tile computes
+      unsigned char* obuf = obase + (int)(it % GFT_OBUF) * GFT_TILE_BYTES;
+      bool obuf_free = false;
+#else
+      unsigned char* obuf = buf;
+#endif
 #pragma unroll 1
       for (int r = 0; r < GFT_R; ++r) {
         const int row = lane + 32 * r;
 #if defined(GFT_STREAM)
         elem_t x[GFT_N];
         load_row(buf, row, x);
-        gft_body(x, buf, row);   // outputs written to the row by the generated code
 #else
         elem_t x[GFT_N], y[GFT_N];
         load_row(buf, row, x);
+#endif
+#if GFT_OBUF > 0
+        if (r == GFT_R - 1) {
+          fence_proxy_async();   // generic-proxy reads of the tile before the async-proxy refill
+          __syncwarp();
+          if (lane == 0) {
+            const long long tn = gw + (it + GFT_STAGES) * nw;
+            if (tn < ntiles && !is_direct(tn)) issue_load(tn, s);
+          }
+        }
+        if (!obuf_free) {   // the store that last read this output tile (tile it - GFT_OBUF) is done reading
+          if (lane == 0) bulk_wait_read<GFT_OBUF - 1>();
+          __syncwarp();
+          obuf_free = true;
+        }
+#endif
+#if defined(GFT_STREAM)
+        gft_body(x, obuf, row);   // outputs written to the row by the generated code
+#else
         gft_body(x, y);
-        store_row(buf, row, y);
+        store_row(obuf, row, y);
 #endif
       }
       fence_proxy_async();
@@ -243,8 +276,11 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       // (profiles/r01/autotune/pace_*.log)
       __nanosleep(GFT_PACE_NS);
 #endif
+#if GFT_OBUF > 0
+      if (lane == 0) issue_store(t, obuf);
+#else
       if (lane == 0) {
-        issue_store(t, s);
+        issue_store(t, buf);
         // the buffer consumed in the previous iteration is free once its store has read it
         bulk_wait_read<1>();
         if (it >= 1) {
@@ -252,6 +288,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
           if (tn < ntiles && !is_direct(tn)) issue_load(tn, (int)((it - 1) % GFT_STAGES));
         }
       }
+#endif
       __syncwarp();
     } else {
 #pragma unroll 1
@@ -278,6 +315,16 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
 #endif
         }
       }
+#if GFT_OBUF > 0
+      // (IO split) this stage's buffer is refilled after a tile is read; a direct tile used it
+      // as scratch, so its refill comes after the direct rows
+      __syncwarp();
+      if (lane == 0) {
+        const long long tn = gw + (it + GFT_STAGES) * nw;
+        if (tn < ntiles && !is_direct(tn)) issue_load(tn, s);
+      }
+      __syncwarp();
+#endif
     }
   }
   if (lane == 0) bulk_wait_all();

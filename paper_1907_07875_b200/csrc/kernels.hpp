@@ -24,6 +24,7 @@ struct KernelCfg {
   int boxc = 0, swz_mask = 0;   // TMA box columns, swizzle mask (7/3/1/0)
   int vec = 1;                  // elements per SMEM vector access
   int pace_ns = 0;              // FMA skeleton: per-tile __nanosleep before the store (tuning.tsv pace=)
+  int obuf = 0;                 // FMA skeleton IO split: output tiles per warp (0 = in place)
   // tensor-core variant (kernel_tc_skeleton.cuh): one 128-row tile per CTA iteration,
   // 4 compute warps + 1 TMA warp, big leaves as tcgen05 3xTF32 micro-GEMMs
   int tc = 0;
@@ -47,7 +48,7 @@ struct KernelCfg {
   int smem_bytes() const {
     if (dgemm) return stages * tile_bytes() + n * n * elem + 2 * stages * 8 + 1024;
     if (tc) return (stages + tc_io_split) * tile_bytes() + tc_b_bytes + (3 * stages + 24) * 8 + 16 + 1024;
-    return warps * stages * tile_bytes() + warps * stages * 8 + 1024;
+    return warps * (stages + obuf) * tile_bytes() + warps * stages * 8 + 1024;
   }
   int swizzle_bytes() const { return swz_mask == 7 ? 128 : swz_mask == 3 ? 64 : swz_mask == 1 ? 32 : 0; }
 };
@@ -105,9 +106,9 @@ void execute_host(Kernel& k, const void* in_host, void* out_host, int64_t batch,
 
 std::string cubin_cache_dir();
 
-// Measured geometry table (paper_1907_07875_b200/tuning.tsv, written by
-// tools/gpu_autotune.py on a B200): lines "fma <n> <f32|f64> <R> <S> <W>".  Returns false
+// Measured geometry table (paper_1907_07875_b200/tuning.tsv, written from geometry sweeps on
+// a B200): lines "fma <n> <f32|f64> <R> <S> <W> [work= kind= pace= obuf=]".  Returns false
 // if (n, dtype) has no entry.  GFT_TUNING_FILE overrides the path ("none" disables).
-bool tuned_geometry(int n, int dtype, int64_t work, int kind, int& R, int& S, int& W, int& pace_ns);
+bool tuned_geometry(int n, int dtype, int64_t work, int kind, int& R, int& S, int& W, int& pace_ns, int& obuf);
 
 }  // namespace gft

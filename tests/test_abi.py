@@ -155,7 +155,7 @@ def test_tuning_record_get_set_on_cpu():
     cfg = workloads.config("cfg3")
     p = G.Plan.from_config(cfg, dtypes=("f32",))
     rec = p.tuning("f32", kinds=(0, 1))
-    assert rec[0] == (3, 3, 4, 400, -1)      # tuning.tsv: fma 25 f32 3 3 4 pace=400
+    assert rec[0] == (4, 2, 3, 150, -1)      # tuning.tsv: fma 25 f32 4 2 3 pace=150 obuf=2
     name0 = p.kernel_name(0, "f32")
     p.set_tuning({0: (2, 2, 8, 150)}, "f32")
     src = p.kernel_source(0, "f32")
@@ -213,10 +213,19 @@ def test_tuning_table_kind_and_work_keys():
         m = re.search(r"#define GFT_PACE_NS (\d+)", src)
         return int(m.group(1)) if m else 0
 
+    def obuf(src):
+        m = re.search(r"#define GFT_OBUF (\d+)", src)
+        return int(m.group(1)) if m else 0
+
     c4 = G.Plan.from_config(workloads.config("cfg4"), dtypes=("f32",))
-    assert geo(c4.kernel_source(0, "f32")) == (2, 2, 4) and pace(c4.kernel_source(0, "f32")) == 0
+    src = c4.kernel_source(0, "f32")
+    assert geo(src) == (1, 3, 3) and pace(src) == 150 and obuf(src) == 2
     f4 = G.Filter(c4, np.ones(64), dtypes=("f32",))
-    assert geo(f4.kernel_source("f32")) == (1, 2, 8) and pace(f4.kernel_source("f32")) == 150
+    src = f4.kernel_source("f32")
+    assert geo(src) == (1, 2, 8) and pace(src) == 150 and obuf(src) == 0
+    c5 = G.Plan.from_config(workloads.config("cfg5a"), dtypes=("f32",))
+    assert geo(c5.kernel_source(0, "f32")) == (1, 2, 8) and obuf(c5.kernel_source(0, "f32")) == 0
+    assert geo(c5.kernel_source(1, "f32")) == (2, 2, 3) and obuf(c5.kernel_source(1, "f32")) == 2
     c1 = G.Plan.from_config(workloads.config("cfg1"), dtypes=("f32",))
     assert geo(c1.kernel_source(0, "f32")) == (8, 3, 4) and pace(c1.kernel_source(0, "f32")) == 0
     assert geo(c1.kernel_source(1, "f32")) == (8, 2, 8) and pace(c1.kernel_source(1, "f32")) == 150

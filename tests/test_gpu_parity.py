@@ -616,3 +616,29 @@ def test_guard_regions_ws_and_f64(which, batch):
     err = np.linalg.norm(Yd.cpu().double().numpy() - ref, axis=1) / np.linalg.norm(ref, axis=1)
     assert err.max() <= tol
     plan.close()
+
+
+@pytest.mark.parametrize("name,dtype,obuf", [("cfg3", "f32", 1), ("cfg3", "f32", 2), ("cfg4", "f64", 1),
+                                             ("cfg4", "f32", 2), ("cfg1", "f32", 2)])
+@pytest.mark.parametrize("batch", [1, 250, 4099])
+def test_fma_io_split_outputs(monkeypatch, name, dtype, obuf, batch):
+    """CUDA-core kernel with separate output tiles (IO split, GFT_FMA_OBUF / tuning.tsv obuf=):
+    bulk (odd pitch, direct ragged tail), TMA and packed-view modes, forward / inverse /
+    fused filter against the oracle on ragged batches."""
+    cfg = workloads.config(name)
+    monkeypatch.setenv("GFT_FMA_OBUF", str(obuf))
+    plan = G.Plan.from_config(cfg, dtypes=(dtype,), no_cubin_cache=True)
+    filt = G.Filter(plan, np.exp(-plan.eigenvalues()), dtypes=(dtype,), no_cubin_cache=True)
+    monkeypatch.delenv("GFT_FMA_OBUF")
+    assert "#define GFT_OBUF %d" % obuf in plan.kernel_source(G.K_FAST_FWD, dtype)
+    lam_o, U_o = oracle_basis(name)
+    X = workloads.signals(cfg, batch=batch, dtype=dtype)
+    Xd = X.cuda()
+    Y = plan.forward(Xd)
+    Xr = plan.inverse(Y)
+    Z = filt.apply(Xd)
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), TOL[dtype])
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL[dtype]
+    Zo = oracle.graph_filter(X.numpy().astype(np.float64), U_o, np.exp(-lam_o))
+    assert oracle.relative_error(Z.cpu().numpy(), Zo).max() <= 4 * TOL[dtype]

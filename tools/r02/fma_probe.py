@@ -40,5 +40,14 @@ for spec in sys.argv[1:]:
         ms = best
         r[tag] = round(nb / ms / 1e6 / 6454.9, 4)
     r["kernel"] = p.kernel_name(0, dt)
+    U = torch.from_numpy(p.basis()).cuda()
+    Xs = X[:70001]
+    p.forward(Xs, Y[:70001])
+    ref = Xs.double() @ U
+    r["fwd_err"] = float(((Y[:70001].double() - ref).norm(dim=1) / ref.norm(dim=1)).max())
+    f.apply(Xs, Y[:70001])
+    refh = ref * torch.from_numpy(np.exp(-p.eigenvalues())).cuda()
+    reff = refh @ U.T
+    r["filt_err"] = float(((Y[:70001].double() - reff).norm(dim=1) / reff.norm(dim=1)).max())
     out["%s_%s" % (name, dt)] = r
 print(json.dumps(out))

@@ -43,10 +43,13 @@ def timed(fn):
 res = []
 plan = gft.Plan.from_config(cfg, dtypes=(dt,), no_cubin_cache=True)
 default = None
-for R, S, W, pace in itertools.product((1, 2, 4), (2, 3), (4, 8, 12), (0, 150)):
+WARPS = tuple(int(w) for w in os.environ.get("SWEEP_WARPS", "4,8,12").split(","))
+OBUFS = tuple(int(w) for w in os.environ.get("SWEEP_OBUF", "0").split(","))
+for R, S, W, pace, ob in itertools.product((1, 2, 4), (2, 3), WARPS, (0, 150), OBUFS):
     tile = 32 * R * cfg.n * esz
-    if W * S * (tile + 8) + 1024 > 227 * 1024 or tile > 32768:
+    if W * (S + ob) * tile + W * S * 8 + 1024 > 227 * 1024 or tile > 32768:
         continue
+    os.environ["GFT_FMA_OBUF"] = str(ob)
     try:
         if kind == "filt":
             for k, v in (("GFT_TUNE_R", R), ("GFT_TUNE_STAGES", S), ("GFT_TUNE_WARPS", W), ("GFT_PACE_NS", pace)):
@@ -56,13 +59,14 @@ for R, S, W, pace in itertools.product((1, 2, 4), (2, 3), (4, 8, 12), (0, 150)):
             f.close()
         else:
             k = 0 if kind == "fwd" else 1
+            plan = gft.Plan.from_config(cfg, dtypes=(dt,), no_cubin_cache=True)
             plan.set_tuning({k: (R, S, W, pace)}, dt)
             fn = plan.forward if k == 0 else plan.inverse
             frac = timed(lambda: fn(X, Y))
     except gft.GFTError as e:
         continue
-    res.append(((R, S, W, pace), round(frac, 4)))
-for k in ("GFT_TUNE_R", "GFT_TUNE_STAGES", "GFT_TUNE_WARPS", "GFT_PACE_NS"):
+    res.append(((R, S, W, pace, ob), round(frac, 4)))
+for k in ("GFT_TUNE_R", "GFT_TUNE_STAGES", "GFT_TUNE_WARPS", "GFT_PACE_NS", "GFT_FMA_OBUF"):
     os.environ.pop(k, None)
 res.sort(key=lambda r: -r[1])
-print(json.dumps({"spec": spec, "kind": kind, "top": res[:6], "n": len(res)}))
+print(json.dumps({"spec": spec, "kind": kind, "top": res[:8], "n": len(res)}))
