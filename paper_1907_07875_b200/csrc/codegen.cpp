@@ -970,10 +970,14 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
       if (io_split) pre << "#define GFT_IO_SPLIT 1\n";
       if (const char* e = getenv("GFT_TC_TRACE")) if (e[0] == '1') pre << "#define GFT_TRACE 1\n";   // experiments
       if (ws) {
-        // load pacing (kernel_tc3_skeleton.cuh pace_load): 0.9 x the CTA's fair share of HBM
-        // time per tile (read + write of its 128 rows at 6455 GB/s over 148 SMs, the measured
-        // copy roof); GFT_TC_LOAD_PACE_NS overrides (0 disables)
-        int pace = (int)(0.9 * 2.0 * c.tile_bytes() / (6455.0 / 148.0));
+        // load pacing (kernel_tc3_skeleton.cuh pace_load): a fraction of the CTA's fair share of
+        // HBM time per tile (read + write of its 128 rows at 6455 GB/s over 148 SMs, the
+        // measured copy roof) -- 0.9 for the IO-split kernel (64 KiB tiles), 0.83 for the
+        // in-place one (32 KiB tiles at n = 64).  The optimum is sharp: cfg5b 2704 ns 6.31 TB/s
+        // vs 5.94 at 2550 and 6.03 at 2850; right-Haar 32|32 1250 ns 6.34 vs 6.12 at 1352
+        // (tools/r02/pace_confirm.py, profiles/r02/r02_pace_confirm.log).
+        // GFT_TC_LOAD_PACE_NS overrides (0 disables)
+        int pace = (int)((io_split ? 0.9 : 0.83) * 2.0 * c.tile_bytes() / (6455.0 / 148.0));
         if (const char* lp = getenv("GFT_TC_LOAD_PACE_NS")) pace = atoi(lp);
         if (pace > 0) pre << "#define GFT_LOAD_PACE_NS " << pace << "\n";
       }

@@ -68,7 +68,7 @@ for tag, fn in fns:   # cold bursts first (after an idle pause: a hot GPU sits a
     time.sleep(4.0)
     ms = timed(fn, 20)
     out[tag + "_burst_gbs"] = round(nb / ms / 1e6, 1)
-for tag, fn in fns:
+for tag, fn in (fns if secs > 0 else ()):
     t0 = time.perf_counter()
     ms = timed(fn, 20)
     n_it = max(1, int(secs * 1e3 / ms))
