@@ -559,11 +559,20 @@ def main():
     chunk_rows = 1 << 17
     wsb = [torch.empty(4 * chunk_rows * c.n, dtype=torch.float32, device=device) for c in cfgs]
 
+    # one caller stream per graph: the two graphs' transfers pipeline back to back through the
+    # library's shared H2D / kernel / D2H stage streams (no drain bubble between calls); each
+    # graph's inverse still follows its forward (stream order on its own stream)
+    gstreams = [torch.cuda.Stream(device), torch.cuda.Stream(device)]
+
     def e2e_step():
-        for i in range(2):
-            plans[i].execute_host(0, Xh[i], Yh[i], wsb[i], chunk_rows, stream)
-        for i in range(2):
-            plans[i].execute_host(1, Yh[i], Zh[i], wsb[i], chunk_rows, stream)
+        for s in gstreams:
+            s.wait_stream(stream)
+        for d in (0, 1):
+            for i in range(2):
+                plans[i].execute_host(d, Xh[i] if d == 0 else Yh[i], Yh[i] if d == 0 else Zh[i], wsb[i], chunk_rows,
+                                      gstreams[i])
+        for s in gstreams:
+            stream.wait_stream(s)
     e2e_step()
     torch.cuda.synchronize()
     barrier(device)

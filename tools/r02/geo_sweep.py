@@ -45,7 +45,9 @@ plan = gft.Plan.from_config(cfg, dtypes=(dt,), no_cubin_cache=True)
 default = None
 WARPS = tuple(int(w) for w in os.environ.get("SWEEP_WARPS", "4,8,12").split(","))
 OBUFS = tuple(int(w) for w in os.environ.get("SWEEP_OBUF", "0").split(","))
-for R, S, W, pace, ob in itertools.product((1, 2, 4), (2, 3), WARPS, (0, 150), OBUFS):
+PACES = tuple(int(w) for w in os.environ.get("SWEEP_PACE", "0,150").split(","))
+RS = tuple(int(w) for w in os.environ.get("SWEEP_R", "1,2,4").split(","))
+for R, S, W, pace, ob in itertools.product(RS, (2, 3), WARPS, PACES, OBUFS):
     tile = 32 * R * cfg.n * esz
     if W * (S + ob) * tile + W * S * 8 + 1024 > 227 * 1024 or tile > 32768:
         continue
