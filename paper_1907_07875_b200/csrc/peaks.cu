@@ -123,13 +123,18 @@ __global__ void __launch_bounds__(128, 1) tf32_probe(int iters, u32* sink) {
 extern "C" __attribute__((visibility("default"))) int gft_peak_run(int which, int sms, void* stream, double* flops,
                                                                     double* ms) {
   cudaStream_t s = (cudaStream_t)stream;
-  cudaEvent_t e0, e1;
-  cudaError_t err;
-  if ((err = cudaEventCreate(&e0)) != cudaSuccess) return (int)err;
-  if ((err = cudaEventCreate(&e1)) != cudaSuccess) return (int)err;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
   void* buf = nullptr;
-  if ((err = cudaMalloc(&buf, 1 << 16)) != cudaSuccess) return (int)err;
-  if ((err = cudaMemsetAsync(buf, 0, 1 << 16, s)) != cudaSuccess) return (int)err;
+  cudaError_t err = cudaEventCreate(&e0);
+  if (err == cudaSuccess) err = cudaEventCreate(&e1);
+  if (err == cudaSuccess) err = cudaMalloc(&buf, 1 << 16);
+  if (err == cudaSuccess) err = cudaMemsetAsync(buf, 0, 1 << 16, s);
+  if (err != cudaSuccess) {   // release whatever was created
+    if (buf) cudaFree(buf);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    return (int)err;
+  }
   double f = 0.0;
   auto launch = [&](bool count) {
     if (which == 0) {
