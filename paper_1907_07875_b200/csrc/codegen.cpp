@@ -753,6 +753,171 @@ void generate_tc_ws(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_co
   o << "}\n";
 }
 
+// host float -> IEEE half (round to nearest even, subnormals, overflow to inf)
+uint16_t f32_to_f16_host(float f) {
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  const uint32_t sign = (x >> 16) & 0x8000u;
+  const int32_t e = (int32_t)((x >> 23) & 0xff) - 127 + 15;
+  uint32_t m = x & 0x7fffffu;
+  if (((x >> 23) & 0xff) == 0xff) return (uint16_t)(sign | 0x7c00u | (m ? 0x200u : 0u));
+  if (e >= 31) return (uint16_t)(sign | 0x7c00u);
+  if (e <= 0) {   // subnormal half (or zero)
+    if (e < -10) return (uint16_t)sign;
+    m |= 0x800000u;
+    const int shift = 14 - e;
+    uint32_t hm = m >> shift;
+    const uint32_t rem = m & ((1u << shift) - 1), half = 1u << (shift - 1);
+    if (rem > half || (rem == half && (hm & 1u))) ++hm;
+    return (uint16_t)(sign | hm);
+  }
+  uint32_t hm = m >> 13;
+  const uint32_t rem = m & 0x1fffu;
+  uint32_t h = sign | ((uint32_t)e << 10) | hm;
+  if (rem > 0x1000u || (rem == 0x1000u && (hm & 1u))) ++h;   // may carry into the exponent: correct
+  return (uint16_t)h;
+}
+float f16_to_f32_host(uint16_t h) {
+  const uint32_t sign = (uint32_t)(h & 0x8000u) << 16;
+  const uint32_t e = (h >> 10) & 0x1f, m = h & 0x3ffu;
+  float v;
+  if (e == 0) v = std::ldexp((float)m, -24);
+  else if (e == 31) v = m ? NAN : INFINITY;
+  else v = std::ldexp((float)(m | 0x400u), (int)e - 25);
+  uint32_t b;
+  std::memcpy(&b, &v, 4);
+  b |= sign;
+  std::memcpy(&v, &b, 4);
+  return v;
+}
+
+// Warp-specialised IO-split kernel with an fp16x2 split instead of 3xTF32 (GFT_TC_F16=1): every
+// row is scaled by a power of two s = 2^-e that brings its largest tensor-core input into [1, 2)
+// (exact; fp16 range), then x' = h + l with h = x' truncated to 11 significant bits (exactly an
+// fp16) and l = fp16(x' - h); the leaf matrix likewise B = B_h + B_l in fp16.  D = h.B_h + h.B_l
+// + l.B_h as kind::f16 MMAs (K = 16 per instruction, twice the tf32 MAC rate) accumulating in
+// fp32; the drainer multiplies by 2^e.  Half the TMEM bytes of the staged A operand (16-bit
+// h and l), half the B bytes, half the MMA instructions.  Error: |x' - h - l| <= 2^-11 |l| <=
+// 2^-22 |x'| per element, B likewise; the dropped l.B_l term is ~2^-22 relative.
+void generate_tc_ws_f16(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_cols, int d_cols,
+                        std::ostringstream& o) {
+  // ---- B operands: per CTA half (N/2 rows), per leaf, parts h then l; K-major, 128B-swizzled
+  // atoms of 64 fp16 (128 B) x 8 rows; K padded to whole 32-element chunks ----
+  std::vector<uint16_t> B;
+  std::vector<int> boff_h(T.size()), boff_l(T.size()), atom_bytes(T.size());
+  for (int r = 0; r < 2; ++r) {
+    int off = 0;
+    for (size_t ti = 0; ti < T.size(); ++ti) {
+      const TcLeaf& t = T[ti];
+      const Leaf& lf = P.leaves[t.leaf];
+      const int rows = t.np / 2, atoms = (t.kp32 + 63) / 64;
+      atom_bytes[ti] = rows * 128;
+      for (int part = 0; part < 2; ++part) {
+        (part == 0 ? boff_h : boff_l)[ti] = off;
+        for (int a = 0; a < atoms; ++a)
+          for (int n = r * rows; n < (r + 1) * rows; ++n)
+            for (int kk = 64 * a; kk < 64 * a + 64; ++kk) {
+              float v = 0.f;
+              if (n < t.k && kk < t.k) v = (float)leaf_coef(lf, d, n, kk);
+              const uint16_t h = f32_to_f16_host(v);
+              B.push_back(part == 0 ? h : f32_to_f16_host(v - f16_to_f32_host(h)));
+            }
+        off += atoms * rows * 128;
+      }
+    }
+  }
+  const size_t per_cta = B.size() / 2;   // fp16 elements per CTA (even: whole 128 B rows)
+  int nch = 0;
+  for (const TcLeaf& t : T) nch += t.kp32 / 32;
+  o << "#define GFT_F16X2 1\n#define GFT_B_FLOATS " << per_cta / 2 << "\n#define GFT_A_COLS " << a_cols
+    << "\n#define GFT_NCH " << nch << "\n#define GFT_D_BASE " << a_cols << "\n#define GFT_D_COLS " << d_cols
+    << "\n#define GFT_SMALL 0\n";
+  o << "__device__ __align__(16) const unsigned int gft_tcB[2][" << per_cta / 2 << "] = {\n";
+  for (size_t i = 0; i < B.size(); i += 2) {
+    char buf[24];
+    std::snprintf(buf, sizeof buf, "0x%08xu,", (unsigned)B[i] | ((unsigned)B[i + 1] << 16));
+    o << buf << ((i % 16 == 14) ? "\n" : "");
+  }
+  o << "};\n";
+  o << "static __device__ __forceinline__ void st_elem(unsigned char* buf, int row, int col, float v) {\n"
+       "  *reinterpret_cast<float*>(buf + tile_off(row, col)) = v;\n}\n";
+  // ---- stager ----
+  o << "static __device__ __forceinline__ void gft_stage(float (&x)[GFT_N], u32 tm, u32 staged0,\n"
+       "    unsigned char* buf, int row, u32 afree, u32 apar, bool await_a, long long it, int* row_e) {\n";
+  if (d != DIR_INV) emit_units(o, P, "x", false, GFT_F32);
+  if (d == DIR_FILTER && !P.post.empty()) fail(GFT_ERR_COMPILE, "filter plan with right Haar stages");
+  if (d == DIR_INV) emit_post_units(o, P, "x", true, "float");
+  // row scale: e = exponent of the largest |input| of the tensor-core leaves
+  o << "  float m_ = 0.f;\n";
+  for (const TcLeaf& t : T)
+    for (int c = 0; c < t.k; ++c) o << "  m_ = fmaxf(m_, fabsf(x[" << in_idx(P.leaves[t.leaf], d, c) << "]));\n";
+  o << "  const int e_ = row_exponent(m_);\n  *row_e = e_;\n  const float sc_ = exp2_int(-e_);\n";
+  int ch = 0;
+  for (const TcLeaf& t : T) {
+    const Leaf& lf = P.leaves[t.leaf];
+    for (int c0 = 0; c0 < t.kp32; c0 += 32, ++ch) {
+      o << "  if (await_a) { mbar_wait(afree + " << 8 * ch << "u, apar); tc_fence_after(); }\n";
+      o << "  if (row == 0) TR(" << 14 + std::min(ch, 3) << ", it);\n";
+      o << "  { u32 h[16], l[16];\n";
+      for (int q = 0; q < 16; ++q) {
+        const int c = c0 + 2 * q;
+        auto v = [&](int cc) {
+          return cc < t.k ? "x[" + std::to_string(in_idx(lf, d, cc)) + "] * sc_" : std::string("0.f");
+        };
+        o << "  split_f16x2(" << v(c) << ", " << v(c + 1) << ", h[" << q << "], l[" << q << "]);\n";
+      }
+      emit_tmem_st(o, "h", t.hi_col + c0 / 2, 16);
+      emit_tmem_st(o, "l", t.lo_col + c0 / 2, 16);
+      o << "  }\n";
+      o << "  signal_staged(staged0 + " << 8 * ch << "u);\n";
+    }
+  }
+  o << "}\n";
+  // ---- drainer: y = 2^e D ----
+  o << "static __device__ __forceinline__ void gft_drain(float (&y)[GFT_N], u32 tm, const unsigned char* buf, int row,\n"
+       "    int e_) {\n  const float u_ = exp2_int(e_);\n";
+  for (const TcLeaf& t : T) {
+    const Leaf& lf = P.leaves[t.leaf];
+    for (int r0 = 0; r0 < t.k; r0 += 32) {
+      const int w = std::min(32, t.np - r0);
+      o << "  { u32 d[" << w << "];\n";
+      emit_tmem_ld(o, "d", t.d_col + r0, w);
+      for (int r = r0; r < std::min(t.k, r0 + w); ++r)
+        o << "  y[" << out_idx(lf, d, r) << "] = __uint_as_float(d[" << r - r0 << "]) * u_;\n";
+      o << "  }\n";
+    }
+  }
+  o << "}\n";
+  o << "static __device__ __forceinline__ void gft_finish(float (&y)[GFT_N]) {\n";
+  if (d == DIR_FWD) emit_post_units(o, P, "y", false, "float");
+  if (d != DIR_FWD) emit_units(o, P, "y", true, GFT_F32);
+  o << "}\n";
+  // ---- issuer: per chunk (two K = 16 steps), passes h.B_h, h.B_l, l.B_h ----
+  o << "static __device__ __forceinline__ void gft_issue_ws(u32 tA, u32 tD, u32 bsm, u32 staged, u32 spar, u32 afree,\n"
+       "    long long it) {\n";
+  ch = 0;
+  for (size_t ti = 0; ti < T.size(); ++ti) {
+    const TcLeaf& t = T[ti];
+    // kind::f16: D f32 (bit 4), A / B f16 (format 0), N >> 3 at bit 17, M >> 4 at bit 24
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(t.np >> 3) << 17) | (16u << 24);
+    for (int c0 = 0; c0 < t.kp32; c0 += 32, ++ch) {
+      o << "  mbar_wait_acq_cluster(staged + " << 8 * ch << "u, spar); tc_fence_after();\n";
+      o << "  TR(" << 10 + std::min(ch, 3) << ", it);\n";
+      for (int pass = 0; pass < 3; ++pass) {
+        const int acol = pass == 2 ? t.lo_col : t.hi_col;
+        const int boff = pass == 1 ? boff_l[ti] : boff_h[ti];
+        for (int j = c0 / 16; j < c0 / 16 + 2; ++j) {
+          const int bo = boff + (j / 4) * atom_bytes[ti] + (j % 4) * 32;
+          o << "  mma_ts2_f16(tD + " << t.d_col << "u, tA + " << (acol + 8 * j) << "u, smem_desc_sw128(bsm + " << bo
+            << "u), " << idesc << "u, " << ((pass == 0 && j == 0) ? 0 : 1) << "u);\n";
+        }
+      }
+      o << "  tc_commit_pair(afree + " << 8 * ch << "u);\n";
+    }
+  }
+  o << "}\n";
+}
+
 // Dense comparison kernel Y = X W (H7) as a register-tiled GEMM with W in SMEM
 // (kernel_dense_skeleton.cuh), for n = 64 / 128 when a tile ring of >= 2 buffers fits beside
 // W.  Thread tile GFT_TM x 8 (TM = 8 fp32, 4 fp64), 256 compute threads: GFT_BM = 256 TM 8 / n.
@@ -961,7 +1126,32 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
       c.tc_b_bytes = b_bytes;
       c.tc_tmem_cols = tmem_cols;
       std::ostringstream gen;
-      if (ws) generate_tc_ws(P, dir, Tws, ws_a, ws_d, gen);
+      // warp-specialised kernels whose every leaf is on the tensor core: the fp16x2 split
+      // (generate_tc_ws_f16) instead of 3xTF32 -- half the TMEM bytes and MMA instructions;
+      // cfg5b forward 6.46 -> 6.50 TB/s burst and 5.93 -> 6.32 sustained at the power cap, max
+      // per-signal error 9.9e-7 -> 7.2e-7 (tools/r02/gpu_f16_probe.sh).  GFT_TC_F16=0: 3xTF32
+      bool f16 = false;
+      if (ws && Tws.size() == P.leaves.size()) {
+        const char* e16 = getenv("GFT_TC_F16");
+        if (!(e16 && e16[0] == '0')) {
+          int ac = 0, dc = 0;
+          for (auto& t : Tws) { t.hi_col = ac; t.lo_col = ac + t.kp32 / 2; ac += t.kp32; }
+          for (auto& t : Tws) { t.d_col = dc; dc += ru(t.np, 32); }
+          int bb = 0;
+          for (auto& t : Tws) bb += 2 * ((t.kp32 + 63) / 64) * (t.np / 2) * 128;
+          if (ac + 2 * dc <= 512) {
+            f16 = true;
+            ws_a = ac;
+            ws_d = dc;
+            tmem_cols = 32;
+            while (tmem_cols < ac + 2 * dc) tmem_cols *= 2;
+            c.tc_tmem_cols = tmem_cols;
+            c.tc_b_bytes = bb + 1024;   // + the per-row exponents (2 tiles x 128 ints)
+          }
+        }
+      }
+      if (f16) generate_tc_ws_f16(P, dir, Tws, ws_a, ws_d, gen);
+      else if (ws) generate_tc_ws(P, dir, Tws, ws_a, ws_d, gen);
       else generate_tc(P, dir, T, pair, gen);
       std::ostringstream pre;
       pre << "#define GFT_N " << c.n << "\n#define GFT_STAGES " << c.stages << "\n#define GFT_TMEM_COLS "

@@ -145,6 +145,30 @@ static __device__ __forceinline__ void mma_ts2(u32 d, u32 a, u64 bdesc, u32 ides
                "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p; }"
                :: "r"(d), "r"(a), "l"(bdesc), "r"(idesc), "r"(acc) : "memory");
 }
+// kind::f16 (fp16 A in TMEM, fp16 B in SMEM, f32 accumulate), M = 256, K = 16
+static __device__ __forceinline__ void mma_ts2_f16(u32 d, u32 a, u64 bdesc, u32 idesc, u32 acc) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+               "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p; }"
+               :: "r"(d), "r"(a), "l"(bdesc), "r"(idesc), "r"(acc) : "memory");
+}
+// fp16x2 split of two scaled inputs (GFT_F16X2): h = the 11 leading significant bits (exactly an
+// fp16 for |x| >= 2^-14), l = fp16(x - h); packed low = a, high = b
+static __device__ __forceinline__ void split_f16x2(float a, float b, u32& h, u32& l) {
+  const float ha = __uint_as_float(__float_as_uint(a) & 0xffffe000u);
+  const float hb = __uint_as_float(__float_as_uint(b) & 0xffffe000u);
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(hb), "f"(ha));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(b - hb), "f"(a - ha));
+}
+// 2^k for k in [-149, 127]
+static __device__ __forceinline__ float exp2_int(int k) {
+  return k >= -126 ? __uint_as_float((u32)(k + 127) << 23) : __uint_as_float(1u << (k + 149));
+}
+// floor(log2 m) clamped to [-126, 127] (0 for m = 0): the row scale 2^-e brings the row's largest
+// tensor-core input into [1, 2) (rows whose largest element is an fp32 subnormal keep 2^126)
+static __device__ __forceinline__ int row_exponent(float m) {
+  const int eb = (int)((__float_as_uint(m) >> 23) & 0xffu);
+  return eb == 0 ? (m == 0.f ? 0 : -126) : (eb == 255 ? 127 : eb - 127);
+}
 // K-major, 128B-swizzled operand: 8-row core-matrix groups 1024 B apart (SBO)
 static __device__ __forceinline__ u64 smem_desc_sw128(u32 saddr) {
   return (u64)((saddr >> 4) & 0x3FFFu) | ((u64)(16u >> 4) << 16) | ((u64)(1024u >> 4) << 32) |
@@ -217,7 +241,13 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   unsigned char* stages = smem;
   unsigned char* outbuf = smem + GFT_STAGES * GFT_TILE_BYTES;
   unsigned char* bsm = smem + (GFT_STAGES + GFT_IO_SPLIT) * GFT_TILE_BYTES;   // this CTA's half of B
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(bsm + GFT_B_FLOATS * 4);
+#ifndef GFT_F16X2
+#define GFT_F16X2 0
+#endif
+  // GFT_F16X2: per-row exponents of the two tiles in flight between stager and drainer
+  int* row_e = reinterpret_cast<int*>(bsm + GFT_B_FLOATS * 4);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(bsm + GFT_B_FLOATS * 4 + (GFT_F16X2 ? 1024 : 0));
+  (void)row_e;
   // bars: full[S], done[S] (= input free when IO-split), rows[S], then the ones below
   // (staged alternates per tile parity, so a stager a tile ahead can never complete a phase
   // the issuer has not yet observed)
@@ -234,7 +264,9 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   // chunk done, multicast commit)
   unsigned long long* b_staged = bars + 3 * GFT_STAGES + 4 + 2 * GFT_NBOX;
   unsigned long long* b_afree = b_staged + 2 * GFT_NCH;
-  u32* tmem_slot = reinterpret_cast<u32*>(b_afree + GFT_NCH);
+  unsigned long long* b_erdy = b_afree + GFT_NCH;    // [2] row exponents of tile t%2 written (4 stager warps)
+  unsigned long long* b_efree = b_erdy + 2;          // [2] ... read (4 drainer warps)
+  u32* tmem_slot = reinterpret_cast<u32*>(b_efree + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const u32 rank = cluster_rank();
   const long long npairs = (batch + 2 * GFT_TILE_ROWS - 1) / (2 * GFT_TILE_ROWS);
@@ -260,6 +292,10 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
     }
     for (int c = 0; c < 2 * GFT_NCH; ++c) mbar_init(smem_u32(&b_staged[c]), 8);
     for (int c = 0; c < GFT_NCH; ++c) mbar_init(smem_u32(&b_afree[c]), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&b_erdy[b]), 4);
+      mbar_init(smem_u32(&b_efree[b]), 4);
+    }
     for (int b = 0; b < GFT_NBOX; ++b) {
       mbar_init(smem_u32(&b_boxrdy[b]), 4);
       mbar_init(smem_u32(&b_boxfree[b]), 1);
@@ -399,7 +435,15 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       // before writing the A columns: the MMAs that last read this A buffer (tile t-1, or
       // t-2 with two buffers) are done
       // chunk c of A is rewritten once the MMAs of tile it-1 on it are done (a_free[c])
+#if GFT_F16X2
+      if (it >= 2) mbar_wait(smem_u32(&b_efree[it & 1]), (u32)(((it >> 1) - 1) & 1));   // drainer of it-2 read them
+      gft_stage(x, tm_a, staged0[it & 1], buf, tid, smem_u32(b_afree), (u32)((it - 1) & 1), it >= 1, it,
+                &row_e[(it & 1) * 128 + tid]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&b_erdy[it & 1]));
+#else
       gft_stage(x, tm_a, staged0[it & 1], buf, tid, smem_u32(b_afree), (u32)((it - 1) & 1), it >= 1, it);
+#endif
       if (tid == 0) TR(3, it);
 #if GFT_SMALL
       __syncwarp();
@@ -428,7 +472,15 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       unsigned char* buf = stages + s * GFT_TILE_BYTES;
 #endif
       float y[GFT_N];
+#if GFT_F16X2
+      mbar_wait(smem_u32(&b_erdy[b]), (u32)((it >> 1) & 1));
+      const int e_row = row_e[b * 128 + row];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&b_efree[b]));
+      gft_drain(y, tmem + lane_off + (u32)(GFT_D_BASE + b * GFT_D_COLS), buf, row, e_row);
+#else
       gft_drain(y, tmem + lane_off + (u32)(GFT_D_BASE + b * GFT_D_COLS), buf, row);
+#endif
       // D[b] read (tcgen05.ld waited inside gft_drain): let the issuer reuse it
       tc_fence_before();
       __syncwarp();

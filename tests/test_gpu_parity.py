@@ -227,8 +227,10 @@ def test_tensor_core_single_cta_and_pair_variants_agree(monkeypatch):
         check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
         assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
     ref = single.forward(Xd).cpu().numpy()
-    for plan in (ws, pair):
-        assert oracle.relative_error(plan.forward(Xd).cpu().numpy(), ref).max() < 1e-6
+    # 3xTF32 variants agree to ~1e-7; the fp16x2 warp-specialised kernel differs by its own
+    # (smaller) rounding, each within ~1e-6 of the oracle
+    assert oracle.relative_error(pair.forward(Xd).cpu().numpy(), ref).max() < 1e-6
+    assert oracle.relative_error(ws.forward(Xd).cpu().numpy(), ref).max() < 3e-6
 
 
 @pytest.mark.parametrize("inverse_small_leaf", [False, True])
@@ -259,8 +261,11 @@ def test_tensor_core_kernel_variants_agree(monkeypatch, inverse_small_leaf):
         check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), 1e-5)
         assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2e-5
         outs.append(Y.cpu().numpy())
-    for o in outs[1:]:
-        assert oracle.relative_error(o, outs[0]).max() < 1e-6
+    # the 3xTF32 kernels agree to ~1e-7; the default warp-specialised kernel (fp16x2 split when
+    # every leaf is on the tensor core) by its own rounding, each within ~1e-6 of the oracle
+    for o in outs[2:]:
+        assert oracle.relative_error(o, outs[1]).max() < 1e-6
+    assert oracle.relative_error(outs[0], outs[1]).max() < 3e-6
 
 
 @pytest.mark.parametrize("name", ["cfg3", "cfg4"])
@@ -442,6 +447,7 @@ def test_tensor_core_io_split_kernel(batch):
     assert "tc3s_" in plan.kernel_name(G.K_FAST_FWD) and "tc3s_" in plan.kernel_name(G.K_FAST_INV)
     src = plan.kernel_source(G.K_FAST_FWD, "f32")
     assert "#define GFT_IO_SPLIT 1" in src and "#define GFT_LOAD_PACE_NS" in src and "#define GFT_NCH 4" in src
+    assert "#define GFT_F16X2 1" in src
     lam_o, U_o = oracle_basis("cfg5b")
     X = workloads.signals(cfg, batch=batch, dtype="f32")
     Y = plan.forward(X.cuda())
@@ -642,3 +648,42 @@ def test_fma_io_split_outputs(monkeypatch, name, dtype, obuf, batch):
     assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL[dtype]
     Zo = oracle.graph_filter(X.numpy().astype(np.float64), U_o, np.exp(-lam_o))
     assert oracle.relative_error(Z.cpu().numpy(), Zo).max() <= 4 * TOL[dtype]
+
+
+@pytest.mark.parametrize("name", ["cfg5b", "rh0"])
+def test_tensor_core_f16x2_extreme_magnitudes(name):
+    """The fp16x2 split of the warp-specialised kernels scales every row by a power of two
+    (its largest tensor-core input into [1, 2)) before splitting into fp16 parts: rows spanning
+    the fp32 range (1e-30 .. 1e30), rows with one huge and many tiny elements, all-zero rows and
+    mixed signs all stay within the per-signal 1e-5 bound, forward and round trip, against the
+    oracle (fp64)."""
+    if name == "cfg5b":
+        cfg = workloads.config("cfg5b")
+        plan = G.Plan.from_config(cfg, dtypes=("f32",))
+        n = cfg.n
+        L = oracle.laplacian(n, cfg.src, cfg.dst, cfg.w, cfg.self_loops)
+    else:
+        n, s_, d_, w_, loops, norm = workloads.right_haar_bench_graph(workloads.RIGHT_HAAR_BENCH_CASES[0])
+        plan = G.Plan(n, s_, d_, w_, loops, dtypes=("f32",), normalized=norm)
+        L = oracle.laplacian(n, s_, d_, w_, loops)
+        if norm:
+            L = oracle.normalized_laplacian(L)
+    assert "#define GFT_F16X2 1" in plan.kernel_source(G.K_FAST_FWD, "f32")
+    lam_o, U_o = oracle.gft_basis(L)
+    g = torch.Generator().manual_seed(11)
+    base = torch.randn(64, n, generator=g)
+    rows = [base[i] * (10.0 ** e) for i, e in enumerate([-30, -20, -10, -5, 0, 5, 10, 20, 30])]
+    spike = torch.randn(n, generator=g) * 1e-6
+    spike[3] = 1e4
+    rows += [spike, -spike, base[20] * torch.logspace(-8, 8, n), torch.zeros(n)]
+    rows += [base[30 + i] for i in range(10)]
+    X = torch.stack(rows).float()
+    X = torch.cat([X, torch.randn(1000, n, generator=g)])   # + full pair tiles and a ragged tail
+    Y = plan.forward(X.cuda())
+    Xr = plan.inverse(Y)
+    torch.cuda.synchronize()
+    Yh, Xn = Y.cpu().numpy().astype(np.float64), X.numpy().astype(np.float64)
+    nz = np.abs(Xn).sum(axis=1) > 0
+    assert np.all(Yh[~nz] == 0)                                # zero rows stay exactly zero
+    check_forward(Yh[nz], Xn[nz], lam_o, U_o, plan.basis(), 1e-5)
+    assert oracle.relative_error(Xr.cpu().numpy()[nz], Xn[nz]).max() <= 2e-5
