@@ -920,17 +920,19 @@ void generate_tc_ws_f16(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int 
 
 // Dense comparison kernel Y = X W (H7) as a register-tiled GEMM with W in SMEM
 // (kernel_dense_skeleton.cuh), for n = 64 / 128 when a tile ring of >= 2 buffers fits beside
-// W.  Thread tile GFT_TM x 8 (TM = 8 fp32, 4 fp64), 256 compute threads: GFT_BM = 256 TM 8 / n.
+// W.  Thread tile GFT_TM x 8 (TM = 6 fp32, 4 fp64), 256 compute threads: GFT_BM = 256 TM 8 / n.
 bool dense_gemm_geometry(int n, int dtype, KernelCfg& c) {
   if (n != 64 && n != 128) return false;
   if (const char* e = getenv("GFT_NO_DENSE_GEMM")) if (e[0] == '1') return false;   // ablation
   auto env_int = [](const char* k, int v) { const char* e = getenv(k); return (e && *e) ? atoi(e) : v; };
   const int elem = dtype == GFT_F64 ? 8 : 4;
-  const int tm = env_int("GFT_DG_TM", dtype == GFT_F64 ? 4 : 8), tn = env_int("GFT_DG_TN", 8);
+  const int tm = env_int("GFT_DG_TM", dtype == GFT_F64 ? 4 : 6), tn = env_int("GFT_DG_TN", 8);
   const int threads = env_int("GFT_DG_THREADS", 256);
   if (tm < 1 || tn < 16 / elem || tn % (16 / elem) || n % tn || (threads != 128 && threads != 256)) return false;
   const int bm = threads * tm * tn / n;
   if (bm > 256 || bm % 8 || (bm / tm) < 8 || (bm / tm) * (n / tn) != threads) return false;
+  // a warp owns whole rows (all n / tn column threads, kernel_dense_skeleton.cuh)
+  if (n / tn > 32 || 32 % (n / tn) || (bm / tm) % (32 / (n / tn))) return false;
   KernelCfg g;
   g.n = n;
   g.elem = elem;
@@ -970,6 +972,12 @@ void generate_dense_gemm(const Plan& P, int kind, int dtype, Kernel& k) {
   pre << "#define GFT_N " << n << "\n#define GFT_BM " << c.bm << "\n#define GFT_TM " << c.R << "\n#define GFT_TN " << c.pack
       << "\n#define GFT_THREADS " << 32 * c.warps << "\n#define GFT_STAGES " << c.stages << "\n";
   if (const char* e = getenv("GFT_DG_PREFETCH")) pre << "#define GFT_DG_PREFETCH " << atoi(e) << "\n";   // experiment
+  {   // k-loop unroll 8 (measured, profiles/r02/r02_dense_probe8.log)
+    const char* e = getenv("GFT_DG_UNROLL");
+    pre << "#define GFT_DG_UNROLL " << ((e && *e) ? atoi(e) : 8) << "\n";
+  }
+  if (const char* e = getenv("GFT_DG_WY")) pre << "#define GFT_DG_WY " << atoi(e) << "\n";   // experiment
+  if (const char* e = getenv("GFT_DG_FFMA2")) pre << "#define GFT_DG_FFMA2 " << atoi(e) << "\n";   // ablation
   const std::string skel(kSkeletonDense);
   const std::string marker = "// @@GFT_GENERATED@@";
   const size_t at = skel.find(marker);

@@ -33,6 +33,20 @@ static __device__ __forceinline__ double fma_(double a, double b, double c) { re
 typedef float4 vec_t;
 static __device__ __forceinline__ float fma_(float a, float b, float c) { return fmaf(a, b, c); }
 #endif
+// fp32: the outer product runs on the packed FFMA2 (fma.rn.f32x2, sm_100): one instruction does
+// acc[i][j..j+1] += a[i] * b[j..j+1] with a[i] broadcast to both halves (ptxas folds the
+// {a, a} pack into a .F32 scalar operand) -- half the issue slots of per-lane FFMAs for the same
+// register operands; each lane is the same IEEE fma.rn, so results are bit-identical.
+#ifndef GFT_DG_FFMA2
+#if GFT_ELEM_IS_DOUBLE
+#define GFT_DG_FFMA2 0
+#else
+#define GFT_DG_FFMA2 1
+#endif
+#endif
+static __device__ __forceinline__ void ffma2_bcast(u64& d, float a, u64 b) {
+  asm("{ .reg .b64 t; mov.b64 t, {%1, %1}; fma.rn.f32x2 %0, t, %2, %0; }" : "+l"(d) : "f"(a), "l"(b));
+}
 #define GFT_NG (GFT_TN / GFT_VEC)
 #define GFT_BOXC (GFT_VEC * 8)
 #define GFT_BOX_BYTES (GFT_BM * 128)
@@ -41,6 +55,13 @@ static __device__ __forceinline__ float fma_(float a, float b, float c) { return
 #define GFT_TY (GFT_BM / GFT_TM)
 #if GFT_TY * (GFT_N / GFT_TN) != GFT_THREADS || GFT_TY % 8 != 0
 #error "dense tile geometry must match GFT_THREADS (and GFT_BM / GFT_TM % 8 == 0)"
+#endif
+#ifndef GFT_DG_WY   // default: a warp owns whole rows (all GFT_N / GFT_TN column threads)
+#define GFT_DG_WY (32 / (GFT_N / GFT_TN))
+#endif
+#define GFT_DG_WX (32 / GFT_DG_WY)
+#if GFT_TY % GFT_DG_WY != 0 || (GFT_N / GFT_TN) % GFT_DG_WX != 0 || GFT_DG_WY * GFT_DG_WX != 32
+#error "dense warp shape must tile the thread grid"
 #endif
 
 static __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
@@ -152,7 +173,11 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   }
 
   // ---------------- compute: GFT_TM x GFT_TN outputs per thread ----------------
-  const int ty = tid % GFT_TY, tx = tid / GFT_TY;
+  // warp shape: GFT_DG_WY row-threads x GFT_DG_WX column-threads.  WY = 8 makes each X load one
+  // 128-B wavefront (8 swizzled rows, broadcast to the WX column threads) and each W load WX
+  // distinct 16-B chunks (one wavefront) instead of 32 rows x 1 column (4 wavefronts per X load)
+  const int ty = (warp % (GFT_TY / GFT_DG_WY)) * GFT_DG_WY + lane % GFT_DG_WY;
+  const int tx = (warp / (GFT_TY / GFT_DG_WY)) * GFT_DG_WX + lane / GFT_DG_WY;
   // rows ty + i*GFT_TY share (row & 7) (GFT_TY % 8 == 0), so the 128B-swizzle term of every X
   // address is one per-thread constant: addr = row_i * 128 + box(kc) + ((kc*elem % 128) ^ sw)
   const u32 sw = (u32)(ty & 7) << 4;
@@ -164,11 +189,19 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
     mbar_wait(smem_u32(&full[s]), (u32)((it / GFT_STAGES) & 1));
     unsigned char* buf = stages + s * GFT_TILE_BYTES;
     const unsigned char* xrow = buf + ty * 128;
+#if GFT_DG_FFMA2
+    u64 acc2[GFT_TM][GFT_TN / 2];   // column pairs (j, j+1) as one f32x2 register pair
+#pragma unroll
+    for (int i = 0; i < GFT_TM; ++i)
+#pragma unroll
+      for (int j = 0; j < GFT_TN / 2; ++j) acc2[i][j] = 0ull;
+#else
     elem_t acc[GFT_TM][GFT_TN];
 #pragma unroll
     for (int i = 0; i < GFT_TM; ++i)
 #pragma unroll
       for (int j = 0; j < GFT_TN; ++j) acc[i][j] = (elem_t)0;
+#endif
 #ifndef GFT_DG_PREFETCH
 #define GFT_DG_PREFETCH 0
 #endif
@@ -178,7 +211,11 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
     for (int i = 0; i < GFT_TM; ++i)
       an[i] = *reinterpret_cast<const vec_t*>(xrow + sw + i * GFT_TY * 128);
 #endif
-#pragma unroll 2
+#ifndef GFT_DG_UNROLL
+#define GFT_DG_UNROLL 2
+#endif
+    constexpr int kUnroll = GFT_DG_UNROLL;   // (#pragma unroll does not macro-expand under nvcc)
+#pragma unroll kUnroll
     for (int kc = 0; kc < GFT_N; kc += GFT_VEC) {
       elem_t a[GFT_TM][GFT_VEC];
 #if GFT_DG_PREFETCH
@@ -207,6 +244,19 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
 #endif
 #pragma unroll
       for (int q = 0; q < GFT_VEC; ++q) {
+#if GFT_DG_FFMA2
+        u64 b2[GFT_TN / 2];
+#pragma unroll
+        for (int j = 0; j < GFT_NG; ++j) {
+          const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(wrow + (kc + q) * GFT_N + j * (GFT_N / GFT_NG));
+          b2[2 * j] = v.x;
+          b2[2 * j + 1] = v.y;
+        }
+#pragma unroll
+        for (int i = 0; i < GFT_TM; ++i)
+#pragma unroll
+          for (int j = 0; j < GFT_TN / 2; ++j) ffma2_bcast(acc2[i][j], a[i][q], b2[j]);
+#else
         elem_t b[GFT_TN];
 #pragma unroll
         for (int j = 0; j < GFT_NG; ++j) {
@@ -219,18 +269,28 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
         for (int i = 0; i < GFT_TM; ++i)
 #pragma unroll
           for (int j = 0; j < GFT_TN; ++j) acc[i][j] = fma_(a[i][q], b[j], acc[i][j]);
+#endif
       }
     }
+#if GFT_DG_WX == GFT_N / GFT_TN
+    __syncwarp();    // this warp owns whole rows (all column threads): overwrite them in place
+#else
     compute_bar();   // every compute thread is done reading this tile: overwrite it in place
+#endif
 #pragma unroll
     for (int i = 0; i < GFT_TM; ++i)
 #pragma unroll
       for (int j = 0; j < GFT_NG; ++j) {
+#if GFT_DG_FFMA2
+        *reinterpret_cast<ulonglong2*>(buf + tile_off(ty + i * GFT_TY, tx * GFT_VEC + j * (GFT_N / GFT_NG))) =
+            make_ulonglong2(acc2[i][j * 2], acc2[i][j * 2 + 1]);
+#else
         vec_t v;
         elem_t* pv = reinterpret_cast<elem_t*>(&v);
 #pragma unroll
         for (int e = 0; e < GFT_VEC; ++e) pv[e] = acc[i][j * GFT_VEC + e];
         *reinterpret_cast<vec_t*>(buf + tile_off(ty + i * GFT_TY, tx * GFT_VEC + j * (GFT_N / GFT_NG))) = v;
+#endif
       }
     fence_proxy_async();
     __syncwarp();

@@ -9,13 +9,15 @@
 //   FFMA : 16 independent fp32 FMA chains per thread (multiplier / addend are kernel
 //          parameters: the constant-bank operand form the generated kernels' immediates use),
 //          1 FMA = 2 flop
-//   FFMA_REG : the same with every operand in a register (the register-tiled dense GEMM's form)
+//   FFMA_REG : the same with every operand in a register
+//   FFMA2 : packed fma.rn.f32x2 with register operands, one multiplicand a scalar broadcast to
+//          both halves (the register-tiled dense GEMM's form), 1 FFMA2 = 4 flop
 //   DFMA : the same in fp64
 //   TF32 : tcgen05.mma.cta_group::1.kind::tf32, M = 128, N = 256, K = 8, A from TMEM, B from
 //          SMEM (the TS form the GFT's tensor-core leaves use), one issuing thread per SM,
 //          back to back into one TMEM accumulator; 1 MAC = 2 flop.
 // C ABI (plain pointers; 0 = ok, otherwise a cudaError_t value):
-//   int gft_peak_run(int which /*0 ffma, 1 dfma, 2 tf32, 3 ffma_reg*/, int sms, void* stream,
+//   int gft_peak_run(int which /*0 ffma, 1 dfma, 2 tf32, 3 ffma_reg, 4 ffma2*/, int sms, void* stream,
 //                    double* flops, double* ms);
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -61,6 +63,33 @@ __global__ void __launch_bounds__(256) ffma_reg_probe(float* out, const float* c
 #pragma unroll
   for (int i = 0; i < CHAINS; ++i) s += acc[i];
   if (s == -12345.0f) out[blockIdx.x] = s;
+}
+
+// packed FFMA2 (fma.rn.f32x2, sm_100) in the dense GEMM's outer-product form: a register-pair
+// accumulator, a register-pair multiplicand and a scalar register broadcast to both halves;
+// 1 FFMA2 = 2 FMA = 4 flop
+__global__ void __launch_bounds__(256) ffma2_probe(float* out, const float* coef, int iters) {
+  u64 acc[CHAINS], b[4];
+  float a[4];
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i) acc[i] = ((u64)(threadIdx.x + i) << 32) | (u64)(threadIdx.x * 3 + i);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    a[i] = coef[i];
+    b[i] = reinterpret_cast<const u64*>(coef)[4 + i];
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+#pragma unroll
+      for (int i = 0; i < CHAINS; ++i)
+        asm("{ .reg .b64 t; mov.b64 t, {%1, %1}; fma.rn.f32x2 %0, t, %2, %0; }"
+            : "+l"(acc[i]) : "f"(a[(i + k) & 3]), "l"(b[(i >> 2) & 3]));
+  }
+  u64 s = 0;
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i) s ^= acc[i];
+  if (s == 0x123456789ull) out[blockIdx.x] = (float)s;
 }
 
 static __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
@@ -149,6 +178,10 @@ extern "C" __attribute__((visibility("default"))) int gft_peak_run(int which, in
       const int blocks = sms * 8, iters = 2048;
       ffma_reg_probe<<<blocks, 256, 0, s>>>((float*)buf, (const float*)buf + 1024, iters);
       if (count) f = 2.0 * blocks * 256.0 * iters * 16.0 * CHAINS;
+    } else if (which == 4) {
+      const int blocks = sms * 8, iters = 2048;
+      ffma2_probe<<<blocks, 256, 0, s>>>((float*)buf, (const float*)buf + 1024, iters);
+      if (count) f = 4.0 * blocks * 256.0 * iters * 16.0 * CHAINS;
     } else {
       const int iters = 2048;
       tf32_probe<<<sms, 128, 0, s>>>(iters, (u32*)buf);

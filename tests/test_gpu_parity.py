@@ -111,6 +111,19 @@ def test_dense_kernel_vs_oracle(name, dtype):
     assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL[dtype]
 
 
+@pytest.mark.parametrize("batch", [1, 95, 96, 97, 127, 129, 191, 193, 257])
+@pytest.mark.parametrize("name,dtype", [("cfg5a", "f32"), ("cfg5b", "f32"), ("cfg4", "f64")])
+def test_dense_gemm_ragged_tiles(name, dtype, batch):
+    """Register-tiled dense GEMM (tile rows 96 / 192 / 128): partial first and last tiles."""
+    cfg, X = roundtrip_inputs(name, batch, dtype)
+    plan = plan_for(name, dtype)
+    assert "dgfwd" in plan.kernel_name(G.K_DENSE_FWD, dtype)
+    lam_o, U_o = oracle_basis(name)
+    Y = plan.dense_forward(X.cuda())
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), TOL[dtype])
+
+
 @pytest.mark.parametrize("name", ["cfg4", "cfg5b"])
 def test_dense_tensor_core_kernel_vs_oracle(name):
     """GFT_FLAG_DENSE_TC: dense U^T x as one tcgen05 3xTF32 leaf."""

@@ -15,3 +15,5 @@ def test_peak_probes_plausible():
     assert 25.0 < p["ffma_reg_tflops"] <= p["ffma_tflops"] * 1.05
     assert 15.0 < p["dfma_tflops"] < 45.0
     assert 600.0 < p["tf32_tflops"] < 1400.0         # dense tcgen05 kind::tf32 ~1.1 PFLOP/s
+    assert 25.0 < p["ffma2_tflops"] < 90.0           # packed fma.rn.f32x2, register operands
+    assert p["fp32_tflops"] == max(p["ffma_tflops"], p["ffma2_tflops"])
