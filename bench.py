@@ -13,7 +13,8 @@ n x n matrix multiplication" (§VI-A).
 
 The LAST stdout line is the headline JSON (kept under 2 KiB: the driver reads a bounded
 tail).  `--tables PATH` additionally writes the per-config side tables (every BASELINE
-config's fast / dense / cuBLAS / filter kernels, right-Haar plans) to PATH as JSON.
+config's fast / dense / cuBLAS / filter kernels, right-Haar plans, and the sustained energy
+per signal of the headline step vs each dense comparison) to PATH as JSON.
 """
 from __future__ import annotations
 
@@ -104,6 +105,15 @@ class ClockSampler:
         if self.ok:
             self._stop.set()
             self.th.join()
+
+    def energy_mj(self):
+        """NVML total energy since driver load (mJ), or None."""
+        if not self.ok:
+            return None
+        try:
+            return float(self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h))
+        except Exception:
+            return None
 
     def summary(self, t0, t1):
         if not self.ok:
@@ -283,7 +293,75 @@ def right_haar_table(args, stream, hbm, device):
     return rows
 
 
+def energy_table(arms, signals_per_step, stream, sampler, seconds):
+    """Sustained throughput and energy per signal of the headline step (fast GFT) against the
+    dense U^T x comparisons on the same inputs, each run back to back for `seconds` at the
+    power cap (the paper's premise: one graph, many transforms).  Energy from
+    NVML's total-energy counter around each window; the fast arm runs first and last (drift)."""
+    import torch
+    rows = []
+    order = list(arms) + [list(arms)[0]]
+    for name in order:
+        fn = arms[name]
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0 = sampler.energy_mj()
+        w0 = time.perf_counter()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        n, tot = 0, 0.0
+        while tot < seconds * 1e3:
+            for _ in range(20):
+                fn()
+            n += 20
+            b.record(stream)
+            b.synchronize()
+            tot = a.elapsed_time(b)
+        w1 = time.perf_counter()
+        e1 = sampler.energy_mj()
+        c = sampler.summary(w0, w1)
+        ms = tot / n
+        row = {"arm": name, "seconds": round(tot / 1e3, 2), "ms_per_step": round(ms, 5),
+               "signals_per_s": signals_per_step / (ms * 1e-3), "sm_mhz": c["sm_mhz"], "power_w": c["power_w"],
+               "reasons": c["reasons"]}
+        if e0 is not None and e1 is not None:
+            row["avg_power_w"] = round((e1 - e0) / 1e3 / (w1 - w0), 1)
+            row["nj_per_signal"] = round((e1 - e0) * 1e6 / (n * signals_per_step), 3)
+        rows.append(row)
+    return rows
+
+
 # ------------------------------------------------------------------------------ helpers
+def _round_sig(v, sig=6):
+    if isinstance(v, float):
+        return float("%.*g" % (sig, v))
+    if isinstance(v, dict):
+        return {k: _round_sig(x, sig) for k, x in v.items()}
+    if isinstance(v, list):
+        return [_round_sig(x, sig) for x in v]
+    return v
+
+
+def headline_line(out, limit=2000):
+    """The last stdout line: floats to 6 significant digits (the top-level value and
+    ms_per_step keep full precision), then -- only if still over `limit` bytes, so that the
+    line survives a bounded stdout tail -- the least important keys are dropped in order."""
+    top = {k: out[k] for k in ("value", "ms_per_step") if k in out}
+    out = _round_sig(out)
+    out.update(top)
+    line = json.dumps(out, separators=(",", ":"))
+    for path in (("peaks_tflops",), ("kernels", "share"), ("cpu_baseline", "sample"), ("kernels",)):
+        if len(line) <= limit:
+            break
+        d = out
+        for k in path[:-1]:
+            d = d.get(k, {})
+        d.pop(path[-1], None)
+        line = json.dumps(out, separators=(",", ":"))
+    return line
+
+
 def pcie_roof(device):
     """Pinned-host copy bandwidth of this box (256 MiB), each direction while both run
     concurrently -- the roof of the e2e path."""
@@ -393,7 +471,9 @@ def main():
     ap.add_argument("--sustain-s", type=float, default=2.0, help="seconds of the sustained-load arm (0: skip)")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle CPU timing")
     ap.add_argument("--ref-rows", type=int, default=1 << 17, help="oracle sample rows per graph")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=2, help="steps per e2e round")
+    ap.add_argument("--e2e-rounds", type=int, default=5, help="e2e rounds (the median is reported)")
+    ap.add_argument("--energy-s", type=float, default=2.0, help="seconds per arm of the energy side table")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -518,41 +598,65 @@ def main():
                "fast_vs_best_dense": round(min(dense.values()) / ms_step, 3),
                "fma_dense_frac": round(dense_flops / (dense["fma"] * 1e-3) / (peaks["fp32_tflops"] * 1e12), 4),
                "plan_create_and_load_ms": round(plan_ms, 1)}
-    for p in dplans:
-        p.close()
 
     # ---- side tables (file only) ----------------------------------------------------------
     if args.tables and rank == 0 and ws == 1:
+        arms = {"fast": step,
+                "dense_tc": lambda: [(dplans[i].dense_forward(X[i], Y[i], stream),
+                                      dplans[i].dense_inverse(Y[i], Z[i], stream)) for i in range(2)],
+                "dense_fma": lambda: [(plans[i].dense_forward(X[i], Y[i], stream),
+                                       plans[i].dense_inverse(Y[i], Z[i], stream)) for i in range(2)],
+                "cublas_tf32_off": lambda: [(torch.matmul(X[i], Us[i], out=Y[i]),
+                                             torch.matmul(Y[i], Us[i].t(), out=Z[i])) for i in range(2)]}
+        tf32 = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
         tables = {"hbm_peak_gbs": hbm, "compute_peaks": peaks,
+                  "energy": energy_table(arms, B, stream, sampler, args.energy_s),
                   "configs": config_table(args, stream, hbm, device, peaks),
                   "right_haar": right_haar_table(args, stream, hbm, device)}
+        torch.backends.cuda.matmul.allow_tf32 = tf32
         os.makedirs(os.path.dirname(os.path.abspath(args.tables)), exist_ok=True)
         with open(args.tables, "w") as f:
             json.dump(tables, f, indent=1)
 
     # ---- sustained load: >= sustain_s seconds of back-to-back steps at the power cap (after
-    # the dense comparisons: a hot GPU sits at a capped clock for a while) ------------------
+    # the dense comparisons: a hot GPU sits at a capped clock for a while), then the same for
+    # the tcgen05 dense step -- the fast transform's fewer operations show as energy per signal
+    # and as a higher capped clock (one graph, many transforms) -----------------
     sustained = None
     if args.sustain_s > 0:
-        chunk = max(1, int(200.0 / ms_step))   # ~0.2 s of steps per event pair
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        tot_ms, nsteps = 0.0, 0
-        s0 = time.perf_counter()
-        a.record(stream)
-        while tot_ms < args.sustain_s * 1e3:
-            for _ in range(chunk):
-                step()
-            nsteps += chunk
-            b.record(stream)
-            b.synchronize()
-            tot_ms = a.elapsed_time(b)
-        s1 = time.perf_counter()
-        sms = max_over_ranks(tot_ms / nsteps, device)
-        sc = sampler.summary(s0, s1)
+        def sustain(fn, ms_hint):
+            chunk = max(1, int(200.0 / ms_hint))   # ~0.2 s of steps per event pair
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            tot_ms, nsteps = 0.0, 0
+            e0 = sampler.energy_mj()
+            s0 = time.perf_counter()
+            a.record(stream)
+            while tot_ms < args.sustain_s * 1e3:
+                for _ in range(chunk):
+                    fn()
+                nsteps += chunk
+                b.record(stream)
+                b.synchronize()
+                tot_ms = a.elapsed_time(b)
+            s1 = time.perf_counter()
+            e1 = sampler.energy_mj()
+            sms = max_over_ranks(tot_ms / nsteps, device)
+            nj = None if e0 is None or e1 is None else round((e1 - e0) * 1e6 / (nsteps * B), 1)
+            return tot_ms, sms, sampler.summary(s0, s1), nj
+        tot_ms, sms, sc, nj = sustain(step, ms_step)
         sustained = {"seconds": round(tot_ms / 1e3, 2), "ms_per_step": round(sms, 5),
                      "value": B * ws / (sms * 1e-3),
                      "dominant_frac": round(nbytes[di] / (sms * share[dom] * 1e-3) / 1e9 / hbm, 4),
+                     "nj_per_signal": nj,
                      "clocks": {k: sc[k] for k in ("sm_mhz", "reasons", "power_w")}}
+        tc_step = lambda: [(dplans[i].dense_forward(X[i], Y[i], stream),   # noqa: E731
+                            dplans[i].dense_inverse(Y[i], Z[i], stream)) for i in range(2)]
+        _, tms, tsc, tnj = sustain(tc_step, dense["tc"])
+        sustained["dense_tc"] = {"ms_per_step": round(tms, 5), "fast_speedup": round(tms / sms, 3),
+                                 "nj_per_signal": tnj, "sm_mhz": tsc["sm_mhz"]}
+    for p in dplans:
+        p.close()
     sampler.stop()
 
     # ---- end to end through the C ABI with pinned HOST buffers (H2D + kernels + D2H timed) ---
@@ -579,18 +683,24 @@ def main():
     e2e_step()
     torch.cuda.synchronize()
     barrier(device)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(args.e2e_steps):
-        e2e_step()
-    b.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(a.elapsed_time(b) / args.e2e_steps, device)
+    # median over rounds of e2e_steps steps each (one round on a box once read 0.73 of the
+    # PCIe roof where every other run, before and after, read 0.96-0.98: tools/r02/e2e_var.py)
+    rounds = []
+    for _ in range(args.e2e_rounds):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        rounds.append(a.elapsed_time(b) / args.e2e_steps)
+    e2e_ms = max_over_ranks(statistics.median(rounds), device)
     rt_err = max(float(((z.double() - x.double()).norm(dim=1) / x.double().norm(dim=1)).max())
                  for z, x in zip(Zh, Xc))
     step_bytes = sum(nbytes)   # per step: each transform copies its input in and its output out
     e2e = {"value": B * ws / (e2e_ms * 1e-3), "unit": "signals/s", "h2d_bytes_per_step": step_bytes,
-           "d2h_bytes_per_step": step_bytes, "ms_per_step": round(e2e_ms, 4), "roundtrip_max_rel_err": rt_err,
+           "d2h_bytes_per_step": step_bytes, "ms_per_step": round(e2e_ms, 4), "rounds": "median of %d x %d steps" % (args.e2e_rounds, args.e2e_steps),
+           "roundtrip_max_rel_err": rt_err,
            "pcie_bidir_each_gbs": pcie_roof(device),
            "achieved_each_dir_gbs": round(step_bytes / (e2e_ms * 1e6), 1)}
 
@@ -616,12 +726,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": len(seq) * args.steps,
             "kernels": kernels, "clocks": clocks,
         }
-        line = json.dumps(out, separators=(",", ":"))
-        if len(line) > 2000:   # keep the headline parseable from a bounded stdout tail
-            for k in ("kernels", "peaks_tflops"):
-                out.pop(k, None)
-            line = json.dumps(out, separators=(",", ":"))
-        print(line, flush=True)
+        print(headline_line(out), flush=True)
     if dist:
         dist.destroy_process_group()
     for p in plans:

@@ -42,3 +42,6 @@ def test_bench_driver_command():
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     s = d["sustained"]
     assert s["seconds"] >= 2.0 and s["value"] > 0
+    assert s["dense_tc"]["ms_per_step"] > 0 and s["dense_tc"]["fast_speedup"] > 0
+    k = d["kernels"]   # the in-run dense comparisons must survive the size limit
+    assert set(k["dense_ms_per_step"]) == {"fma", "tc", "cublas"} and k["fast_vs_best_dense"] > 0

@@ -1,7 +1,7 @@
 """FMA-skeleton geometry sweep for one plan kernel (fwd / inv / filter): each (R, stages, warps,
 pace) candidate is set through gft_plan_tuning_set / a filter rebuilt under GFT_TUNE_* env, and
 timed as best of 3 x 60 back-to-back launches (the built-in tuner's 2 x 10 is within noise of
-these differences).  python geo_sweep.py <cfg>[:f64] <fwd|inv|filt>"""
+these differences).  python geo_sweep.py <cfg|rhN>[:f64][@log2batch] <fwd|inv|filt>"""
 import itertools
 import json
 import os
@@ -11,16 +11,34 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import workloads  # noqa: E402
 from paper_1907_07875_b200 import gft  # noqa: E402
 
 spec, kind = sys.argv[1], sys.argv[2]
+spec, lb = spec.split("@") if "@" in spec else (spec, None)
 name, dt = spec.split(":") if ":" in spec else (spec, "f32")
-cfg = workloads.config(name)
+if name.startswith("rh"):
+    import probe_plans
+    case = workloads.RIGHT_HAAR_BENCH_CASES[int(name[2:])]
+    dt = case[4]
+    gn, gs, gd, gw, gl, gnorm = workloads.right_haar_bench_graph(case)
+    NB = 1 << 20
+
+    def new_plan(**kw):
+        return gft.Plan(gn, gs, gd, gw, gl, dtypes=(dt,), normalized=gnorm, **kw)
+else:
+    cfg = workloads.config(name)
+    gn, NB = cfg.n, cfg.batch
+
+    def new_plan(**kw):
+        return gft.Plan.from_config(cfg, dtypes=(dt,), **kw)
+if lb:
+    NB = 1 << int(lb)
 tdt = torch.float64 if dt == "f64" else torch.float32
-X = torch.randn(cfg.batch, cfg.n, device="cuda", dtype=tdt)
+X = torch.randn(NB, gn, device="cuda", dtype=tdt)
 Y = torch.empty_like(X)
-nb = 2 * cfg.batch * cfg.n * X.element_size()
+nb = 2 * NB * gn * X.element_size()
 esz = X.element_size()
 
 
@@ -41,14 +59,14 @@ def timed(fn):
 
 
 res = []
-plan = gft.Plan.from_config(cfg, dtypes=(dt,), no_cubin_cache=True)
+plan = new_plan(no_cubin_cache=True)
 default = None
 WARPS = tuple(int(w) for w in os.environ.get("SWEEP_WARPS", "4,8,12").split(","))
 OBUFS = tuple(int(w) for w in os.environ.get("SWEEP_OBUF", "0").split(","))
 PACES = tuple(int(w) for w in os.environ.get("SWEEP_PACE", "0,150").split(","))
 RS = tuple(int(w) for w in os.environ.get("SWEEP_R", "1,2,4").split(","))
 for R, S, W, pace, ob in itertools.product(RS, (2, 3), WARPS, PACES, OBUFS):
-    tile = 32 * R * cfg.n * esz
+    tile = 32 * R * gn * esz
     if W * (S + ob) * tile + W * S * 8 + 1024 > 227 * 1024 or tile > 32768:
         continue
     os.environ["GFT_FMA_OBUF"] = str(ob)
@@ -61,7 +79,7 @@ for R, S, W, pace, ob in itertools.product(RS, (2, 3), WARPS, PACES, OBUFS):
             f.close()
         else:
             k = 0 if kind == "fwd" else 1
-            plan = gft.Plan.from_config(cfg, dtypes=(dt,), no_cubin_cache=True)
+            plan = new_plan(no_cubin_cache=True)
             plan.set_tuning({k: (R, S, W, pace)}, dt)
             fn = plan.forward if k == 0 else plan.inverse
             frac = timed(lambda: fn(X, Y))

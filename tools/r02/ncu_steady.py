@@ -29,5 +29,8 @@ for k, m in rows.items():
                          "dram_write_per_launch": round(statistics.mean(wr[1:])),
                          "first_launch_bytes": round(rd[0] + wr[0]),
                          "duration_us_mean": round(statistics.mean(m["gpu__time_duration.sum"][1:]), 2)}
+    pct = m.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")
+    if pct:
+        out["kernels"][k]["dram_pct_of_peak_mean"] = round(statistics.mean(pct[1:]), 2)
 json.dump(out, open(sys.argv[2], "w"), indent=1)
 print(json.dumps(out, indent=1))

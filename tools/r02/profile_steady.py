@@ -9,16 +9,16 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch  # noqa: E402
 
-import workloads  # noqa: E402
-from paper_1907_07875_b200 import gft  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import probe_plans  # noqa: E402
 
-for name in ("cfg5a", "cfg5b"):
-    cfg = workloads.config(name)
-    p = gft.Plan.from_config(cfg, dtypes=("f32",))
-    X = torch.randn(cfg.batch, cfg.n, device="cuda")
+# plans by probe name (default: the headline's cfg5a and cfg5b; e.g. rh0 for the right-Haar 32|32 kernel)
+for name in (sys.argv[1:] or ["cfg5a", "cfg5b"]):
+    p, n, batch, dt = probe_plans.make(name)
+    X = torch.randn(batch, n, device="cuda", dtype=torch.float64 if dt == "f64" else torch.float32)
     Y = torch.empty_like(X)
     for kind, f in ((0, p.forward), (1, p.inverse)):
-        print(name, kind, p.kernel_name(kind, "f32"), flush=True)
+        print(name, kind, p.kernel_name(kind, dt), flush=True)
         for _ in range(6):
             f(X, Y)
         torch.cuda.synchronize()
