@@ -261,6 +261,106 @@ def config_table(args, stream, hbm, device, peaks):
     return rows
 
 
+def paper_table(args, stream, hbm, device):
+    """tab:runtime of Sec. VI-A re-timed on B200: the paper's graphs, its
+    printed operation counts and C-runtime reductions (hardware not stated) beside ours.
+    Signals are i.i.d. U[0,1] fp32 as in PAPER.md:757, at the paper's 20000 signals (launch-
+    bound: CUDA-graph replay) and at 2^21 (bandwidth regime).  runtime reduction =
+    1 - t_fast / t_dense for the forward transform, against our CUDA-core dense kernel (the
+    "single n x n matrix multiplication" analogue) and against the best dense kernel."""
+    import torch
+    import workloads
+    from paper_1907_07875_b200 import gft
+    rows = []
+    tf32 = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    for topo, n, build, phi, paper_ops, paper_red in workloads.tab_runtime_graphs():
+        s, d, w = build()
+        plan = gft.Plan(n, s, d, w, None, phi, dtypes=("f32",))
+        info = plan.info()
+        row = {"topology": topo, "n": n, "leaves": plan.leaf_sizes(),
+               "paper": {"matrix_adds": paper_ops[0], "matrix_mults": paper_ops[1], "fast_adds": paper_ops[2],
+                         "fast_mults": paper_ops[3], "runtime_reduction_pct": paper_red,
+                         "hardware": "not stated (C implementation)"},
+               "ours": {"fast_adds": info["adds"], "fast_mults_paper_convention": info["paper_mults"],
+                        "fast_mults_kernel": info["mults"]}}
+        # tcgen05 dense comparison wherever the tensor-core kernels apply (n % 4 == 0, rows padded
+        # to 32 columns) and the product is big enough to matter
+        dplan = gft.Plan(n, s, d, w, None, phi, dtypes=("f32",), dense_tc=True) if n % 4 == 0 and n >= 32 else None
+        U = torch.from_numpy(plan.basis()).to(device=device, dtype=torch.float32)
+        for batch in (20000, 1 << 21):
+            g = torch.Generator(device=device).manual_seed(n)
+            X = torch.rand(batch, n, generator=g, device=device)
+            Y = torch.empty_like(X)
+            # current stream (= `stream`), so that the same calls can be captured into a graph
+            arms = {"fast": lambda: plan.forward(X, Y), "dense": lambda: plan.dense_forward(X, Y),
+                    "cublas": lambda: torch.matmul(X, U, out=Y)}
+            if dplan is not None:
+                arms["dense_tc"] = lambda: dplan.dense_forward(X, Y)
+            if batch <= 20000:
+                t = {k: time_graph(f, 50) for k, f in arms.items()}
+            else:
+                t = {k: time_kernel(f, stream, 3, args.table_iters) for k, f in arms.items()}
+            best = min(v for k, v in t.items() if k != "fast")
+            row["b%d" % batch] = {"ms": {k: round(v, 5) for k, v in t.items()},
+                                  "reduction_vs_dense_pct": round(100 * (1 - t["fast"] / t["dense"]), 1),
+                                  "reduction_vs_best_dense_pct": round(100 * (1 - t["fast"] / best), 1),
+                                  "fast_hbm_frac": round(2 * batch * n * 4 / (t["fast"] * 1e-3) / 1e9 / hbm, 4)}
+            del X, Y
+        rows.append(row)
+        if dplan is not None:
+            dplan.close()
+        plan.close()
+    torch.backends.cuda.matmul.allow_tf32 = tf32
+    return rows
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_table(max_rows):
+    """SURVEY §8(d) oracle timing: the oracle's dense fp64 forward Y = X U of every config on
+    the host, with all BLAS threads and with 1 thread (bounded to `max_rows` rows per config)."""
+    import oracle
+    import workloads
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:   # pragma: no cover
+        threadpool_limits = None
+    out = {"cpu_model": cpu_model(), "cores": os.cpu_count(), "blas_threads": blas_threads(), "configs": []}
+    for name, dtype in (("cfg2", "f32"), ("cfg3", "f32"), ("cfg4", "f32"), ("cfg4", "f64"), ("cfg5a", "f32"),
+                        ("cfg5b", "f32")):
+        cfg = workloads.config(name)
+        rows = min(cfg.batch, max_rows)
+        U = oracle.gft_basis(oracle.laplacian(cfg.n, cfg.src, cfg.dst, cfg.w, cfg.self_loops))[1]
+        X = workloads.signals(cfg, batch=rows, dtype=dtype).numpy()
+        r = {"config": name, "dtype": dtype, "rows": rows}
+        for tag, nt in (("all_threads", None), ("one_thread", 1)):
+            ctx = threadpool_limits(limits=nt) if (threadpool_limits and nt) else None
+            if ctx:
+                ctx.__enter__()
+            try:
+                best = 1e9
+                for _ in range(2):
+                    t = time.perf_counter()
+                    oracle.forward(X, U)
+                    best = min(best, time.perf_counter() - t)
+            finally:
+                if ctx:
+                    ctx.__exit__(None, None, None)
+            r[tag + "_signals_per_s"] = rows / best
+        out["configs"].append(r)
+    return out
+
+
 def right_haar_table(args, stream, hbm, device):
     """Right Haar stages: plans with / without them on bipartite graphs
     whose Laplacian diagonal is constant, device-resident N(0,1), 2^20 signals."""
@@ -613,7 +713,9 @@ def main():
         tables = {"hbm_peak_gbs": hbm, "compute_peaks": peaks,
                   "energy": energy_table(arms, B, stream, sampler, args.energy_s),
                   "configs": config_table(args, stream, hbm, device, peaks),
-                  "right_haar": right_haar_table(args, stream, hbm, device)}
+                  "right_haar": right_haar_table(args, stream, hbm, device),
+                  "paper_tab_runtime": paper_table(args, stream, hbm, device),
+                  "oracle_cpu": oracle_table(1 << 18)}
         torch.backends.cuda.matmul.allow_tf32 = tf32
         os.makedirs(os.path.dirname(os.path.abspath(args.tables)), exist_ok=True)
         with open(args.tables, "w") as f:

@@ -227,7 +227,10 @@ def test_tuning_table_kind_and_work_keys():
     assert geo(c5.kernel_source(0, "f32")) == (1, 2, 8) and obuf(c5.kernel_source(0, "f32")) == 0
     assert geo(c5.kernel_source(1, "f32")) == (2, 2, 3) and obuf(c5.kernel_source(1, "f32")) == 2
     c1 = G.Plan.from_config(workloads.config("cfg1"), dtypes=("f32",))
-    assert geo(c1.kernel_source(0, "f32")) == (8, 3, 4) and pace(c1.kernel_source(0, "f32")) == 0
-    assert geo(c1.kernel_source(1, "f32")) == (8, 2, 8) and pace(c1.kernel_source(1, "f32")) == 150
+    for k in (0, 1):   # kind=fwd / kind=inv entries (r12)
+        src = c1.kernel_source(k, "f32")
+        assert geo(src) == (8, 3, 3) and pace(src) == 150 and obuf(src) == 2
+    f1 = G.Filter(c1, np.ones(8), dtypes=("f32",))   # kind=filter keeps its own entry
+    assert geo(f1.kernel_source("f32")) == (8, 2, 8) and pace(f1.kernel_source("f32")) == 150
     # the dense kernels of cfg1 take the plain n = 8 entry
-    assert geo(c1.kernel_source(2, "f32")) == (8, 3, 4)
+    assert geo(c1.kernel_source(2, "f32")) == (8, 3, 4) and pace(c1.kernel_source(2, "f32")) == 0

@@ -33,7 +33,7 @@ import numpy as np
 
 __all__ = ["Config", "CONFIGS", "config", "signals", "path_graph", "cycle_graph",
            "grid_graph", "skeleton25_graph", "random_symmetric_graph", "precision_matrix",
-           "random_bipartite_graph", "regular_bipartite_graph", "RIGHT_HAAR_BENCH_CASES",
+           "random_bipartite_graph", "regular_bipartite_graph", "RIGHT_HAAR_BENCH_CASES", "tab_runtime_graphs",
            "right_haar_bench_graph"]
 
 
@@ -365,6 +365,24 @@ def z_grid(N=8, w=2.0):
             if r + 1 < N and c >= 1:
                 pairs.append((v, v + N - 1)); wts.append(w)
     return _edges(pairs, wts)
+
+
+# tab:runtime of Sec. VI-A: the paper's matrix-vs-fast comparison graphs with
+# its printed operation counts (matrix adds / mults, fast adds / mults) and C-runtime reduction
+# (hardware not stated), re-timed on B200 by bench.py --tables.  The 15-node skeleton exists only
+# as a figure and is not rebuilt; the 25-node one is cfg3's topology.
+def tab_runtime_graphs():
+    diag4 = np.array([4 * (i % 4) + i // 4 for i in range(16)], np.int32)
+    diag8 = np.array([8 * (i % 8) + i // 8 for i in range(64)], np.int32)
+    return [("Cycle", 12, lambda: cycle_graph(12), None, (132, 144, 44, 30), 52.7),
+            ("Cycle", 80, lambda: cycle_graph(80), None, (6320, 6400, 1224, 1078), 79.7),
+            ("6-conn. grid", 16, lambda: bidiag_grid(4), diag4, (240, 256, 80, 80), 53.7),
+            ("6-conn. grid", 64, lambda: bidiag_grid(8), diag8, (4032, 4096, 1104, 1072), 68.5),
+            ("Z-shaped grid", 16, lambda: z_grid(4), np.array([15 - i for i in range(16)], np.int32),
+             (240, 256, 128, 112), 41.5),
+            ("Z-shaped grid", 64, lambda: z_grid(8), np.array([63 - i for i in range(64)], np.int32),
+             (4032, 4096, 2048, 2048), 45.0),
+            ("Skeleton", 25, skeleton25_graph, config("cfg3").phi, (600, 625, 272, 282), 47.5)]
 
 
 # Approximate-GFT comparison of Sec. VI-B, timed by bench.py and
