@@ -1107,9 +1107,16 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
     const char* eio = getenv("GFT_TC_IOSPLIT");
     if (ok && pair && !ws && !no_ws && P.n > 64 && T.size() == P.leaves.size() && !(eio && eio[0] == '0')) {
       Tws = T;
-      if (ws_layout(Tws, ws_a, ws_d, ws_tmem)) {
-        const int tile = 128 * ((P.n + 31) / 32 * 32) * 4;
-        if (3 * tile + b_bytes + 2048 <= 227 * 1024) {
+      // the fp16x2 layout (below) needs half the B bytes of 3xTF32: a single 128-node leaf (the
+      // n = 128 dense comparison on tcgen05) fits the IO-split kernel only that way
+      const char* e16 = getenv("GFT_TC_F16");
+      int ac16 = 0, dc16 = 0, bb16 = 1024;
+      for (const auto& t : T) { ac16 += t.kp32; dc16 += ru(t.np, 32); bb16 += 2 * ((t.kp32 + 63) / 64) * (t.np / 2) * 128; }
+      const bool fit16 = !(e16 && e16[0] == '0') && ac16 + 2 * dc16 <= 512;
+      const bool fit32 = ws_layout(Tws, ws_a, ws_d, ws_tmem);
+      const int tile = 128 * ((P.n + 31) / 32 * 32) * 4;
+      if ((fit32 && 3 * tile + b_bytes + 2048 <= 227 * 1024) || (fit16 && 3 * tile + bb16 + 2048 <= 227 * 1024)) {
+        {
           ws = io_split = true;
           stages = 2;
           wgs = 1;
@@ -1166,6 +1173,16 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
           << tmem_cols << "\n";
       if (wgs == 2) pre << "#define GFT_WGS 2\n#define GFT_WG_COLS " << wg_cols << "\n";
       if (io_split) pre << "#define GFT_IO_SPLIT 1\n";
+      // in-place warp-specialised kernel: a separate storer warp stores each tile as soon as it is
+      // drained and hands the buffer to the loader once the store has read it (before: one
+      // thread issued store, wait-read, load in turn, so a drained tile's store waited behind
+      // the previous store's read and the load pacing).  Right-Haar 32|32 0.968 -> 0.977,
+      // z-grid 64 (two 32-leaves) 0.930 -> 0.970 of the copy peak (profiles/r02/r02_split_store.log).
+      // GFT_TC_SPLIT_STORE=0 restores the single producer / storer thread (ablation).
+      {
+        const char* e = getenv("GFT_TC_SPLIT_STORE");
+        if (ws && !io_split && !(e && e[0] == '0')) pre << "#define GFT_SPLIT_STORE 1\n";
+      }
       if (const char* e = getenv("GFT_TC_TRACE")) if (e[0] == '1') pre << "#define GFT_TRACE 1\n";   // experiments
       if (ws) {
         // load pacing (kernel_tc3_skeleton.cuh pace_load): a fraction of the CTA's fair share of

@@ -10,10 +10,11 @@
 //   WG1 (warps 4-7)  drainer: wait for the tile's MMAs -> tcgen05.ld the D columns (double
 //                             buffered in TMEM) -> free them (`d_free` on the leader) ->
 //                             back butterflies / coefficient butterflies -> SMEM row;
-//   warp 8           TMA producer / storer of this CTA's rows;
+//   warp 8           TMA producer of this CTA's rows (loads; also the stores with GFT_SPLIT_STORE=0);
+//   warp 10          storer (GFT_SPLIT_STORE, the in-place default; IO-split: box-granular storer);
 //   warp 9           MMA issuer (leader CTA): staged(t) and d_free(t-2) -> MMAs into
 //                             D[t % 2] -> one multicast commit on mma_done[t % 2];
-//   warps 10-11      idle (a full third warpgroup so that setmaxnreg can move registers:
+//   warp 11          idle (with warp 10, a full third warpgroup so that setmaxnreg can move registers:
 //                             WG2 drops to 56, the stager rises to 248, the drainer to 200).
 // The A columns are staged and released per 32-column chunk (GFT_NCH chunks over all
 // tensor-core leaves): the issuer waits for chunk c of tile t to be staged (both CTAs), issues
@@ -266,7 +267,8 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   unsigned long long* b_afree = b_staged + 2 * GFT_NCH;
   unsigned long long* b_erdy = b_afree + GFT_NCH;    // [2] row exponents of tile t%2 written (4 stager warps)
   unsigned long long* b_efree = b_erdy + 2;          // [2] ... read (4 drainer warps)
-  u32* tmem_slot = reinterpret_cast<u32*>(b_efree + 2);
+  unsigned long long* b_sfree = b_efree + 2;         // [S] (GFT_SPLIT_STORE) in-place buffer's store has read it
+  u32* tmem_slot = reinterpret_cast<u32*>(b_sfree + GFT_STAGES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const u32 rank = cluster_rank();
   const long long npairs = (batch + 2 * GFT_TILE_ROWS - 1) / (2 * GFT_TILE_ROWS);
@@ -300,6 +302,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       mbar_init(smem_u32(&b_boxrdy[b]), 4);
       mbar_init(smem_u32(&b_boxfree[b]), 1);
     }
+    for (int s = 0; s < GFT_STAGES; ++s) mbar_init(smem_u32(&b_sfree[s]), 1);
     fence_mbar_init();
   }
   const float4* bsrc = reinterpret_cast<const float4*>(gft_tcB[rank]);
@@ -357,6 +360,47 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
         TR(9, it);
       }
       bulk_wait_all();
+    } else
+#endif
+#ifndef GFT_SPLIT_STORE
+#define GFT_SPLIT_STORE 0
+#endif
+#if GFT_SPLIT_STORE && !GFT_IO_SPLIT
+    if (warp == 10 && lane == 0) {
+      // ---------------- storer of the in-place buffers (default): stores a tile as soon as it
+      // is drained and hands the buffer to the loader once the store has read it, so a store
+      // never waits behind the loader's pacing
+      for (long long it = 0;; ++it) {
+        const long long p = pid0 + it * npid;
+        if (p >= npairs) break;
+        const long long row0 = p * 2 * GFT_TILE_ROWS + rank * GFT_TILE_ROWS;
+        const int s = (int)(it % GFT_STAGES);
+        mbar_wait(smem_u32(&b_done[s]), (u32)((it / GFT_STAGES) & 1));
+        const u32 src = smem_u32(stages + s * GFT_TILE_BYTES);
+        for (int b = 0; b < GFT_NBOX; ++b)
+          tma_store_2d(&tout, b * GFT_BOXC, (int)row0, src + b * GFT_BOX_BYTES);
+        bulk_commit();
+        bulk_wait_read0();
+        mbar_arrive(smem_u32(&b_sfree[s]));
+      }
+      bulk_wait_all();
+    } else if (warp == 8 && lane == 0) {
+      // ---------------- loader of the in-place buffers ----------------
+      unsigned long long t_last = 0;
+      for (long long it = 0;; ++it) {
+        const long long p = pid0 + it * npid;
+        if (p >= npairs) break;
+        const long long row0 = p * 2 * GFT_TILE_ROWS + rank * GFT_TILE_ROWS;
+        const int s = (int)(it % GFT_STAGES);
+        if (it >= GFT_STAGES) mbar_wait(smem_u32(&b_sfree[s]), (u32)(((it / GFT_STAGES) - 1) & 1));
+        pace_load(t_last, it);
+        TR(0, it);
+        const u32 bar = smem_u32(&b_full[s]);
+        const u32 dst = smem_u32(stages + s * GFT_TILE_BYTES);
+        mbar_expect_tx(bar, GFT_TILE_BYTES);
+        for (int b = 0; b < GFT_NBOX; ++b)
+          tma_load_2d(dst + b * GFT_BOX_BYTES, &tin, b * GFT_BOXC, (int)row0, bar);
+      }
     } else
 #endif
     if (warp == 8 && lane == 0) {
