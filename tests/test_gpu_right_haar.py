@@ -104,3 +104,22 @@ def test_right_stage_filter(kind, a, b, dtype):
     Y2 = plan.inverse(plan.forward(X.cuda()) * torch.from_numpy(h).to(TDT[dtype]).cuda())
     torch.cuda.synchronize()
     assert oracle.relative_error(Yf.cpu().numpy(), Y2.cpu().numpy()).max() <= 4 * tol
+
+
+@pytest.mark.parametrize("batch", [1, 255, 256, 70001])
+def test_split_store_bit_identical(batch, monkeypatch):
+    """The in-place warp-specialised tcgen05 kernel's split storer (default) only reorders
+    stores and loads: outputs are bit-identical to the single producer / storer thread
+    (GFT_TC_SPLIT_STORE=0), for ragged batches of 1 .. several tiles, forward and inverse."""
+    n, (s, d, w, loops), norm, _ = _graph("norm", 32, 32, 11)
+    X = torch.randn(batch, n, generator=torch.Generator().manual_seed(batch), dtype=torch.float32).cuda()
+    outs = []
+    for v in ("1", "0"):
+        monkeypatch.setenv("GFT_TC_SPLIT_STORE", v)
+        p = G.Plan(n, s, d, w, loops, dtypes=("f32",), normalized=norm, no_cubin_cache=True)
+        assert "tc3_" in p.kernel_name(0, "f32")
+        outs.append((p.forward(X), p.inverse(X), p.kernel_name(0, "f32")))
+        p.close()
+    torch.cuda.synchronize()
+    assert outs[0][2] != outs[1][2]   # two different kernels
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
