@@ -800,7 +800,7 @@ float f16_to_f32_host(uint16_t h) {
 // h and l), half the B bytes, half the MMA instructions.  Error: |x' - h - l| <= 2^-11 |l| <=
 // 2^-22 |x'| per element, B likewise; the dropped l.B_l term is ~2^-22 relative.
 void generate_tc_ws_f16(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int a_cols, int d_cols,
-                        std::ostringstream& o) {
+                        int a_bufs, std::ostringstream& o) {
   // ---- B operands: per CTA half (N/2 rows), per leaf, parts h then l; K-major, 128B-swizzled
   // atoms of 64 fp16 (128 B) x 8 rows; K padded to whole 32-element chunks ----
   std::vector<uint16_t> B;
@@ -830,8 +830,8 @@ void generate_tc_ws_f16(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int 
   int nch = 0;
   for (const TcLeaf& t : T) nch += t.kp32 / 32;
   o << "#define GFT_F16X2 1\n#define GFT_B_FLOATS " << per_cta / 2 << "\n#define GFT_A_COLS " << a_cols
-    << "\n#define GFT_NCH " << nch << "\n#define GFT_D_BASE " << a_cols << "\n#define GFT_D_COLS " << d_cols
-    << "\n#define GFT_SMALL 0\n";
+    << "\n#define GFT_A_BUFS " << a_bufs << "\n#define GFT_NCH " << nch << "\n#define GFT_D_BASE " << a_bufs * a_cols
+    << "\n#define GFT_D_COLS " << d_cols << "\n#define GFT_SMALL 0\n";
   o << "__device__ __align__(16) const unsigned int gft_tcB[2][" << per_cta / 2 << "] = {\n";
   for (size_t i = 0; i < B.size(); i += 2) {
     char buf[24];
@@ -1146,6 +1146,7 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
       // cfg5b forward 6.46 -> 6.50 TB/s burst and 5.93 -> 6.32 sustained at the power cap, max
       // per-signal error 9.9e-7 -> 7.2e-7 (tools/r02/gpu_f16_probe.sh).  GFT_TC_F16=0: 3xTF32
       bool f16 = false;
+      int a_bufs = 1;
       if (ws && Tws.size() == P.leaves.size()) {
         const char* e16 = getenv("GFT_TC_F16");
         if (!(e16 && e16[0] == '0')) {
@@ -1158,14 +1159,22 @@ void generate_kernel(const Plan& P, int kind, int dtype, Kernel& k, bool allow_t
             f16 = true;
             ws_a = ac;
             ws_d = dc;
+            // IO-split kernels: two A buffers when they fit TMEM beside the double-buffered D, so
+            // staging tile t+1 never waits for the MMAs of tile t (cfg5b 0.999 -> 1.010 of the copy
+            // peak in a burst, sustained unchanged; in-place n <= 64 kernels mixed: right-Haar 32|32
+            // +0.5%, z-grid 64 -2%, so they keep one; profiles/r02/r02_a2.log).  GFT_TC_A2=0 / 1
+            // forces one / two (ablation)
+            const char* ea2 = getenv("GFT_TC_A2");
+            const bool want2 = ea2 && *ea2 ? ea2[0] == '1' : io_split;
+            a_bufs = (2 * ac + 2 * dc <= 512 && want2) ? 2 : 1;
             tmem_cols = 32;
-            while (tmem_cols < ac + 2 * dc) tmem_cols *= 2;
+            while (tmem_cols < a_bufs * ac + 2 * dc) tmem_cols *= 2;
             c.tc_tmem_cols = tmem_cols;
             c.tc_b_bytes = bb + 1024;   // + the per-row exponents (2 tiles x 128 ints)
           }
         }
       }
-      if (f16) generate_tc_ws_f16(P, dir, Tws, ws_a, ws_d, gen);
+      if (f16) generate_tc_ws_f16(P, dir, Tws, ws_a, ws_d, a_bufs, gen);
       else if (ws) generate_tc_ws(P, dir, Tws, ws_a, ws_d, gen);
       else generate_tc(P, dir, T, pair, gen);
       std::ostringstream pre;

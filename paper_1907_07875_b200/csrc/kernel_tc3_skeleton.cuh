@@ -264,8 +264,13 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
   // per A chunk: staged[t%2][c] (leader; 8 stager warps of the pair), a_free[c] (MMAs of the
   // chunk done, multicast commit)
   unsigned long long* b_staged = bars + 3 * GFT_STAGES + 4 + 2 * GFT_NBOX;
-  unsigned long long* b_afree = b_staged + 2 * GFT_NCH;
-  unsigned long long* b_erdy = b_afree + GFT_NCH;    // [2] row exponents of tile t%2 written (4 stager warps)
+#ifndef GFT_A_BUFS
+#define GFT_A_BUFS 1
+#endif
+  // GFT_A_BUFS == 2: tile t stages into A buffer t % 2 (GFT_A_COLS columns each), so staging
+  // tile t+1 never waits for the MMAs of tile t -- only for those of tile t-1 on the same buffer
+  unsigned long long* b_afree = b_staged + 2 * GFT_NCH;   // [GFT_A_BUFS][GFT_NCH]
+  unsigned long long* b_erdy = b_afree + GFT_A_BUFS * GFT_NCH;    // [2] row exponents of tile t%2 written (4 stager warps)
   unsigned long long* b_efree = b_erdy + 2;          // [2] ... read (4 drainer warps)
   unsigned long long* b_sfree = b_efree + 2;         // [S] (GFT_SPLIT_STORE) in-place buffer's store has read it
   u32* tmem_slot = reinterpret_cast<u32*>(b_sfree + GFT_STAGES);
@@ -293,7 +298,7 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       mbar_init(smem_u32(&b_dfree[b]), 8);
     }
     for (int c = 0; c < 2 * GFT_NCH; ++c) mbar_init(smem_u32(&b_staged[c]), 8);
-    for (int c = 0; c < GFT_NCH; ++c) mbar_init(smem_u32(&b_afree[c]), 1);
+    for (int c = 0; c < GFT_A_BUFS * GFT_NCH; ++c) mbar_init(smem_u32(&b_afree[c]), 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&b_erdy[b]), 4);
       mbar_init(smem_u32(&b_efree[b]), 4);
@@ -451,8 +456,9 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
         // out of the loop into registers (this warpgroup runs with 56 registers)
         u32 bs;
         asm volatile("mov.b32 %0, %1;" : "=r"(bs) : "r"(bsm_s));
-        gft_issue_ws(tmem, tmem + (u32)(GFT_D_BASE + b * GFT_D_COLS), bs, smem_u32(&b_staged[b * GFT_NCH]),
-                     (u32)((it >> 1) & 1), smem_u32(b_afree), it);
+        const int ab = GFT_A_BUFS == 2 ? b : 0;
+        gft_issue_ws(tmem + (u32)(ab * GFT_A_COLS), tmem + (u32)(GFT_D_BASE + b * GFT_D_COLS), bs,
+                     smem_u32(&b_staged[b * GFT_NCH]), (u32)((it >> 1) & 1), smem_u32(&b_afree[ab * GFT_NCH]), it);
         tc_commit_pair(smem_u32(&b_mma[b]));
         TR(5, it);
       }
@@ -481,8 +487,15 @@ GFT_KNAME(const __grid_constant__ TmaDesc tin, const __grid_constant__ TmaDesc t
       // chunk c of A is rewritten once the MMAs of tile it-1 on it are done (a_free[c])
 #if GFT_F16X2
       if (it >= 2) mbar_wait(smem_u32(&b_efree[it & 1]), (u32)(((it >> 1) - 1) & 1));   // drainer of it-2 read them
+#if GFT_A_BUFS == 2
+      // A buffer it % 2 was last read by the MMAs of tile it - 2
+      gft_stage(x, tm_a + (u32)((it & 1) * GFT_A_COLS), staged0[it & 1], buf, tid,
+                smem_u32(&b_afree[(it & 1) * GFT_NCH]), (u32)(((it >> 1) - 1) & 1), it >= 2, it,
+                &row_e[(it & 1) * 128 + tid]);
+#else
       gft_stage(x, tm_a, staged0[it & 1], buf, tid, smem_u32(b_afree), (u32)((it - 1) & 1), it >= 1, it,
                 &row_e[(it & 1) * 128 + tid]);
+#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&b_erdy[it & 1]));
 #else

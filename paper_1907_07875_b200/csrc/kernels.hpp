@@ -47,7 +47,7 @@ struct KernelCfg {
   int tiles_per_cta() const { return (tc || dgemm) ? 1 : warps; }   // tiles processed concurrently per CTA
   int smem_bytes() const {
     if (dgemm) return stages * tile_bytes() + n * n * elem + 2 * stages * 8 + 1024;
-    if (tc) return (stages + tc_io_split) * tile_bytes() + tc_b_bytes + (4 * stages + 24) * 8 + 16 + 1024;
+    if (tc) return (stages + tc_io_split) * tile_bytes() + tc_b_bytes + (4 * stages + 48) * 8 + 16 + 1024;
     return warps * (stages + obuf) * tile_bytes() + warps * stages * 8 + 1024;
   }
   int swizzle_bytes() const { return swz_mask == 7 ? 128 : swz_mask == 3 ? 64 : swz_mask == 1 ? 32 : 0; }
