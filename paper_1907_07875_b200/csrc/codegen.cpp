@@ -158,6 +158,33 @@ double leaf_coef(const Leaf& lf, Dir d, int o, int i) {
   return d == DIR_INV ? lf.M[(size_t)i * lf.k + o] : lf.M[(size_t)o * lf.k + i];
 }
 
+// fp32 Haar unit as ONE packed FFMA2 (sm_100 fma.rn.f32x2 with both scalar operands broadcast):
+// {P, P} * {pm.lo, pm.hi} + {Q, Q}, pm = {1, -1} or {-1, 1}; fma(P, +-1, Q) is the exactly rounded
+// Q +- P, so the result is bit-identical to two FADDs and the butterfly costs half the issue
+// slots (the outputs form the destination register pair; the inputs need no packing).
+// Opt-in (GFT_FFMA2_UNITS=1), tcgen05 kernels' stager / drainer only: timed alone it lifts the
+// IO-split kernels 0.4-1.3% (cfg5b, right-Haar 64|64), but inside the headline step, interleaved
+// in one process, it is 0.2-0.5% SLOWER (the pair destinations cost ~140 extra MOVs per row
+// elsewhere); in the CUDA-core FMA skeleton it cost up to 18% (cfg2 fwd 1.036 -> 0.851, cfg4 inv
+// 1.047 -> 0.872, cfg5a filter 0.975 -> 0.927) and is never used there
+// (profiles/r02/r02_ffma2_units.log).
+bool ffma2_units() {
+  const char* e = getenv("GFT_FFMA2_UNITS");
+  return e && e[0] == '1';
+}
+// (dst0, dst1) <- (Q + pm.lo * P, Q + pm.hi * P); minus_first: pm = {-1, 1} instead of {1, -1}
+std::string unit2(const std::string& d0, const std::string& d1, const std::string& P_, const std::string& Q_,
+                  bool minus_first) {
+  return "{ unsigned long long d_; asm(\"{ .reg .b64 t0, t1; mov.b64 t0, {%1, %1}; mov.b64 t1, {%2, %2}; "
+         "fma.rn.f32x2 %0, t1, %3, t0; }\" : \"=l\"(d_) : \"f\"(" + Q_ + "), \"f\"(" + P_ + "), \"l\"(" +
+         (minus_first ? "0x3F800000BF800000ull" : "0xBF8000003F800000ull") +
+         ")); asm(\"mov.b64 {%0, %1}, %2;\" : \"=f\"(" + d0 + "), \"=f\"(" + d1 + ") : \"l\"(d_)); }";
+}
+std::string unit_ab(const char* arr, int a, int b) {   // (x_a, x_b) <- (x_a + x_b, x_a - x_b)
+  const std::string A = xs(arr, a), B = xs(arr, b);
+  return unit2(A, B, B, A, false);
+}
+
 void emit_units_elem(std::ostringstream& o, const Plan& P, const char* arr, bool reverse, int dtype) {
   o << "  { elem_t a_, b_;\n";
   int lvl = -1;
@@ -257,10 +284,18 @@ void emit_leaf_fma(std::ostringstream& o, const Leaf& lf, size_t l, Dir d, int d
 // Right Haar stages on the coefficients, type T of the array:
 //   forward (after the leaves):  y_p <- a + b,  y_q <- s (a - b)
 //   inverse (before the leaves): x_p <- y_p + s y_q,  x_q <- y_p - s y_q   (transpose)
-void emit_post_units(std::ostringstream& o, const Plan& P, const char* arr, bool inverse, const char* T) {
+void emit_post_units(std::ostringstream& o, const Plan& P, const char* arr, bool inverse, const char* T,
+                     bool f32 = true) {
   if (P.post.empty()) return;
   o << "  // ---- right Haar stage (" << P.post.size() << " coefficient pairs)\n  { " << T << " a_, b_;\n";
   for (const PostUnit& u : P.post) {
+    if (f32 && ffma2_units()) {
+      const std::string A = xs(arr, u.p), B = xs(arr, u.q);
+      // forward (a+b, s(a-b)); inverse (a + s b, a - s b)
+      if (!inverse) o << "  " << (u.s > 0 ? unit2(A, B, B, A, false) : unit2(A, B, A, B, false)) << "\n";
+      else o << "  " << (u.s > 0 ? unit2(A, B, B, A, false) : unit2(A, B, B, A, true)) << "\n";
+      continue;
+    }
     o << "  a_ = " << arr << "[" << u.p << "]; b_ = " << arr << "[" << u.q << "]; ";
     if (!inverse)
       o << arr << "[" << u.p << "] = a_ + b_; " << arr << "[" << u.q << "] = "
@@ -276,11 +311,11 @@ void emit_fast(std::ostringstream& o, const Plan& P, int dtype, Dir d, bool stre
   if (d == DIR_FILTER && !P.post.empty()) fail(GFT_ERR_COMPILE, "filter plan with right Haar stages");
   if (stream) o << "  elem_t y[GFT_N];\n";
   if (d != DIR_INV) emit_units_elem(o, P, "x", false, dtype);
-  if (d == DIR_INV) emit_post_units(o, P, "x", true, "elem_t");
+  if (d == DIR_INV) emit_post_units(o, P, "x", true, "elem_t", false);
   for (size_t l = 0; l < P.leaves.size(); ++l) emit_leaf_fma(o, P.leaves[l], l, d, dtype, stream);
   const bool after = (d == DIR_FWD && !P.post.empty()) || (d != DIR_FWD && !P.ops.empty());
   if (stream && after) o << "  load_row(buf_, row_, y);   // leaf outputs back for the stages after the leaves\n";
-  if (d == DIR_FWD) emit_post_units(o, P, "y", false, "elem_t");
+  if (d == DIR_FWD) emit_post_units(o, P, "y", false, "elem_t", false);
   if (d != DIR_FWD) emit_units_elem(o, P, "y", true, dtype);
   if (stream && after) o << "  store_row(buf_, row_, y);\n";
 }
@@ -430,7 +465,9 @@ std::string split_line(int i, const std::string& src) {
 void emit_units(std::ostringstream& o, const Plan& P, const char* arr, bool reverse, int dtype) {
   o << "  { float a_, b_;\n";
   auto one = [&](const Op& op) {
-    if (op.kind == Op::UNIT)
+    if (op.kind == Op::UNIT && ffma2_units())
+      o << "  " << unit_ab(arr, op.a, op.b) << "\n";
+    else if (op.kind == Op::UNIT)
       o << "  a_ = " << arr << "[" << op.a << "]; b_ = " << arr << "[" << op.b << "]; " << arr << "["
         << op.a << "] = a_ + b_; " << arr << "[" << op.b << "] = a_ - b_;\n";
     else
@@ -882,7 +919,16 @@ void generate_tc_ws_f16(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int 
       const int w = std::min(32, t.np - r0);
       o << "  { u32 d[" << w << "];\n";
       emit_tmem_ld(o, "d", t.d_col + r0, w);
-      for (int r = r0; r < std::min(t.k, r0 + w); ++r)
+      const int r1 = std::min(t.k, r0 + w);
+      int r = r0;
+      const char* efm = getenv("GFT_FMUL2_DRAIN");   // experiment
+      if (efm && efm[0] == '1')   // 2^e scale of two adjacent D columns as one packed FMUL2 (exact, like FMUL)
+        for (; r + 1 < r1; r += 2)
+          o << "  { unsigned long long p_; asm(\"{ .reg .b64 t0, t1; mov.b64 t0, {%1, %2}; mov.b64 t1, {%3, %3}; "
+               "mul.rn.f32x2 %0, t0, t1; }\" : \"=l\"(p_) : \"r\"(d[" << r - r0 << "]), \"r\"(d[" << r + 1 - r0
+            << "]), \"f\"(u_)); asm(\"mov.b64 {%0, %1}, %2;\" : \"=f\"(y[" << out_idx(lf, d, r) << "]), \"=f\"(y["
+            << out_idx(lf, d, r + 1) << "]) : \"l\"(p_)); }\n";
+      for (; r < r1; ++r)
         o << "  y[" << out_idx(lf, d, r) << "] = __uint_as_float(d[" << r - r0 << "]) * u_;\n";
       o << "  }\n";
     }

@@ -131,8 +131,9 @@ def test_kernel_source_is_plan_specialised():
     src = p.kernel_source(G.K_FAST_FWD, "f32")
     name = p.kernel_name(G.K_FAST_FWD, "f32")
     assert name in src and "gft_body" in src and "cp.async.bulk" in src
-    # 7 Haar units -> 7 add/sub pairs, leaves 1,1,2,4 -> 22 multiplies (FMA immediates)
-    assert src.count("= a_ + b_;") == 7
+    # 7 Haar units -> 7 add/sub pairs (the CUDA-core skeleton keeps FADD pairs), leaves 1,1,2,4
+    # -> 22 multiplies (FMA immediates)
+    assert src.count("= a_ + b_;") == 7 and src.count("fma.rn.f32x2") == 0
     assert src.count("__fmul_rn(") + src.count("__fmaf_rn(") == 22
     # inverse and dense kernels differ
     assert p.kernel_name(G.K_FAST_INV, "f32") != name
@@ -234,3 +235,21 @@ def test_tuning_table_kind_and_work_keys():
     assert geo(f1.kernel_source("f32")) == (8, 2, 8) and pace(f1.kernel_source("f32")) == 150
     # the dense kernels of cfg1 take the plain n = 8 entry
     assert geo(c1.kernel_source(2, "f32")) == (8, 3, 4) and pace(c1.kernel_source(2, "f32")) == 0
+
+
+def test_packed_ffma2_units_opt_in(monkeypatch):
+    """GFT_FFMA2_UNITS=1 (opt-in) turns the tcgen05 kernels' Haar units into single packed FFMA2
+    ops ({b,b}*{1,-1}+{a,a}), one per unit (cfg5b: 64 in the stager); the default and the
+    CUDA-core kernels keep FADD pairs."""
+    cfg = workloads.config("cfg5b")
+    p = G.Plan.from_config(cfg, dtypes=("f32",))
+    assert p.kernel_source(0, "f32").count("fma.rn.f32x2") == 0
+    monkeypatch.setenv("GFT_FFMA2_UNITS", "1")
+    p = G.Plan.from_config(cfg, dtypes=("f32",))
+    for k in (0, 1):
+        src = p.kernel_source(k, "f32")
+        assert "tc3s_" in p.kernel_name(k, "f32")
+        assert src.count("fma.rn.f32x2") == p.info()["units_per_level"][0] == 64
+        assert "0xBF8000003F800000ull" in src
+    c1 = G.Plan.from_config(workloads.config("cfg1"), dtypes=("f32",))
+    assert c1.kernel_source(0, "f32").count("fma.rn.f32x2") == 0

@@ -13,6 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import torch  # noqa: E402
 
 import probe_plans  # noqa: E402
+from paper_1907_07875_b200 import gft  # noqa: E402
 
 name = sys.argv[1]
 variants = sys.argv[2:]
@@ -45,11 +46,24 @@ def timed(fn):
     return nb / best / 1e6
 
 
+# ENV_CONFIRM_FILTER=1: the "inv" column times the heat-kernel fused filter instead
+filters = []
+if os.environ.get("ENV_CONFIRM_FILTER") == "1":
+    import numpy as np
+    for v, p in zip(variants, plans):
+        env = {} if v == "default" else dict(kv.split("=", 1) for kv in v.split(","))
+        os.environ.update(env)
+        filters.append(gft.Filter(p, np.exp(-p.eigenvalues()), dtypes=(dt,), no_cubin_cache=True))
+        for k in env:
+            os.environ.pop(k)
 res = {(v, k): [] for v in variants for k in ("fwd", "inv")}
 for _ in range(3):
-    for v, p in zip(variants, plans):
+    for j, (v, p) in enumerate(zip(variants, plans)):
         res[(v, "fwd")].append(timed(lambda: p.forward(X, Y)))
-        res[(v, "inv")].append(timed(lambda: p.inverse(X, Y)))
+        if filters:
+            res[(v, "inv")].append(timed(lambda: filters[j].apply(X, Y)))
+        else:
+            res[(v, "inv")].append(timed(lambda: p.inverse(X, Y)))
 for v, p in zip(variants, plans):
     f, i = statistics.median(res[(v, "fwd")]), statistics.median(res[(v, "inv")])
     print(json.dumps({"plan": name, "variant": v, "kernel": p.kernel_name(0, dt), "fwd_gbs": round(f, 1),
