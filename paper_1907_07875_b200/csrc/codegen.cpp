@@ -921,13 +921,6 @@ void generate_tc_ws_f16(const Plan& P, Dir d, const std::vector<TcLeaf>& T, int 
       emit_tmem_ld(o, "d", t.d_col + r0, w);
       const int r1 = std::min(t.k, r0 + w);
       int r = r0;
-      const char* efm = getenv("GFT_FMUL2_DRAIN");   // experiment
-      if (efm && efm[0] == '1')   // 2^e scale of two adjacent D columns as one packed FMUL2 (exact, like FMUL)
-        for (; r + 1 < r1; r += 2)
-          o << "  { unsigned long long p_; asm(\"{ .reg .b64 t0, t1; mov.b64 t0, {%1, %2}; mov.b64 t1, {%3, %3}; "
-               "mul.rn.f32x2 %0, t0, t1; }\" : \"=l\"(p_) : \"r\"(d[" << r - r0 << "]), \"r\"(d[" << r + 1 - r0
-            << "]), \"f\"(u_)); asm(\"mov.b64 {%0, %1}, %2;\" : \"=f\"(y[" << out_idx(lf, d, r) << "]), \"=f\"(y["
-            << out_idx(lf, d, r + 1) << "]) : \"l\"(p_)); }\n";
       for (; r < r1; ++r)
         o << "  y[" << out_idx(lf, d, r) << "] = __uint_as_float(d[" << r - r0 << "]) * u_;\n";
       o << "  }\n";
