@@ -123,3 +123,27 @@ def test_split_store_bit_identical(batch, monkeypatch):
     torch.cuda.synchronize()
     assert outs[0][2] != outs[1][2]   # two different kernels
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("knob", ["GFT_TC_A2=0", "GFT_FFMA2_UNITS=1"])
+def test_tc_variants_bit_identical(knob, monkeypatch):
+    """Variants that only change scheduling or the instruction form give bit-identical outputs:
+    one vs two A buffers in TMEM (GFT_TC_A2) and packed-FFMA2 vs FADD Haar units
+    (GFT_FFMA2_UNITS: fma(b, +-1, a) is the exactly rounded a +- b), on a 64|64 right-Haar plan
+    (IO-split kernel; coefficient butterflies of both signs after / before the leaves) with a
+    ragged batch, forward and inverse."""
+    n, (s, d, w, loops), norm, _ = _graph("norm", 64, 64, 5)
+    X = torch.randn(70001, n, generator=torch.Generator().manual_seed(3), dtype=torch.float32).cuda()
+    outs = []
+    for env in ({}, dict([knob.split("=")])):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        p = G.Plan(n, s, d, w, loops, dtypes=("f32",), normalized=norm, no_cubin_cache=True)
+        assert "tc3s_" in p.kernel_name(0, "f32") and p.info()["n_right_pairs"] == 64
+        outs.append((p.forward(X), p.inverse(X), p.kernel_name(0, "f32")))
+        p.close()
+        for k in env:
+            monkeypatch.delenv(k)
+    torch.cuda.synchronize()
+    assert outs[0][2] != outs[1][2]
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
