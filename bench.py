@@ -315,6 +315,38 @@ def paper_table(args, stream, hbm, device):
     return rows
 
 
+def energy_config_table(stream, sampler, seconds, device):
+    """Per-config energy: the fast forward against each dense forward of the same config (own
+    CUDA-core kernel, tcgen05 dense where it applies, cuBLAS TF32 off), each back to back for
+    `seconds` at the power cap, on the configs where the dense product is not trivially
+    HBM-bound (n = 64 / 128, fp32 and fp64)."""
+    import torch
+    import workloads
+    from paper_1907_07875_b200 import gft
+    out = []
+    for name, dtype in (("cfg4", "f32"), ("cfg4", "f64"), ("cfg5a", "f32"), ("cfg5b", "f32")):
+        cfg = workloads.config(name)
+        plan = gft.Plan.from_config(cfg, dtypes=(dtype,))
+        tdt = torch.float64 if dtype == "f64" else torch.float32
+        X = torch.randn(cfg.batch, cfg.n, generator=torch.Generator(device=device).manual_seed(cfg.seed),
+                        device=device, dtype=tdt)
+        Y = torch.empty_like(X)
+        U = torch.from_numpy(plan.basis()).to(device=device, dtype=tdt)
+        arms = {"fast": lambda: plan.forward(X, Y, stream), "dense": lambda: plan.dense_forward(X, Y, stream),
+                "cublas": lambda: torch.matmul(X, U, out=Y)}
+        dplan = None
+        if dtype == "f32":
+            dplan = gft.Plan.from_config(cfg, dtypes=(dtype,), dense_tc=True)
+            arms["dense_tc"] = lambda: dplan.dense_forward(X, Y, stream)
+        rows = energy_table(arms, cfg.batch, stream, sampler, seconds)
+        out.append({"config": name, "dtype": dtype, "arms": rows})
+        if dplan is not None:
+            dplan.close()
+        plan.close()
+        del X, Y
+    return out
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -712,6 +744,7 @@ def main():
         torch.backends.cuda.matmul.allow_tf32 = False
         tables = {"hbm_peak_gbs": hbm, "compute_peaks": peaks,
                   "energy": energy_table(arms, B, stream, sampler, args.energy_s),
+                  "energy_configs": energy_config_table(stream, sampler, 0.5 * args.energy_s, device),
                   "configs": config_table(args, stream, hbm, device, peaks),
                   "right_haar": right_haar_table(args, stream, hbm, device),
                   "paper_tab_runtime": paper_table(args, stream, hbm, device),

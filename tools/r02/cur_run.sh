@@ -1,4 +1,4 @@
-# r34: box-paced tile loads in the IO-split kernel (GFT_TC_BOX_PACE=1) vs one burst per tile
-timeout 900 python tools/r02/env_confirm.py cfg5b default GFT_TC_BOX_PACE=1 GFT_TC_BOX_PACE=1,GFT_TC_LOAD_PACE_NS=2550 \
-  GFT_TC_BOX_PACE=1,GFT_TC_LOAD_PACE_NS=2850 GFT_TC_BOX_PACE=1,GFT_TC_LOAD_PACE_NS=2400 > gpurun_out/r34_boxpace.log 2>&1
-timeout 900 python tools/r02/env_confirm.py rh1 default GFT_TC_BOX_PACE=1 GFT_TC_BOX_PACE=1,GFT_TC_LOAD_PACE_NS=2550 >> gpurun_out/r34_boxpace.log 2>&1
+# r36: warp-major tile numbering in the CUDA-core skeleton (GFT_SM_STRIPE=1): per-kernel A/B and in-step A/B
+for p in cfg5a cfg4 cfg2 cfg3; do timeout 600 python tools/r02/env_confirm.py $p default GFT_SM_STRIPE=1 >> gpurun_out/r36_burst.log 2>&1; done
+timeout 900 python tools/r02/step_ab.py default GFT_SM_STRIPE=1 > gpurun_out/r36_step_ab.log 2>&1
+timeout 900 python tools/r02/step_ab.py GFT_SM_STRIPE=1 default >> gpurun_out/r36_step_ab.log 2>&1
