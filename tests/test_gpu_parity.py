@@ -700,3 +700,23 @@ def test_tensor_core_f16x2_extreme_magnitudes(name):
     assert np.all(Yh[~nz] == 0)                                # zero rows stay exactly zero
     check_forward(Yh[nz], Xn[nz], lam_o, U_o, plan.basis(), 1e-5)
     assert oracle.relative_error(Xr.cpu().numpy()[nz], Xn[nz]).max() <= 2e-5
+
+
+def test_max_size_n256():
+    """The largest n with kernels (256): the 256-cycle plan (leaves up to 64, too big for the
+    tensor-core tiles at this row width, so the CUDA-core skeleton in stream mode) forward and
+    inverse on a ragged batch against the oracle, per eigen-cluster (the cycle's eigenvalues are
+    2-fold); the spectrum is also pinned to the closed form 2 - 2 cos(2 pi k / 256)."""
+    n = 256
+    s, d, w = workloads.cycle_graph(n)
+    plan = G.Plan(n, s, d, w, dtypes=("f32",))
+    assert "GFT_STREAM" in plan.kernel_source(G.K_FAST_FWD, "f32")
+    L = oracle.laplacian(n, s, d, w)
+    lam_o, U_o = oracle.gft_basis(L)
+    assert np.abs(lam_o - np.sort(2 - 2 * np.cos(2 * np.pi * np.arange(n) / n))).max() < 1e-10
+    X = torch.randn(1001, n, generator=torch.Generator().manual_seed(256), dtype=torch.float32)
+    Y = plan.forward(X.cuda())
+    Xr = plan.inverse(Y)
+    torch.cuda.synchronize()
+    check_forward(Y.cpu().numpy(), X.numpy(), lam_o, U_o, plan.basis(), TOL["f32"])
+    assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL["f32"]
