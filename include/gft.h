@@ -92,11 +92,15 @@ typedef struct {
                                        (Theorem 3 holds for it);
                                        every degree d_i = l_ii must be > 0 */
 #define GFT_FLAG_DENSE_TC 16u       /* the dense comparison kernels (gft_dense_*) run the whole
-                                       basis as one tcgen05 3xTF32 leaf (fp32, n % 4 == 0,
-                                       n >= 32)
+                                       basis as one tcgen05 leaf (fp32, n % 4 == 0, n >= 32)
                                        instead of CUDA-core FMA: the strongest dense baseline */
 #define GFT_FLAG_NO_TENSOR_CORES 4u /* fp32 leaves >= 32 stay on CUDA-core FMA instead of
-                                       tcgen05 3xTF32 micro-GEMMs (ablation / comparison) */
+                                       tcgen05 micro-GEMMs (ablation / comparison).  Tensor-core
+                                       leaves are fp32-accurate: the warp-specialised kernels
+                                       split each row (scaled by a power of two) into fp16
+                                       hi / lo parts and B into fp16 hi / lo, three kind::f16
+                                       passes with fp32 accumulation; the other variants use
+                                       3xTF32 */
 #define GFT_FLAG_NO_RIGHT_HAAR 32u  /* do not factor right Haar stages (PAPER.md:218-269,
                                        eq:right_gft) out of symmetry-free bipartite leaves
                                        whose Laplacian diagonal is constant; such leaves then
@@ -251,7 +255,8 @@ GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kin
  * CTA pair, pair with two compute warpgroups, warp-specialised pair, single CTA), same rule;
  * the choice is recorded like a geometry (gft_plan_tuning_get).  FMA-skeleton
  * candidates change no arithmetic, so they compute bit-identical outputs; tcgen05 variants
- * compute the same 3xTF32 products (fp32-accurate, not guaranteed bit-identical).
+ * compute the same split products (fp16x2 or 3xTF32; fp32-accurate, not guaranteed
+ * bit-identical).
  * X, Y: caller-owned device buffers of >= batch x n elements of `dtype` (16-byte aligned,
  *   distinct); X is read, Y is overwritten.  batch should exceed L2 (e.g. >= 256 MiB of rows)
  *   for the timing to reflect HBM streaming.  reps <= 0 selects 10.

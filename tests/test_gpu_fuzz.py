@@ -61,7 +61,11 @@ def _case(seed):
     return n, (s, d, w, loops, phi), dtype, kw, L
 
 
-@pytest.mark.parametrize("seed", range(40))
+# GFT_FUZZ_SEEDS=a:b widens the sweep (the default suite runs seeds 0..39)
+_SEEDS = range(*(int(v) for v in __import__("os").environ.get("GFT_FUZZ_SEEDS", "0:40").split(":")))
+
+
+@pytest.mark.parametrize("seed", _SEEDS)
 def test_random_plan_parity(seed):
     n, (s, d, w, loops, phi), dtype, kw, L = _case(seed)
     plan = G.Plan(n, s, d, w, loops, phi, dtypes=(dtype,), **kw)
