@@ -88,11 +88,19 @@ def test_random_plan_parity(seed):
     Xr = plan.inverse(Y)
     torch.cuda.synchronize()
     Y_o = oracle.forward(X.numpy(), U_o)
-    R = oracle.cluster_rotation(U_o, plan.basis(), lam_o)
-    # near-degenerate random spectra: allow the eigenvector conditioning eps |L| / gap
+    U_f = plan.basis()
+    # (1) the kernels apply exactly the plan's basis: against X U_f in fp64 at the dtype tolerance
+    ref_f = X.numpy().astype(np.float64) @ U_f
+    assert oracle.relative_error(Y.cpu().numpy(), ref_f).max() <= TOL[dtype], (seed, n, dtype, kw)
+    # (2) the plan's basis agrees with the oracle's per eigen-cluster; for random spectra with
+    # nearly (not exactly) repeated eigenvalues two correct eigensolves may differ by the
+    # Davis-Kahan bound sin(theta) <= |r|_2 / gap (r = residual L u - lambda u of either side;
+    # DESIGN.md reading A-5a), so the tolerance is the larger of that bound and the dtype's
+    R = oracle.cluster_rotation(U_o, U_f, lam_o)
     gaps = np.diff(lam_o)
     gap = gaps[gaps > 1e-9 * max(1, abs(lam_o).max())].min(initial=1.0)
-    tol = max(TOL[dtype], 1e-15 * np.abs(L).max() / gap)
+    res = np.abs(L @ U_o - U_o * lam_o).max() + plan.info()["residual"]
+    tol = max(TOL[dtype], np.sqrt(n) * res / gap)
     e = oracle.aligned_error(Y.cpu().numpy(), Y_o, R)
     assert e.max() <= tol, (seed, n, dtype, kw, plan.leaf_sizes(), e.max(), tol)
     assert oracle.relative_error(Xr.cpu().numpy(), X.numpy()).max() <= 2 * TOL[dtype]
