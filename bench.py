@@ -338,7 +338,8 @@ def energy_config_table(stream, sampler, seconds, device):
         if dtype == "f32":
             dplan = gft.Plan.from_config(cfg, dtypes=(dtype,), dense_tc=True)
             arms["dense_tc"] = lambda: dplan.dense_forward(X, Y, stream)
-        rows = energy_table(arms, cfg.batch, stream, sampler, seconds)
+        arms["copy"] = lambda: Y.copy_(X)
+        rows = energy_table(arms, cfg.batch, stream, sampler, seconds, bytes_per_step=2 * X.numel() * X.element_size())
         out.append({"config": name, "dtype": dtype, "arms": rows})
         if dplan is not None:
             dplan.close()
@@ -425,7 +426,7 @@ def right_haar_table(args, stream, hbm, device):
     return rows
 
 
-def energy_table(arms, signals_per_step, stream, sampler, seconds):
+def energy_table(arms, signals_per_step, stream, sampler, seconds, bytes_per_step=None):
     """Sustained throughput and energy per signal of the headline step (fast GFT) against the
     dense U^T x comparisons on the same inputs, each run back to back for `seconds` at the
     power cap (the paper's premise: one graph, many transforms).  Energy from
@@ -460,6 +461,8 @@ def energy_table(arms, signals_per_step, stream, sampler, seconds):
         if e0 is not None and e1 is not None:
             row["avg_power_w"] = round((e1 - e0) / 1e3 / (w1 - w0), 1)
             row["nj_per_signal"] = round((e1 - e0) * 1e6 / (n * signals_per_step), 3)
+            if bytes_per_step:
+                row["pj_per_byte"] = round((e1 - e0) * 1e9 / (n * bytes_per_step), 1)
         rows.append(row)
     return rows
 
@@ -739,11 +742,13 @@ def main():
                 "dense_fma": lambda: [(plans[i].dense_forward(X[i], Y[i], stream),
                                        plans[i].dense_inverse(Y[i], Z[i], stream)) for i in range(2)],
                 "cublas_tf32_off": lambda: [(torch.matmul(X[i], Us[i], out=Y[i]),
-                                             torch.matmul(Y[i], Us[i].t(), out=Z[i])) for i in range(2)]}
+                                             torch.matmul(Y[i], Us[i].t(), out=Z[i])) for i in range(2)],
+                # the same bytes moved by plain device copies: the data-movement energy floor
+                "copy": lambda: [(Y[i].copy_(X[i]), Z[i].copy_(Y[i])) for i in range(2)]}
         tf32 = torch.backends.cuda.matmul.allow_tf32
         torch.backends.cuda.matmul.allow_tf32 = False
         tables = {"hbm_peak_gbs": hbm, "compute_peaks": peaks,
-                  "energy": energy_table(arms, B, stream, sampler, args.energy_s),
+                  "energy": energy_table(arms, B, stream, sampler, args.energy_s, bytes_per_step=2 * sum(nbytes)),
                   "energy_configs": energy_config_table(stream, sampler, 0.5 * args.energy_s, device),
                   "configs": config_table(args, stream, hbm, device, peaks),
                   "right_haar": right_haar_table(args, stream, hbm, device),
@@ -790,6 +795,11 @@ def main():
         _, tms, tsc, tnj = sustain(tc_step, dense["tc"])
         sustained["dense_tc"] = {"ms_per_step": round(tms, 5), "fast_speedup": round(tms / sms, 3),
                                  "nj_per_signal": tnj, "sm_mhz": tsc["sm_mhz"]}
+        # the same bytes as plain device copies: what the box sustains for pure data movement
+        copy_step = lambda: [(Y[i].copy_(X[i]), Z[i].copy_(Y[i])) for i in range(2)]   # noqa: E731
+        _, cms, _, cnj = sustain(copy_step, ms_step)
+        sustained["copy"] = {"ms_per_step": round(cms, 5), "fast_frac_of_copy": round(cms / sms, 4),
+                             "nj_per_signal": cnj}
     for p in dplans:
         p.close()
     sampler.stop()

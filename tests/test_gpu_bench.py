@@ -43,5 +43,6 @@ def test_bench_driver_command():
     s = d["sustained"]
     assert s["seconds"] >= 2.0 and s["value"] > 0
     assert s["dense_tc"]["ms_per_step"] > 0 and s["dense_tc"]["fast_speedup"] > 0
+    assert s["copy"]["ms_per_step"] > 0 and 0.5 < s["copy"]["fast_frac_of_copy"] < 1.5
     k = d["kernels"]   # the in-run dense comparisons must survive the size limit
     assert set(k["dense_ms_per_step"]) == {"fma", "tc", "cublas"} and k["fast_vs_best_dense"] > 0
