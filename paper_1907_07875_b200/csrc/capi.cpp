@@ -8,6 +8,7 @@
 #include <new>
 #include <set>
 #include <string>
+#include <system_error>
 #include <thread>
 #include <vector>
 
@@ -65,6 +66,40 @@ void check_io(const void* a, const void* b) {
   if (!a || !b) gft::fail(GFT_ERR_INVALID_ARG, "NULL signal pointer");
   if ((reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
     gft::fail(GFT_ERR_ALIGNMENT, "X and Y must be 16-byte aligned");
+}
+
+// Compile kernels on one host thread each.  No exception may leave a std::thread (that would
+// call std::terminate, and the boundary never aborts): each worker records its failure, a
+// thread that cannot be started falls back to compiling on the caller's thread, and the first
+// failure is re-thrown on the caller's thread once every worker has joined.
+void compile_all(const std::vector<gft::Kernel*>& ks, bool cache) {
+  std::vector<gft::Error> errs(ks.size(), gft::Error{GFT_OK, ""});
+  auto one = [&](size_t i) noexcept {
+    try {
+      std::lock_guard<std::mutex> lk(ks[i]->mu);
+      gft::compile_kernel(*ks[i], cache);
+    } catch (const gft::Error& e) {
+      errs[i] = e;
+    } catch (const std::bad_alloc&) {
+      errs[i] = gft::Error{GFT_ERR_NOMEM, "out of host memory while compiling " + ks[i]->name};
+    } catch (const std::exception& e) {
+      errs[i] = gft::Error{GFT_ERR_COMPILE, std::string("compile failed: ") + e.what()};
+    } catch (...) {
+      errs[i] = gft::Error{GFT_ERR_COMPILE, "compile failed: unknown error"};
+    }
+  };
+  std::vector<std::thread> th;
+  th.reserve(ks.size());
+  for (size_t i = 0; i < ks.size(); ++i) {
+    try {
+      th.emplace_back(one, i);
+    } catch (const std::system_error&) {
+      one(i);   // no more threads: compile here
+    }
+  }
+  for (auto& t : th) t.join();
+  for (auto& e : errs)
+    if (e.status != GFT_OK) throw e;
 }
 
 gft_status run(gft_plan plan, int kind, const void* in, void* out, int64_t batch, gft_dtype dtype,
@@ -429,20 +464,7 @@ gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask)
     for (int kind = 0; kind < gft::K_NUM; ++kind)
       if (kinds_mask & (1u << kind)) ks.push_back(&kernel_of(plan, kind, dtype));
     const bool cache = !(plan->flags & GFT_FLAG_NO_CUBIN_CACHE);
-    std::vector<std::thread> th;
-    std::vector<gft::Error> errs(ks.size(), gft::Error{GFT_OK, ""});
-    for (size_t i = 0; i < ks.size(); ++i)
-      th.emplace_back([&, i] {
-        try {
-          std::lock_guard<std::mutex> lk(ks[i]->mu);
-          gft::compile_kernel(*ks[i], cache);
-        } catch (const gft::Error& e) {
-          errs[i] = e;
-        }
-      });
-    for (auto& t : th) t.join();
-    for (auto& e : errs)
-      if (e.status != GFT_OK) throw e;
+    compile_all(ks, cache);
   });
 }
 
@@ -463,20 +485,9 @@ struct TuneCand {
 };
 
 void compile_parallel(std::vector<TuneCand>& cs, bool cache) {
-  std::vector<gft::Error> errs(cs.size(), gft::Error{GFT_OK, ""});
-  std::vector<std::thread> th;
-  for (size_t i = 0; i < cs.size(); ++i)
-    th.emplace_back([&, i] {
-      try {
-        std::lock_guard<std::mutex> lk(cs[i].k->mu);
-        gft::compile_kernel(*cs[i].k, cache);
-      } catch (const gft::Error& e) {
-        errs[i] = e;
-      }
-    });
-  for (auto& t : th) t.join();
-  for (auto& e : errs)
-    if (e.status != GFT_OK) throw e;
+  std::vector<gft::Kernel*> ks;
+  for (auto& c : cs) ks.push_back(c.k.get());
+  compile_all(ks, cache);
 }
 
 // Measured tuning of one kernel slot (gft_plan_tune / gft_filter_tune); out4 = {R, stages,
