@@ -205,7 +205,9 @@ GFT_API gft_status gft_dense_inverse(gft_plan plan, const void* Y, void* X, int6
  * so H2D, compute and D2H of neighbouring chunks overlap on both copy directions.
  * `workspace` is a device buffer of `workspace_bytes` >= 2 * chunk_rows * n * sizeof(dtype)
  * (chunk_rows > 0; 3-4 slots of 2^18 rows measured best on PCIe Gen5).
- * Concurrent calls from several host threads are serialised while they enqueue.  Work is
+ * Concurrent calls from several host threads are serialised while they enqueue.  The caller
+ * owns `workspace`; calls that may be in flight together (issued on different streams) need
+ * distinct workspaces -- consecutive calls on ONE stream may share it (stream order).  Work is
  * ordered after prior work on `stream` and `stream` is made to wait for completion;
  * host buffers must stay valid until `stream` completes (use pinned memory for overlap).
  * direction: 0 = forward, 1 = inverse. */

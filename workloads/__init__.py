@@ -220,6 +220,20 @@ def signals(cfg: Config, batch: Optional[int] = None, dtype: str = "f32", seed: 
     raise ValueError(cfg.signal)
 
 
+def signals_device(n: int, batch: int, dtype: str = "f32", seed: int = 0, device: str = "cuda"):
+    """Seeded i.i.d. N(0,1) [batch, n] signals drawn ON the device (torch's CUDA generator),
+    for inputs too large to draw on the host (the > 4 GiB / > 2^30-row edge-case tests); drawn
+    in slabs so no temporary exceeds 1 GiB."""
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    X = torch.empty(batch, n, dtype=tdt, device=device)
+    slab = max(1, (1 << 28) // n)
+    for r0 in range(0, batch, slab):
+        X[r0:r0 + slab].normal_(generator=g)
+    return X
+
+
 def random_symmetric_graph(rng: np.random.Generator, n: int, density: float = 0.5,
                            loops: bool = True, fixed_frac: float = 0.3, negative: bool = False):
     """Random phi-symmetric graph for property tests: draws a random involution phi and
