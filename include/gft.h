@@ -247,7 +247,7 @@ GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kin
  * fixes only the arithmetic).  For every kernel kind in kinds_mask (bits as in
  * gft_plan_compile; 0 = fast-fwd | fast-inv) that runs on the FMA skeleton:
  *   1. with GFT_TUNE_GEOMETRY in flags, the kernel is regenerated for every warp-tile geometry
- *      (rows per thread R in {1,2,4,8}, stages {2,3,4}, warps {4,8,12}; 1-32 KiB tiles that
+ *      (rows per thread R in {1,2,4,8}, stages {2,3,4}, warps {1,2,3,4,8,12}; 1-32 KiB tiles that
  *      fit shared memory) and the fastest geometry is kept for step 2;
  *   2. the kernel is regenerated with each per-tile pacing in {0, 150, 300, 450} ns;
  * candidates are compiled in parallel (NVRTC) and timed twice over `reps` back-to-back
@@ -259,6 +259,11 @@ GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kin
  * candidates change no arithmetic, so they compute bit-identical outputs; tcgen05 variants
  * compute the same split products (fp16x2 or 3xTF32; fp32-accurate, not guaranteed
  * bit-identical).
+ * With GFT_TUNE_SUSTAINED in flags the current kernel first runs back to back for >= 1 s and
+ * every timing pass is 10 x reps launches, so candidates are compared in the state a long
+ * stream of transforms sees: on a GPU that reaches its power cap the ranking differs from the
+ * burst ranking (1-3 warp, paced geometries lost 7-12% there and won on an uncapped GPU;
+ * DESIGN.md §4 "Burst vs sustained").  Tune in the regime the plan will serve.
  * X, Y: caller-owned device buffers of >= batch x n elements of `dtype` (16-byte aligned,
  *   distinct); X is read, Y is overwritten.  batch should exceed L2 (e.g. >= 256 MiB of rows)
  *   for the timing to reflect HBM streaming.  reps <= 0 selects 10.
@@ -270,6 +275,7 @@ GFT_API gft_status gft_plan_compile(gft_plan plan, gft_dtype dtype, uint32_t kin
  * Errors: GFT_ERR_INVALID_ARG (NULL / bad sizes / unknown flags), GFT_ERR_ALIGNMENT,
  * GFT_ERR_UNSUPPORTED (dtype not prepared), GFT_ERR_COMPILE, GFT_ERR_NO_DEVICE / GFT_ERR_CUDA. */
 #define GFT_TUNE_GEOMETRY 1u
+#define GFT_TUNE_SUSTAINED 2u
 GFT_API gft_status gft_plan_tune(gft_plan plan, gft_dtype dtype, uint32_t kinds_mask, uint32_t flags,
                                  const void* X, void* Y, int64_t batch, int32_t reps, gft_stream stream,
                                  int32_t* choice_out);

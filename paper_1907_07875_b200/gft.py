@@ -279,6 +279,7 @@ def gft_plan_compile(h, dtype, kinds_mask=0):
 
 
 GFT_TUNE_GEOMETRY = 1
+GFT_TUNE_SUSTAINED = 2
 
 
 def gft_plan_tune(h, dtype, kinds_mask, X, Y, batch, reps=0, stream=None, flags=0):
@@ -442,14 +443,14 @@ class Filter:
         gft_filter_apply(self._h, X, Y, X.shape[0], dt, stream)
         return Y
 
-    def tune(self, X, Y=None, dtype="f32", reps=0, stream=None, geometry=False):
+    def tune(self, X, Y=None, dtype="f32", reps=0, stream=None, geometry=False, sustained=False):
         """gft_filter_tune on the device tensors X -> Y: (R, stages, warps, pace_ns) kept, or
-        None for a tensor-core filter kernel."""
+        None for a tensor-core filter kernel.  sustained=True: GFT_TUNE_SUSTAINED."""
         import torch
         if Y is None:
             Y = torch.empty_like(X)
         return gft_filter_tune(self._h, dtype, X, Y, X.shape[0], reps, stream,
-                               GFT_TUNE_GEOMETRY if geometry else 0)
+                               (GFT_TUNE_GEOMETRY if geometry else 0) | (GFT_TUNE_SUSTAINED if sustained else 0))
 
     def kernel_name(self, dtype="f32"):
         return gft_filter_kernel_name(self._h, dtype)
@@ -574,9 +575,10 @@ class Plan:
         gft_plan_compile(self._h, dtype, sum(1 << k for k in kinds))
 
     def tune(self, dtype="f32", kinds=(0, 1), X=None, Y=None, batch=None, reps=0, stream=None,
-             geometry=False):
+             geometry=False, sustained=False):
         """gft_plan_tune on the device tensors X -> Y (or on scratch buffers of `batch` rows,
-        default 256 MiB of rows, > L2); geometry=True also searches the warp-tile geometry.
+        default 256 MiB of rows, > L2); geometry=True also searches the warp-tile geometry;
+        sustained=True (GFT_TUNE_SUSTAINED) times the candidates after >= 1 s of load.
         Returns {kind: (R, stages, warps, pace_ns)} for the kinds on the FMA skeleton."""
         import torch
         tdt = torch.float64 if dtype == "f64" else torch.float32
@@ -589,7 +591,7 @@ class Plan:
         if X.dtype != tdt or Y.dtype != tdt or X.shape[1] != self.n or Y.shape != X.shape:
             raise ValueError("X, Y: [batch, %d] tensors of the tuned dtype" % self.n)
         return gft_plan_tune(self._h, dtype, sum(1 << k for k in kinds), X, Y, X.shape[0], reps, stream,
-                             GFT_TUNE_GEOMETRY if geometry else 0)
+                             (GFT_TUNE_GEOMETRY if geometry else 0) | (GFT_TUNE_SUSTAINED if sustained else 0))
 
     def tuning(self, dtype="f32", kinds=(0, 1, 2, 3)):
         """Tuning records {kind: (R, stages, warps, pace_ns, tc_variant)}."""

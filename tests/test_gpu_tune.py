@@ -60,11 +60,34 @@ def test_tune_errors():
     with pytest.raises(gft.GFTError, match="UNSUPPORTED"):
         gft.gft_plan_tune(plan._h, "f64", 3, X, torch.empty_like(X), 4096)
     with pytest.raises(gft.GFTError, match="INVALID_ARG"):
-        gft.gft_plan_tune(plan._h, "f32", 3, X, torch.empty_like(X), 4096, flags=2)
+        gft.gft_plan_tune(plan._h, "f32", 3, X, torch.empty_like(X), 4096, flags=8)   # unknown flag bit
     # the plan still works and matches the oracle-free identity round trip
     Y = plan.forward(X)
     Z = plan.inverse(Y)
     assert float((Z - X).norm() / X.norm()) < 1e-5
+    plan.close()
+
+
+def test_tune_sustained_regime_bit_identical():
+    """GFT_TUNE_SUSTAINED: the current kernel runs >= 1 s before the candidates are timed (10 x
+    reps launches per pass), so the ranking is the sustained one; whatever pacing is kept, the
+    outputs stay bit-identical, and the call takes at least that second."""
+    import time
+    cfg = workloads.config("cfg2")
+    plan = gft.Plan.from_config(cfg, dtypes=("f32",))
+    g = torch.Generator(device="cuda").manual_seed(5)
+    X = torch.randn((1 << 20) + 3, cfg.n, generator=g, device="cuda")
+    Y0 = plan.forward(X)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    paces = plan.tune("f32", (0,), X=X, reps=2, sustained=True)
+    assert time.perf_counter() - t0 >= 1.0
+    assert set(paces) == {0} and paces[0][3] in CAND
+    Y1 = plan.forward(X)
+    torch.cuda.synchronize()
+    assert torch.equal(Y0, Y1)
+    with pytest.raises(gft.GFTError, match="INVALID_ARG"):
+        gft.gft_plan_tune(plan._h, "f32", 1, X, torch.empty_like(X), X.shape[0], flags=4)   # unknown flag
     plan.close()
 
 

@@ -3,7 +3,10 @@
 sweeps disagree with the step (cfg5a fwd with 2,2,3,150,2: 0.84 of HBM when launched after
 itself, fast after another kernel).  Each argument is "fwd=R,S,W,pace,obuf;inv=R,S,W,pace,obuf"
 (either part optional, "default" = tuning.tsv); candidates are timed in interleaved rounds
-(best of 3 x 20 steps per round, 3 rounds); prints the median step time and the 5a share."""
+(best of 3 x 20 steps per round, 3 rounds); prints the median step time and the 5a share.
+NOTE (r44-r48): with many candidates the GPU is at the power cap from the second round on, so
+the medians are SUSTAINED-regime numbers (default 0.527 ms here vs 0.4986 ms for bench.py's
+burst on the same box); step_sweep2.py measures both regimes per candidate."""
 import json
 import os
 import statistics
@@ -40,6 +43,14 @@ def make(spec):
 
 cands = sys.argv[1:] or ["default"]
 made = [(c, make(c)) for c in cands]
+# every candidate computes the same rows bit for bit (same FFMA order per row)
+ref_y = made[0][1][0].forward(XA)
+ref_z = made[0][1][1].inverse(ref_y)
+for c, pl in made[1:]:
+    y = pl[0].forward(XA)
+    assert torch.equal(y, ref_y), c
+    assert torch.equal(pl[1].inverse(y), ref_z), c
+del ref_y, ref_z
 
 
 def timed(pl):
@@ -63,6 +74,26 @@ def timed(pl):
     return best
 
 
+def copy_step_ms():
+    """the same bytes as plain device copies (what this box moves for pure data movement)"""
+    def step():
+        YA.copy_(XA); YB.copy_(XB); ZA.copy_(YA); ZB.copy_(YB)
+    for _ in range(5):
+        step()
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(20):
+            step()
+        b.record()
+        b.synchronize()
+        best = min(best, a.elapsed_time(b) / 20)
+    return best
+
+
+print(json.dumps({"copy_step_ms": round(copy_step_ms(), 5)}), flush=True)
 res = {c: [] for c in cands}
 for _ in range(3):
     for c, pl in made:
