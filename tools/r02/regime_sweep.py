@@ -2,7 +2,9 @@
 burst (idle pause, 5 warm-up, 20 timed pairs) and sustained (1.5 s of pairs, then the mean of the
 next 3 x 200 pairs at the power cap).  python regime_sweep.py <cfg> <f32|f64> cand...  with cand =
 "default" | "copy" | "R,S,W,pace,obuf" (both directions).  Interleaved rounds, medians; GB/s =
-algorithmic bytes of the pair / time, and the fraction of the copy pair measured the same way."""
+algorithmic bytes of the pair / time, and the fraction of the copy pair measured the same way.
+SWEEP_FILTER=1: the fused filter (X -> Y, then Y -> Z) instead of the forward / inverse pair, the
+geometry set through the GFT_TUNE_* / GFT_PACE_NS / GFT_FMA_OBUF knobs at kernel generation."""
 import json
 import os
 import statistics
@@ -24,9 +26,27 @@ nbytes = 2 * 2 * X.numel() * X.element_size()
 stream = torch.cuda.current_stream()
 
 
+FILTER = os.environ.get("SWEEP_FILTER") == "1"
+
+
+def make_filter(spec):
+    import numpy as np
+    keys = ("GFT_TUNE_R", "GFT_TUNE_STAGES", "GFT_TUNE_WARPS", "GFT_PACE_NS", "GFT_FMA_OBUF")
+    if spec != "default":
+        for k, v in zip(keys, spec.split(",")):
+            os.environ[k] = v
+    p = gft.Plan.from_config(cfg, dtypes=(dt,))
+    f = gft.Filter(p, np.exp(-0.5 * p.eigenvalues()), dtypes=(dt,), no_cubin_cache=spec != "default")
+    for k in keys:
+        os.environ.pop(k, None)
+    return f
+
+
 def make(spec):
     if spec == "copy":
         return None
+    if FILTER:
+        return make_filter(spec)
     if spec == "default":
         return gft.Plan.from_config(cfg, dtypes=(dt,))
     R, S, W, pace, ob = (int(v) for v in spec.split(","))
@@ -41,6 +61,12 @@ def stepper(p):
     if p is None:
         def step():
             Y.copy_(X); Z.copy_(Y)
+        return step
+
+    if FILTER:
+        def step():
+            p.apply(X, Y, stream)
+            p.apply(Y, Z, stream)
         return step
 
     def step():
@@ -93,7 +119,7 @@ cb = statistics.median(res["copy"][0]) if "copy" in res else None
 cs = statistics.median(res["copy"][1]) if "copy" in res else None
 for c, p in made:
     b, s = statistics.median(res[c][0]), statistics.median(res[c][1])
-    print(json.dumps({"cfg": name, "dtype": dt, "cand": c, "burst_gbs": round(nbytes / b / 1e6, 1),
+    print(json.dumps({"cfg": name + ("_filter" if FILTER else ""), "dtype": dt, "cand": c, "burst_gbs": round(nbytes / b / 1e6, 1),
                       "sustained_gbs": round(nbytes / s / 1e6, 1),
                       "burst_vs_copy": round(cb / b, 4) if cb else None,
                       "sustained_vs_copy": round(cs / s, 4) if cs else None}), flush=True)
