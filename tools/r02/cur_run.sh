@@ -1,3 +1,6 @@
-# r59: extended randomised parity sweep, seeds 300..800 (500 new random plans)
+# r60: brute-force burst sweep of cfg5a fwd / inv geometry inside the headline step
 mkdir -p gpurun_out
-GFT_FUZZ_SEEDS=300:800 timeout 2400 python -m pytest tests/test_gpu_fuzz.py -q > gpurun_out/r59_fuzz.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r59_fuzz.log
+nvidia-smi --query-gpu=uuid --format=csv,noheader > gpurun_out/r60_fwd.log
+timeout 2400 python tools/r02/step_sweep3.py fwd >> gpurun_out/r60_fwd.log 2>&1
+nvidia-smi --query-gpu=uuid --format=csv,noheader > gpurun_out/r60_inv.log
+timeout 2400 python tools/r02/step_sweep3.py inv >> gpurun_out/r60_inv.log 2>&1
