@@ -1,8 +1,9 @@
-# r66: tcgen05 load pacing: spin on %globaltimer instead of __nanosleep(64) in pace_load (cfg5b, rh0)
+# r67: e2e arm: equal-byte chunks per graph and the order of the graphs (fill / drain bubble)
 mkdir -p gpurun_out
-L=gpurun_out/r66_tc_spin.log; nvidia-smi --query-gpu=uuid --format=csv,noheader > $L
-python tools/r02/tc_probe.py cfg5b 1.5 >> $L 2>&1
-for P in 2500 2600 2704 2800 2900 3000 3100; do
-GFT_TC_PACE_SPIN=1 GFT_TC_LOAD_PACE_NS=$P python tools/r02/tc_probe.py cfg5b 1.5 >> $L 2>&1
-done
-python tools/r02/tc_probe.py cfg5b 1.5 >> $L 2>&1
+L=gpurun_out/r67_e2e.log; nvidia-smi --query-gpu=uuid --format=csv,noheader > $L
+python tools/r02/e2e_var.py >> $L 2>&1
+E2E_CHUNK_BYTES=33554432 python tools/r02/e2e_var.py >> $L 2>&1
+E2E_CHUNK_BYTES=16777216 python tools/r02/e2e_var.py >> $L 2>&1
+E2E_ORDER=10 python tools/r02/e2e_var.py >> $L 2>&1
+E2E_CHUNK_BYTES=33554432 E2E_ORDER=10 python tools/r02/e2e_var.py >> $L 2>&1
+python tools/r02/e2e_var.py >> $L 2>&1

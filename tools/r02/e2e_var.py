@@ -20,7 +20,11 @@ Yh = [torch.empty_like(x).pin_memory() for x in Xh]
 Zh = [torch.empty_like(x).pin_memory() for x in Xh]
 chunk = int(os.environ.get("E2E_CHUNK", 1 << 17))
 slots = int(os.environ.get("E2E_SLOTS", 4))
-wsb = [torch.empty(slots * chunk * c.n, dtype=torch.float32, device=dev) for c in cfgs]
+# E2E_CHUNK_BYTES: chunks of equal BYTES for both graphs (rows = bytes / row bytes) instead of equal rows
+cbytes = int(os.environ.get("E2E_CHUNK_BYTES", 0))
+chunks = [cbytes // (c.n * 4) if cbytes else chunk for c in cfgs]
+order = [int(v) for v in os.environ.get("E2E_ORDER", "01")]   # graph order inside each direction
+wsb = [torch.empty(slots * ch * c.n, dtype=torch.float32, device=dev) for c, ch in zip(cfgs, chunks)]
 stream = torch.cuda.current_stream()
 gs = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
 step_bytes = sum(2 * c.batch * c.n * 4 for c in cfgs)
@@ -30,8 +34,8 @@ def e2e_step():
     for s in gs:
         s.wait_stream(stream)
     for d in (0, 1):
-        for i in range(2):
-            plans[i].execute_host(d, Xh[i] if d == 0 else Yh[i], Yh[i] if d == 0 else Zh[i], wsb[i], chunk, gs[i])
+        for i in order:
+            plans[i].execute_host(d, Xh[i] if d == 0 else Yh[i], Yh[i] if d == 0 else Zh[i], wsb[i], chunks[i], gs[i])
     for s in gs:
         stream.wait_stream(s)
 
@@ -47,6 +51,6 @@ for r in range(6):
     b.record(stream)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / 3
-    print(json.dumps({"round": r, "chunk": chunk, "slots": slots, "ms": round(ms, 3),
+    print(json.dumps({"round": r, "chunks": chunks, "order": order, "slots": slots, "ms": round(ms, 3),
                       "each_dir_gbs": round(step_bytes / (ms * 1e6), 1)}), flush=True)
 print(json.dumps({"pcie_roof_after": bench.pcie_roof(dev)}), flush=True)
