@@ -27,6 +27,7 @@ stream = torch.cuda.current_stream()
 
 
 FILTER = os.environ.get("SWEEP_FILTER") == "1"
+MODE = os.environ.get("SWEEP_MODE", "pair")   # pair | fwd | inv (forward-only / inverse-only streams)
 
 
 def make_filter(spec):
@@ -67,6 +68,17 @@ def stepper(p):
         def step():
             p.apply(X, Y, stream)
             p.apply(Y, Z, stream)
+        return step
+
+    if MODE == "fwd":      # forward-only stream (two launches per step, like the pair)
+        def step():
+            p.forward(X, Y, stream)
+            p.forward(X, Z, stream)
+        return step
+    if MODE == "inv":
+        def step():
+            p.inverse(X, Y, stream)
+            p.inverse(X, Z, stream)
         return step
 
     def step():
@@ -119,7 +131,7 @@ cb = statistics.median(res["copy"][0]) if "copy" in res else None
 cs = statistics.median(res["copy"][1]) if "copy" in res else None
 for c, p in made:
     b, s = statistics.median(res[c][0]), statistics.median(res[c][1])
-    print(json.dumps({"cfg": name + ("_filter" if FILTER else ""), "dtype": dt, "cand": c, "burst_gbs": round(nbytes / b / 1e6, 1),
+    print(json.dumps({"cfg": name + ("_filter" if FILTER else "") + ("" if MODE == "pair" else "_" + MODE), "dtype": dt, "cand": c, "burst_gbs": round(nbytes / b / 1e6, 1),
                       "sustained_gbs": round(nbytes / s / 1e6, 1),
                       "burst_vs_copy": round(cb / b, 4) if cb else None,
                       "sustained_vs_copy": round(cs / s, 4) if cs else None}), flush=True)
