@@ -149,6 +149,25 @@ def _dev_ptr(t):
     return t.data_ptr()
 
 
+
+def _check_pair(a, b, n, cuda):
+    """The output tensor `b` of a call must mirror the input `a`: same device kind, shape
+    [batch, n], dtype, contiguous -- the library writes batch x n elements through its raw
+    pointer, so a smaller / strided / host-vs-device mismatch would corrupt memory."""
+    import torch
+    where = "CUDA" if cuda else "host"
+    for t, nm in ((a, "input"), (b, "output")):
+        if not isinstance(t, torch.Tensor) or t.is_cuda != cuda:
+            raise ValueError("%s: a %s tensor is required" % (nm, where))
+        if t.dim() != 2 or t.shape[1] != n or not t.is_contiguous():
+            raise ValueError("%s: expected a contiguous [batch, %d] tensor" % (nm, n))
+        if t.dtype is not torch.float32 and t.dtype is not torch.float64:
+            raise ValueError("%s: float32 / float64 tensors only" % nm)
+    if b.shape != a.shape or b.dtype != a.dtype:
+        raise ValueError("input and output must have the same shape and dtype")
+    if cuda and a.device != b.device:
+        raise ValueError("input and output must be on the same device")
+
 _raw_stream = None
 
 
@@ -439,6 +458,7 @@ class Filter:
             raise ValueError("expected a contiguous CUDA [batch, %d] tensor" % self.n)
         if Y is None:
             Y = torch.empty_like(X)
+        _check_pair(X, Y, self.n, cuda=True)
         dt = GFT_F64 if X.dtype == torch.float64 else GFT_F32
         gft_filter_apply(self._h, X, Y, X.shape[0], dt, stream)
         return Y
@@ -449,6 +469,7 @@ class Filter:
         import torch
         if Y is None:
             Y = torch.empty_like(X)
+        _check_pair(X, Y, self.n, cuda=True)
         return gft_filter_tune(self._h, dtype, X, Y, X.shape[0], reps, stream,
                                (GFT_TUNE_GEOMETRY if geometry else 0) | (GFT_TUNE_SUSTAINED if sustained else 0))
 
@@ -561,11 +582,15 @@ class Plan:
         adt = a.dtype
         if b.dtype != adt or (adt is not torch.float32 and adt is not torch.float64):
             raise ValueError("float32/float64 tensors of equal dtype required")
+        _check_pair(a, b, self.n, cuda=True)
         fn(self._h, a, b, shape[0], GFT_F64 if adt is torch.float64 else GFT_F32, stream)
         return b
 
     def execute_host(self, direction, in_host, out_host, workspace, chunk_rows, stream=None):
         import torch
+        _check_pair(in_host, out_host, self.n, cuda=False)
+        if not isinstance(workspace, torch.Tensor) or not workspace.is_cuda or not workspace.is_contiguous():
+            raise ValueError("workspace: a contiguous CUDA tensor is required")
         dt = GFT_F64 if in_host.dtype == torch.float64 else GFT_F32
         gft_execute_host(self._h, direction, in_host, out_host, in_host.shape[0], dt, workspace,
                          workspace.numel() * workspace.element_size(), chunk_rows, stream)
@@ -590,6 +615,7 @@ class Plan:
             Y = torch.empty_like(X)
         if X.dtype != tdt or Y.dtype != tdt or X.shape[1] != self.n or Y.shape != X.shape:
             raise ValueError("X, Y: [batch, %d] tensors of the tuned dtype" % self.n)
+        _check_pair(X, Y, self.n, cuda=True)
         return gft_plan_tune(self._h, dtype, sum(1 << k for k in kinds), X, Y, X.shape[0], reps, stream,
                              (GFT_TUNE_GEOMETRY if geometry else 0) | (GFT_TUNE_SUSTAINED if sustained else 0))
 

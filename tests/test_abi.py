@@ -254,3 +254,26 @@ def test_packed_ffma2_units_opt_in(monkeypatch):
         assert "0xBF8000003F800000ull" in src
     c1 = G.Plan.from_config(workloads.config("cfg1"), dtypes=("f32",))
     assert c1.kernel_source(0, "f32").count("fma.rn.f32x2") == 0
+
+
+def test_binding_validates_output_tensors():
+    """The binding passes raw pointers: an output tensor that does not mirror the input (host vs
+    device, shape, dtype, strides) must be refused before the library is called."""
+    torch = pytest.importorskip("torch")
+    p = G.Plan.from_config(workloads.config("cfg1"), dtypes=("f32",), host_only=True)
+    a = torch.zeros(16, 8)
+    G._check_pair(a, torch.empty_like(a), 8, cuda=False)
+    G._check_pair(a, a, 8, cuda=False)                       # in place
+    for bad in (torch.zeros(8, 8), torch.zeros(16, 8, dtype=torch.float64), torch.zeros(8, 16).t(),
+                torch.zeros(16, 8, dtype=torch.float16), torch.zeros(16 * 8)):
+        with pytest.raises(ValueError):
+            G._check_pair(a, bad, 8, cuda=False)
+    with pytest.raises(ValueError):
+        G._check_pair(a, torch.empty_like(a), 8, cuda=True)  # device call with host tensors
+    with pytest.raises(ValueError):
+        p.forward(a)                                         # host tensor to a device entry point
+    ws = torch.zeros(2 * 16 * 8)
+    with pytest.raises(ValueError):
+        p.execute_host(0, a, torch.zeros(8, 8), ws, 16)      # output smaller than the input
+    with pytest.raises(ValueError):
+        p.execute_host(0, a, torch.empty_like(a), ws, 16)    # workspace must be a CUDA tensor
