@@ -1,11 +1,7 @@
-# r68: forward-only / inverse-only streams (not pairs) for the few-warp paced geometries, both regimes
+# r69: validation after the binding's output-tensor checks (full GPU suite, smoke, driver bench, reference arm, host overhead)
 mkdir -p gpurun_out
-L=gpurun_out/r68_fwd_only.log; nvidia-smi --query-gpu=uuid --format=csv,noheader > $L
-for M in fwd inv pair; do
-SWEEP_MODE=$M SWEEP_BATCH=16777216 python tools/r02/regime_sweep.py cfg1 f32 copy default 8,2,8,150,0 8,3,4,0,0 8,3,3,100,2 8,3,3,200,2 >> $L 2>&1
-done
-for M in fwd inv; do
-SWEEP_MODE=$M python tools/r02/regime_sweep.py cfg2 f32 copy default 4,2,8,0,0 >> $L 2>&1
-SWEEP_MODE=$M python tools/r02/regime_sweep.py cfg4 f32 copy default 1,2,8,0,0 >> $L 2>&1
-SWEEP_MODE=$M python tools/r02/regime_sweep.py cfg3 f32 copy default 4,2,6,0,0 >> $L 2>&1
-done
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r69_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r69_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r69_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r69_smoke.log
+timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/r69_bench.log 2> gpurun_out/r69_bench.err
+timeout 600 python bench.py --impl reference --gpus 1 --steps 3 --warmup 3 > gpurun_out/r69_ref.log 2>&1
+timeout 300 python tools/host_overhead_probe.py > gpurun_out/r69_host.log 2>&1
