@@ -326,6 +326,8 @@ def gft_plan_tuning_get(h, dtype, kind):
 
 def gft_plan_tuning_set(h, dtype, kind, rec):
     """rec: (R, stages, warps, pace_ns[, tc_variant]) -- a 4-tuple means tc_variant -1."""
+    if len(rec) not in (4, 5):
+        raise ValueError("tuning record: (R, stages, warps, pace_ns[, tc_variant])")
     vals = [int(v) for v in rec] + ([-1] if len(rec) == 4 else [])
     _check(lib().gft_plan_tuning_set(h, _dtype_code(dtype), int(kind), (ctypes.c_int32 * 5)(*vals)))
 
@@ -381,6 +383,8 @@ def gft_plan_launch_config(h, kind, dtype, batch):
 def gft_laplacian(n, src, dst, w, self_loops=None):
     src, dst, w = _edges_arrays(src, dst, w)
     s = None if self_loops is None else np.ascontiguousarray(self_loops, dtype=np.float64)
+    if s is not None and s.shape != (n,):
+        raise ValueError("self_loops must have length n")
     L = np.empty((n, n), dtype=np.float64)
     _check(lib().gft_laplacian(int(n), len(src), _ptr(src), _ptr(dst), _ptr(w), _ptr(s), _ptr(L)))
     return L
@@ -390,6 +394,8 @@ def gft_decompose(L, phi, sym_rtol=1e-12):
     L = np.ascontiguousarray(L, dtype=np.float64)
     n = L.shape[0]
     phi = np.ascontiguousarray(phi, dtype=np.int32)
+    if L.ndim != 2 or L.shape != (n, n) or phi.shape != (n,):
+        raise ValueError("L must be n x n and phi of length n")
     p = int(np.sum(phi > np.arange(n)))
     Lp = np.empty((n - p, n - p), dtype=np.float64)
     Lm = np.empty((p, p), dtype=np.float64)
@@ -402,6 +408,8 @@ def gft_decompose(L, phi, sym_rtol=1e-12):
 def gft_find_involution(L, rtol=1e-10, budget=1000000):
     L = np.ascontiguousarray(L, dtype=np.float64)
     n = L.shape[0]
+    if L.ndim != 2 or L.shape != (n, n):
+        raise ValueError("L must be n x n")
     phi = np.empty(n, dtype=np.int32)
     p, comp = c_int32(), c_int32()
     _check(lib().gft_find_involution(n, _ptr(L), float(rtol), int(budget), _ptr(phi), ctypes.byref(p),

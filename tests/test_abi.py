@@ -277,3 +277,19 @@ def test_binding_validates_output_tensors():
         p.execute_host(0, a, torch.zeros(8, 8), ws, 16)      # output smaller than the input
     with pytest.raises(ValueError):
         p.execute_host(0, a, torch.empty_like(a), ws, 16)    # workspace must be a CUDA tensor
+
+
+def test_binding_validates_host_array_sizes():
+    """Array lengths the C side cannot see are checked by the binding."""
+    with pytest.raises(ValueError):
+        G.gft_laplacian(4, [0, 1], [1, 2], [1.0, 1.0], self_loops=[0.5, 0.5])      # loops shorter than n
+    L = G.gft_laplacian(4, [0, 1, 2], [1, 2, 3], [1.0, 1.0, 1.0])
+    with pytest.raises(ValueError):
+        G.gft_decompose(L, [3, 2, 1])                                             # phi shorter than n
+    with pytest.raises(ValueError):
+        G.gft_decompose(L[:3], [3, 2, 1, 0])                                      # L not square
+    with pytest.raises(ValueError):
+        G.gft_find_involution(L[:, :3])
+    p = G.Plan.from_config(workloads.config("cfg1"), dtypes=("f32",))
+    with pytest.raises(ValueError):
+        p.set_tuning({0: (8, 3, 4)}, "f32")                                        # record too short
