@@ -174,6 +174,26 @@ def time_kernel(fn, stream, warmup, iters):
     return s.elapsed_time(e) / iters
 
 
+def time_kernel_stats(fn, stream, warmup=5, rounds=5, iters=10):
+    """>= 5 warm-up calls, then >= 50 timed calls (rounds x iters back-to-back
+    launches, one event pair per round so launches inside a round keep their PDL overlap);
+    returns (median, min) of the per-round mean time per call in ms."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    per = []
+    for _ in range(rounds):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(iters):
+            fn()
+        e.record(stream)
+        e.synchronize()
+        per.append(s.elapsed_time(e) / iters)
+    return statistics.median(per), min(per)
+
+
 def time_graph(fn, iters):
     """Per-launch device time of `fn` replayed from a captured CUDA graph (launch-bound cases)."""
     import torch
@@ -194,8 +214,16 @@ def time_graph(fn, iters):
 
 
 def rec(ms, nbytes, hbm, signals):
-    return {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1), "frac": round(nbytes / ms / 1e6 / hbm, 4),
-            "signals_per_s": signals / ms * 1e3}
+    """ms: a time per call, or (median, min) from time_kernel_stats (the median is reported as
+    `ms` and feeds every derived figure; `ms_min` beside it)."""
+    ms_min = None
+    if isinstance(ms, tuple):
+        ms, ms_min = ms
+    out = {"ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1), "frac": round(nbytes / ms / 1e6 / hbm, 4),
+           "signals_per_s": signals / ms * 1e3}
+    if ms_min is not None:
+        out["ms_min"] = round(ms_min, 5)
+    return out
 
 
 # ------------------------------------------------------------------------------ side tables
@@ -206,6 +234,9 @@ def config_table(args, stream, hbm, device, peaks):
     import workloads
     from paper_1907_07875_b200 import gft
     rows = []
+
+    def tk(fn):   # (median, min) over 5 rounds of max(10, table_iters / 2) calls after 5 warm-up calls
+        return time_kernel_stats(fn, stream, 5, 5, max(10, args.table_iters // 2))
     for name, dtype in (("cfg1", "f32"), ("cfg1@2^24", "f32"), ("cfg2", "f32"), ("cfg2b", "f32"),
                         ("cfg3", "f32"), ("cfg4", "f32"), ("cfg4", "f64"), ("cfg5a", "f32"), ("cfg5b", "f32")):
         cfg = workloads.config(name.split("@")[0])
@@ -221,8 +252,7 @@ def config_table(args, stream, hbm, device, peaks):
                "units_per_level": plan.info()["units_per_level"], "leaves": plan.leaf_sizes(),
                "kernel_fwd": plan.kernel_name(0, dtype), "kernel_dense_fwd": plan.kernel_name(2, dtype)}
         for kind, f in ((0, plan.forward), (1, plan.inverse), (2, plan.dense_forward), (3, plan.dense_inverse)):
-            row[KIND_NAMES[kind]] = rec(time_kernel(lambda: f(X, Y, stream), stream, 3, args.table_iters),
-                                        nbytes, hbm, cfg.batch)
+            row[KIND_NAMES[kind]] = rec(tk(lambda: f(X, Y, stream)), nbytes, hbm, cfg.batch)
         if cfg.batch * cfg.n * X.element_size() <= (64 << 20):   # launch-bound: replay a graph
             row["fast_fwd"]["graph_ms"] = round(time_graph(lambda: plan.forward(X, Y), 50), 5)
             Z1 = torch.empty_like(X)
@@ -231,29 +261,27 @@ def config_table(args, stream, hbm, device, peaks):
         row["dense_fwd"]["fma_frac"] = round(2.0 * cfg.n * cfg.n * cfg.batch / (row["dense_fwd"]["ms"] * 1e-3) / pk, 4)
         row["fast_vs_dense_fwd"] = round(row["dense_fwd"]["ms"] / row["fast_fwd"]["ms"], 3)
         filt = gft.Filter(plan, np.exp(-plan.eigenvalues()), dtypes=(dtype,))
-        ms = time_kernel(lambda: filt.apply(X, Y, stream), stream, 3, args.table_iters)
-        row["filter"] = dict(rec(ms, nbytes, hbm, cfg.batch), kernel=filt.kernel_name(dtype))
-        row["fused_filter_vs_two_pass"] = round((row["fast_fwd"]["ms"] + row["fast_inv"]["ms"]) / ms, 3)
+        row["filter"] = dict(rec(tk(lambda: filt.apply(X, Y, stream)), nbytes, hbm, cfg.batch), kernel=filt.kernel_name(dtype))
+        row["fused_filter_vs_two_pass"] = round((row["fast_fwd"]["ms"] + row["fast_inv"]["ms"]) / row["filter"]["ms"], 3)
         U = torch.from_numpy(plan.basis()).to(device=device, dtype=tdt)
         tf32 = torch.backends.cuda.matmul.allow_tf32
         torch.backends.cuda.matmul.allow_tf32 = False
-        ms = time_kernel(lambda: torch.matmul(X, U, out=Y), stream, 3, args.table_iters)
+        row["cublas_fwd"] = rec(tk(lambda: torch.matmul(X, U, out=Y)), nbytes, hbm, cfg.batch)
         torch.backends.cuda.matmul.allow_tf32 = tf32
-        row["cublas_fwd"] = rec(ms, nbytes, hbm, cfg.batch)
-        best = min(row["dense_fwd"]["ms"], ms)
+        best = min(row["dense_fwd"]["ms"], row["cublas_fwd"]["ms"])
         if dtype == "f32" and cfg.n % 32 == 0:
             dplan = gft.Plan.from_config(cfg, dtypes=(dtype,), dense_tc=True)
-            ms = time_kernel(lambda: dplan.dense_forward(X, Y, stream), stream, 3, args.table_iters)
-            row["dense_tc_fwd"] = dict(rec(ms, nbytes, hbm, cfg.batch), kernel=dplan.kernel_name(2, dtype))
-            best = min(best, ms)
+            row["dense_tc_fwd"] = dict(rec(tk(lambda: dplan.dense_forward(X, Y, stream)), nbytes, hbm, cfg.batch),
+                                       kernel=dplan.kernel_name(2, dtype))
+            best = min(best, row["dense_tc_fwd"]["ms"])
             dplan.close()
         row["fast_vs_best_dense_fwd"] = round(best / row["fast_fwd"]["ms"], 3)
         if args.tune and cfg.batch * cfg.n * X.element_size() > (64 << 20):
             ch = plan.tune(dtype, (0, 1), X, Y, stream=stream, geometry=True)
             for kind, f in ((0, plan.forward), (1, plan.inverse)):
                 if kind in ch:
-                    ms = time_kernel(lambda: f(X, Y, stream), stream, 3, args.table_iters)
-                    row[KIND_NAMES[kind] + "_tuned"] = dict(rec(ms, nbytes, hbm, cfg.batch), geometry_pace=ch[kind])
+                    row[KIND_NAMES[kind] + "_tuned"] = dict(rec(tk(lambda: f(X, Y, stream)), nbytes, hbm, cfg.batch),
+                                                            geometry_pace=ch[kind])
         rows.append(row)
         del X, Y
         filt.close()
@@ -416,7 +444,7 @@ def right_haar_table(args, stream, hbm, device):
             r = {"leaves": plan.leaf_sizes(), "pairs": info["n_right_pairs"], "mults": info["mults"],
                  "adds": info["adds"], "kernel": plan.kernel_name(0, dtype)}
             for k, f in ((0, plan.forward), (1, plan.inverse)):
-                r[KIND_NAMES[k]] = rec(time_kernel(lambda: f(X, Y, stream), stream, 3, args.table_iters),
+                r[KIND_NAMES[k]] = rec(time_kernel_stats(lambda: f(X, Y, stream), stream, 5, 5, max(10, args.table_iters // 2)),
                                        nbytes, hbm, batch)
             row[tag] = r
             plan.close()
