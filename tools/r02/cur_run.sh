@@ -1,7 +1,6 @@
-# r81: final validation after cfg2 moved to the sustained-regime geometry (GPU suite, smoke, driver bench, reference arm, side tables)
+# r82: cfg1 @ 2^24 on this box: table (8/3/3/150/2) vs 8 warps, fwd-only and pair streams, both regimes
 mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r81_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r81_pytest.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r81_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r81_smoke.log
-timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/r81_bench.log 2> gpurun_out/r81_bench.err
-timeout 600 python bench.py --impl reference --gpus 1 --steps 3 --warmup 3 > gpurun_out/r81_ref.log 2>&1
-timeout 1800 python bench.py --gpus 1 --steps 20 --warmup 5 --tables gpurun_out/r81_tables.json > gpurun_out/r81_bench_tables.log 2>&1
+L=gpurun_out/r82_cfg1.log; nvidia-smi --query-gpu=uuid --format=csv,noheader > $L
+for M in fwd pair; do
+SWEEP_MODE=$M SWEEP_BATCH=16777216 python tools/r02/regime_sweep.py cfg1 f32 copy default 8,2,8,150,0 8,3,4,0,0 8,2,8,0,0 >> $L 2>&1
+done
